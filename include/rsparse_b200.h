@@ -1,0 +1,204 @@
+/*
+ * rsparse_b200.h -- C ABI of the B200-native R-Sparse linear operator.
+ *
+ * This is the drop-in boundary for the reference's operator API
+ * (namespace rsparse, /root/reference/proj/core/include/rsparse/layer.hpp,
+ * sparsity.hpp, matrix.hpp, search.hpp).  Each entry point names the
+ * reference interface it replaces.  Plain C types only: pointers, sizes and
+ * enums -- no torch or C++ types cross this line.  Device pointers are CUDA
+ * device addresses on the handle's device; `stream` is a cudaStream_t passed
+ * as void*.
+ *
+ * Errors: every call returns rsp_status.  The codes mirror the reference
+ * exception taxonomy (include/rsparse/errors.hpp:8-22): usage_error ->
+ * RSP_E_USAGE, numeric_error -> RSP_E_NUMERIC, io_error -> RSP_E_IO; CUDA
+ * failures are RSP_E_CUDA.  rsp_last_error() returns the message of the
+ * calling thread's last failure.
+ *
+ * Threading: a handle is immutable after rsp_linear_create (like a
+ * DecomposedLayer, layer.hpp:38-48).  rsp_linear_forward is re-entrant
+ * across streams when each concurrent call passes its own workspace
+ * (SPEC.md:331 allows concurrent forward calls).  rsp_linear_forward_host
+ * uses per-handle staging buffers and is NOT re-entrant on one handle.
+ */
+#ifndef RSPARSE_B200_H_
+#define RSPARSE_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RSP_ABI_VERSION 1
+
+typedef enum rsp_status {
+  RSP_OK = 0,
+  RSP_E_NUMERIC = 1, /* rsparse::numeric_error */
+  RSP_E_USAGE = 2,   /* rsparse::usage_error   */
+  RSP_E_IO = 3,      /* rsparse::io_error      */
+  RSP_E_CUDA = 4,    /* CUDA runtime failure   */
+  RSP_E_UNSUPPORTED = 5
+} rsp_status;
+
+typedef enum rsp_dtype { RSP_F32 = 0, RSP_BF16 = 1, RSP_F64 = 2 } rsp_dtype;
+
+typedef enum rsp_memory { RSP_MEM_HOST = 0, RSP_MEM_DEVICE = 1 } rsp_memory;
+
+/* Layout of desc.w.  ROW_MAJOR is rsparse::Matrix (m_out x m_in, matrix.hpp:13-46);
+ * COL_MAJOR is rsparse::ColMajorMatrix::data (data[j*m_out+i] == W(i,j),
+ * layer.hpp:20-27), i.e. DecomposedLayer::w_cols. */
+typedef enum rsp_w_layout { RSP_W_ROW_MAJOR = 0, RSP_W_COL_MAJOR = 1 } rsp_w_layout;
+
+typedef struct rsp_linear rsp_linear;
+
+/* Everything a rsparse::DecomposedLayer holds (layer.hpp:38-48):
+ * W, a_r = U_r sqrt(Sigma_r) (m_out x r row-major), b_r = sqrt(Sigma_r) Vt_r
+ * (r x m_in row-major), and its SparsityPlan {keep_fraction, rank}
+ * (sparsity.hpp:34-39). */
+typedef struct rsp_linear_desc {
+  uint32_t m_in;
+  uint32_t m_out;
+  uint32_t rank;
+  double keep_fraction;     /* s in [0,1]; k = ceil(s * m_in) exactly as sparsity.cpp:26-27 */
+  int64_t k_override;       /* < 0: use keep_fraction; else explicit k (0..m_in) */
+  rsp_dtype weight_dtype;   /* device storage of W, a_r, b_r: RSP_F32 or RSP_BF16 */
+  rsp_dtype src_dtype;      /* dtype of the w / a_r / b_r arrays: F64, F32 or BF16 */
+  rsp_memory src_memory;    /* where w / a_r / b_r live */
+  rsp_w_layout w_layout;
+  const void* w;
+  const void* a_r;          /* may be NULL when rank == 0 */
+  const void* b_r;          /* may be NULL when rank == 0 */
+  int device;               /* CUDA ordinal */
+  uint32_t shard_rank;      /* output-row sharding: this handle owns rows   */
+  uint32_t shard_count;     /* [m_out*rank/count, m_out*(rank+1)/count)     */
+} rsp_linear_desc;
+
+typedef struct rsp_linear_info {
+  uint32_t m_in, m_out, rank, k;
+  uint32_t row_begin, row_end; /* output rows owned by this shard */
+  uint32_t m_pad, r_pad;       /* padded device widths (multiples of 8) */
+  uint32_t col_tiles, k_splits, grid; /* fused-kernel decomposition */
+  uint32_t smem_bytes;
+  rsp_dtype weight_dtype;
+  uint64_t device_bytes;       /* weights + factors resident in HBM */
+} rsp_linear_info;
+
+/* io_cost (layer.cpp:125-140) plus the bytes the B200 kernel actually moves. */
+typedef struct rsp_io_report {
+  uint64_t dense_bytes;        /* reference: m_in*m_out*4 */
+  uint64_t touched_bytes;      /* reference: (ceil(s*n)*m + r*(m+n))*4 */
+  double relative_cost;        /* reference: r(m+n)/(mn) + s */
+  uint64_t kernel_weight_bytes;/* elem*(k*m + (n-k)*r + r*m), this shard, padded widths */
+  uint64_t kernel_total_bytes; /* + x, y, partial-sum traffic */
+  uint64_t dense_weight_bytes; /* elem*m*n of this shard (dense GEMV of the same layer) */
+} rsp_io_report;
+
+/* -- library ------------------------------------------------------------ */
+int rsp_abi_version(void);
+const char* rsp_last_error(void);
+
+/* -- plan helpers -------------------------------------------------------- */
+/* k = ceil(s * n) evaluated in double (sparsity.cpp:26-27, layer.cpp:129-130). */
+rsp_status rsp_keep_count(double keep_fraction, uint32_t n, uint32_t* k_out);
+/* Recipe::plan_for for one layer (search.cpp:14-25, search.hpp:24):
+ * s = rho*budget, r = clamp(llround((1-rho)*budget*m*n/(m+n)), 0, min(m,n)). */
+rsp_status rsp_plan_for(double rho, double budget, uint32_t m_in, uint32_t m_out,
+                        double* keep_fraction, uint32_t* rank);
+
+/* Output rows [*begin, *end) owned by shard `shard_rank` of `shard_count`
+ * (the row partition rsp_linear_create applies; host-only, no device). */
+rsp_status rsp_shard_rows(uint32_t m_out, uint32_t shard_rank, uint32_t shard_count,
+                          uint32_t* begin, uint32_t* end);
+
+/* -- operator -------------------------------------------------------------- */
+/* Replaces building a rsparse::DecomposedLayer (decompose_with_svd,
+ * layer.cpp:35-68, with the factors precomputed on the host).  Uploads W in
+ * input-channel-major layout Wt[m_in][m_pad], A_r^T[r][m_pad], B_r^T[m_in][r_pad]. */
+rsp_status rsp_linear_create(const rsp_linear_desc* desc, rsp_linear** out);
+void rsp_linear_destroy(rsp_linear* h);
+rsp_status rsp_linear_info_get(const rsp_linear* h, rsp_linear_info* out);
+
+/* Bytes of scratch one in-flight forward needs (partial sums + barriers).
+ * The buffer must be zeroed once before first use (rsp_workspace_init). */
+size_t rsp_linear_workspace_size(const rsp_linear* h, uint32_t batch);
+rsp_status rsp_workspace_init(void* workspace, size_t bytes, void* stream);
+
+/* Replaces rsparse::forward(const DecomposedLayer&, span<const double> x)
+ * (layer.hpp:75, layer.cpp:95-123).  x_dev: batch x m_in (x_dtype F32/BF16);
+ * y_dev: batch x (row_end-row_begin) fp32.  One fused kernel: selection,
+ * gathered-row GEMV and the two-stage low-rank term.  batch must be 1 in
+ * ABI v1 (batch > 1 tokens are run as independent per-token forwards, which
+ * is the reference semantics). */
+rsp_status rsp_linear_forward(const rsp_linear* h, const void* x_dev, rsp_dtype x_dtype,
+                              float* y_dev, uint32_t batch, void* workspace,
+                              size_t workspace_bytes, void* stream);
+
+/* Host-buffer convenience (the end-to-end path): copies x (host) to the
+ * device, runs rsp_linear_forward on the handle's internal stream, copies y
+ * back and synchronises.  y_host is fp32 (or fp64 when y_dtype == RSP_F64). */
+rsp_status rsp_linear_forward_host(rsp_linear* h, const void* x_host, rsp_dtype x_dtype,
+                                   void* y_host, rsp_dtype y_dtype, uint32_t batch);
+
+/* Dense baseline of the same layer: y = W x over all m_in channels with the
+ * same streaming kernel (k = m_in, no low-rank term).  Reference analogue:
+ * the dense sweep of bench_matvec (layer.cpp:142-210) / matvec (matrix.cpp:66-79). */
+rsp_status rsp_linear_dense_forward(const rsp_linear* h, const void* x_dev, rsp_dtype x_dtype,
+                                    float* y_dev, void* workspace, size_t workspace_bytes,
+                                    void* stream);
+
+/* Replaces rsparse::gather_matvec(w_cols, x, kept, touched_bytes)
+ * (layer.hpp:69-71, layer.cpp:74-93).  kept_host: nkept indices in
+ * accumulation order (validated on the host: out-of-range -> RSP_E_USAGE).
+ * Adds nkept*m_out*4 to *touched_bytes when non-NULL (layer.cpp:91). */
+rsp_status rsp_gather_matvec(const rsp_linear* h, const void* x_dev, rsp_dtype x_dtype,
+                             const int64_t* kept_host, uint32_t nkept, float* y_dev,
+                             uint64_t* touched_bytes, void* stream);
+
+/* The channel set forward() selects for x (debug/parity): S ascending into
+ * S_host (capacity m_in), *k_out = |S|.  Synchronous. */
+rsp_status rsp_linear_selected(const rsp_linear* h, const void* x_dev, rsp_dtype x_dtype,
+                               int32_t* S_host, uint32_t* k_out);
+
+/* io_cost (layer.hpp:77, layer.cpp:125-140) plus kernel byte counts. */
+rsp_status rsp_linear_io_cost(const rsp_linear* h, rsp_io_report* out);
+
+/* Copy the device-resident operands back as row-major float64
+ * (which: 0 = W m_shard x m_in, 1 = a_r m_shard x r, 2 = b_r r x m_in) so a
+ * checker can run on exactly the values the kernels read.  Synchronous. */
+rsp_status rsp_linear_export(const rsp_linear* h, int which, double* out_host);
+
+/* -- selector ---------------------------------------------------------------- */
+/* Replaces top_k_by_magnitude(span<const double> x, size_t k) (matrix.hpp:63,
+ * matrix.cpp:100-117): indices of the k largest |x|, ties to the lower index,
+ * ascending.  kept_dev receives k int32 indices; rest_dev (may be NULL)
+ * receives the n-k complement indices ascending.  k > n -> RSP_E_USAGE. */
+rsp_status rsp_top_k_by_magnitude(const void* x_dev, rsp_dtype x_dtype, uint32_t n, uint32_t k,
+                                  int32_t* kept_dev, int32_t* rest_dev, void* stream);
+
+/* Replaces threshold_sparsify(x, s) (sparsity.hpp:43-44, sparsity.cpp:20-32):
+ * k = ceil(s*n); sparse_x_dev (fp32, n) = x on the kept set, 0 elsewhere;
+ * kept_dev (capacity n) ascending; *k_out = k.  s outside [0,1] -> RSP_E_USAGE. */
+rsp_status rsp_threshold_sparsify(const void* x_dev, rsp_dtype x_dtype, uint32_t n,
+                                  double keep_fraction, float* sparse_x_dev, int32_t* kept_dev,
+                                  uint32_t* k_out, void* stream);
+
+/* -- stack executor ----------------------------------------------------------- */
+/* A sequence of forwards captured once into a CUDA graph (decode: linear
+ * i+1 runs after linear i).  x_devs[i] / y_devs[i] are bound at creation. */
+typedef struct rsp_stack rsp_stack;
+rsp_status rsp_stack_create(const rsp_linear* const* layers, uint32_t count,
+                            const void* const* x_devs, rsp_dtype x_dtype, float* const* y_devs,
+                            int dense, rsp_stack** out);
+rsp_status rsp_stack_launch(rsp_stack* s, void* stream);
+void rsp_stack_destroy(rsp_stack* s);
+
+/* -- device helpers ------------------------------------------------------------- */
+int rsp_device_sm_count(int device);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RSPARSE_B200_H_ */

@@ -1,0 +1,223 @@
+// ref_shim.cpp -- extern "C" access to the UNMODIFIED reference library.
+//
+// TEST INFRASTRUCTURE ONLY.  Compiled together with the reference's own
+// sources, in place under /root/reference/proj/core/src, by oracle/Makefile
+// into oracle/_ref/librsparse_ref.so.  Used to (1) pin the C restatement
+// oracle/rsparse_oracle.c, (2) generate the golden fixtures under
+// tests/golden/, and (3) time the reference CPU path for bench.py's
+// cpu_baseline and `--impl reference` arms.  Never linked by the product.
+//
+// Nothing here re-implements reference logic: every entry point forwards to
+// the reference function named in its comment.
+#include <cstdint>
+#include <cstring>
+#include <atomic>
+#include <exception>
+#include <span>
+#include <thread>
+#include <vector>
+
+#include "rsparse/errors.hpp"
+#include "rsparse/layer.hpp"
+#include "rsparse/matrix.hpp"
+#include "rsparse/rng.hpp"
+#include "rsparse/scores.hpp"
+#include "rsparse/search.hpp"
+#include "rsparse/sparsity.hpp"
+#include "rsparse/svd.hpp"
+
+using namespace rsparse;
+
+namespace {
+
+int status_of(const std::exception_ptr& e) {
+  try {
+    std::rethrow_exception(e);
+  } catch (const usage_error&) {
+    return 2;
+  } catch (const numeric_error&) {
+    return 1;
+  } catch (const io_error&) {
+    return 3;
+  } catch (...) {
+    return 5;
+  }
+}
+
+#define GUARD(...)                           \
+  try {                                      \
+    __VA_ARGS__;                             \
+    return 0;                                \
+  } catch (...) {                            \
+    return status_of(std::current_exception()); \
+  }
+
+}  // namespace
+
+extern "C" {
+
+// rng.hpp:18-24
+uint64_t rspr_derive_seed(uint64_t root, const char* tag) { return derive_seed(root, tag); }
+
+// tests/unit/test_helpers.hpp:12-27 semantics: one Rng(seed), count normal(0, sigma) draws
+void rspr_fill_normal(uint64_t seed, double mean, double stddev, double* out, size_t count) {
+  Rng rng(seed);
+  for (size_t i = 0; i < count; ++i) out[i] = rng.normal(mean, stddev);
+}
+
+void rspr_fill_uniform01(uint64_t seed, double* out, size_t count) {
+  Rng rng(seed);
+  for (size_t i = 0; i < count; ++i) out[i] = rng.uniform01();
+}
+
+// matrix.cpp:100-117
+int rspr_top_k_by_magnitude(const double* x, size_t n, size_t k, int64_t* out) {
+  GUARD({
+    auto idx = top_k_by_magnitude(std::span<const double>(x, n), k);
+    for (size_t i = 0; i < idx.size(); ++i) out[i] = static_cast<int64_t>(idx[i]);
+  })
+}
+
+// sparsity.cpp:20-32
+int rspr_threshold_sparsify(const double* x, size_t n, double s, double* sparse_x, int64_t* kept,
+                            size_t* k_out) {
+  GUARD({
+    auto [sx, idx] = threshold_sparsify(std::span<const double>(x, n), s);
+    std::memcpy(sparse_x, sx.data(), n * sizeof(double));
+    for (size_t i = 0; i < idx.size(); ++i) kept[i] = static_cast<int64_t>(idx[i]);
+    *k_out = idx.size();
+  })
+}
+
+// layer.cpp:74-93; w_cols is column-major (data[j*m+i] = W(i,j))
+int rspr_gather_matvec(const double* w_cols, size_t m_out, size_t m_in, const double* x,
+                       const int64_t* kept, size_t nkept, double* y, uint64_t* touched) {
+  GUARD({
+    ColMajorMatrix cm;
+    cm.rows = m_out;
+    cm.cols = m_in;
+    cm.data.assign(w_cols, w_cols + m_out * m_in);
+    std::vector<size_t> k(kept, kept + nkept);
+    auto out = gather_matvec(cm, std::span<const double>(x, m_in), k, touched);
+    std::memcpy(y, out.data(), m_out * sizeof(double));
+  })
+}
+
+// matrix.cpp:66-79
+int rspr_matvec(const double* w, size_t rows, size_t cols, const double* x, double* y) {
+  GUARD({
+    Matrix m(rows, cols, std::vector<double>(w, w + rows * cols));
+    auto out = matvec(m, std::span<const double>(x, cols));
+    std::memcpy(y, out.data(), rows * sizeof(double));
+  })
+}
+
+// A DecomposedLayer (layer.hpp:38-48) assembled from host arrays: w_cols
+// column-major m_out x m_in, a_r m_out x r row-major, b_r r x m_in row-major.
+void* rspr_layer_create(size_t m_in, size_t m_out, size_t rank, double keep_fraction,
+                        const double* w_cols, const double* a_r, const double* b_r) {
+  try {
+    auto* L = new DecomposedLayer();
+    L->m_in = m_in;
+    L->m_out = m_out;
+    L->w_cols.rows = m_out;
+    L->w_cols.cols = m_in;
+    L->w_cols.data.assign(w_cols, w_cols + m_in * m_out);
+    L->a_r = Matrix(m_out, rank, std::vector<double>(a_r, a_r + m_out * rank));
+    L->b_r = Matrix(rank, m_in, std::vector<double>(b_r, b_r + rank * m_in));
+    L->plan = SparsityPlan{keep_fraction, rank};
+    L->selected_components.resize(rank);
+    for (size_t c = 0; c < rank; ++c) L->selected_components[c] = c;
+    return L;
+  } catch (...) {
+    return nullptr;
+  }
+}
+
+void rspr_layer_destroy(void* h) { delete static_cast<DecomposedLayer*>(h); }
+
+// layer.cpp:95-123
+int rspr_layer_forward(const void* h, const double* x, double* y) {
+  GUARD({
+    const auto* L = static_cast<const DecomposedLayer*>(h);
+    auto out = forward(*L, std::span<const double>(x, L->m_in));
+    std::memcpy(y, out.data(), L->m_out * sizeof(double));
+  })
+}
+
+// Independent forwards over `threads` std::threads (SPEC.md:331 allows
+// concurrent forward calls on immutable layers).  Item i runs
+// forward(*layers[i], xs[i]) into ys[i].
+int rspr_forward_many(const void* const* layers, const double* const* xs, double* const* ys,
+                      size_t count, int threads) {
+  if (threads < 1) threads = 1;
+  std::atomic<size_t> next{0};
+  std::atomic<int> err{0};
+  auto work = [&]() {
+    for (;;) {
+      const size_t i = next.fetch_add(1);
+      if (i >= count) break;
+      if (int st = rspr_layer_forward(layers[i], xs[i], ys[i])) err = st;
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t) pool.emplace_back(work);
+  for (auto& t : pool) t.join();
+  return err.load();
+}
+
+// layer.cpp:125-140
+void rspr_io_cost(size_t m_in, size_t m_out, double keep_fraction, size_t rank,
+                  uint64_t* dense_bytes, uint64_t* touched_bytes, double* relative_cost) {
+  DecomposedLayer L;
+  L.m_in = m_in;
+  L.m_out = m_out;
+  L.plan = SparsityPlan{keep_fraction, rank};
+  const IoReport r = io_cost(L);
+  *dense_bytes = r.dense_bytes;
+  *touched_bytes = r.touched_bytes;
+  *relative_cost = r.relative_cost;
+}
+
+// search.cpp:14-25
+void rspr_plan_for(double rho, double budget, size_t m_in, size_t m_out, double* keep_fraction,
+                   size_t* rank) {
+  Recipe rec;
+  rec.rho = {rho};
+  rec.budget = {budget};
+  const SparsityPlan p = rec.plan_for(0, m_in, m_out);
+  *keep_fraction = p.keep_fraction;
+  *rank = p.rank;
+}
+
+// layer.cpp:35-72 with a uniform score (test_layer.cpp:19-22), i.e. the
+// reference's own Jacobi SVD truncated to `rank` components.  Small shapes
+// only (the Jacobi SVD is O(m n^2) per sweep).  Outputs a_r (m x r),
+// b_r (r x n) and the selected components (r).
+int rspr_decompose_uniform(const double* w, size_t m_out, size_t m_in, double keep_fraction,
+                           size_t rank, double* a_r, double* b_r, int64_t* comps) {
+  GUARD({
+    Matrix W(m_out, m_in, std::vector<double>(w, w + m_out * m_in));
+    const size_t kc = std::min(m_out, m_in);
+    ScoreMatrix sc{Matrix(kc, m_in, std::vector<double>(kc * m_in, 1.0)), 1, ""};
+    const DecomposedLayer L = decompose(W, SparsityPlan{keep_fraction, rank}, sc);
+    std::memcpy(a_r, L.a_r.data(), m_out * rank * sizeof(double));
+    std::memcpy(b_r, L.b_r.data(), rank * m_in * sizeof(double));
+    for (size_t c = 0; c < rank; ++c) comps[c] = static_cast<int64_t>(L.selected_components[c]);
+  })
+}
+
+// layer.cpp:161-210 (the reference's own fp32 timing harness)
+int rspr_bench_matvec(size_t m_in, size_t m_out, double s, size_t reps, uint64_t seed,
+                      double* dense_ns, double* gather_ns, uint64_t* dense_bytes,
+                      uint64_t* touched_bytes) {
+  GUARD({
+    const BenchReport r = bench_matvec(m_in, m_out, s, reps, seed);
+    *dense_ns = r.dense_ns_median;
+    *gather_ns = r.gather_ns_median;
+    *dense_bytes = r.dense_bytes;
+    *touched_bytes = r.touched_bytes;
+  })
+}
+
+}  // extern "C"

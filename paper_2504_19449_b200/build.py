@@ -1,0 +1,46 @@
+"""Build the sm_100a library in-tree (nvcc cross-compiles; no GPU needed).
+
+    python -m paper_2504_19449_b200.build
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+LIB = os.path.join(PKG, "librsparse_b200.so")
+SOURCES = ["rsp_kernels.cu", "rsp_api.cu"]
+HEADERS = ["rsp_device.cuh", "rsp_internal.h"]
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+         "-Xptxas", "-v", f"-I{os.path.join(ROOT, 'include')}"]
+
+
+def _stale(target: str, deps) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
+    deps.append(os.path.join(ROOT, "include", "rsparse_b200.h"))
+    if force or _stale(LIB, deps):
+        cmd = [NVCC, *ARCH, *FLAGS, *[os.path.join(CSRC, f) for f in SOURCES], "-o", LIB]
+        out = subprocess.run(cmd, capture_output=True, text=True)
+        if out.returncode != 0:
+            raise RuntimeError("nvcc failed:\n" + out.stdout + out.stderr)
+        with open(os.path.join(PKG, "ptxas_info.txt"), "w") as f:
+            f.write(out.stderr)
+        if verbose:
+            print(out.stderr, file=sys.stderr)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose=True))

@@ -1,0 +1,700 @@
+// rsp_api.cu -- the C ABI (include/rsparse_b200.h) over the sm_100a kernels.
+//
+// Host-side responsibilities: validate arguments exactly where the reference
+// throws (layer.cpp:96-99, sparsity.cpp:22-25, matrix.cpp:101-104,
+// layer.cpp:83-86, layer.cpp:40-49), upload the operator in the B200 layout,
+// plan the fused kernel's decomposition for this GPU, and capture stacks of
+// forwards into CUDA graphs.  There is no CPU compute fallback: every
+// numeric result comes from a kernel in rsp_kernels.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/rsparse_b200.h"
+#include "rsp_internal.h"
+
+using rsp::FusedParams;
+using rsp::LaunchPlan;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+rsp_status fail(rsp_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return st;
+}
+
+#define RSP_CUDA(call)                                                                    \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(RSP_E_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                    \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+struct DevProps {
+  int sms = 0;
+  int smem_optin = 0;
+};
+
+DevProps device_props(int dev) {
+  static std::mutex mu;
+  static std::vector<DevProps> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev >= static_cast<int>(cache.size())) cache.resize(dev + 1);
+  if (cache[dev].sms == 0) {
+    cudaDeviceGetAttribute(&cache[dev].sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&cache[dev].smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  }
+  return cache[dev];
+}
+
+bool env_flag(const char* name, bool dflt) {
+  const char* v = std::getenv(name);
+  if (!v || !*v) return dflt;
+  return !(v[0] == '0' || v[0] == 'n' || v[0] == 'N' || v[0] == 'f' || v[0] == 'F');
+}
+
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return (v && *v) ? std::atoi(v) : dflt;
+}
+
+size_t dtype_size(rsp_dtype d) { return d == RSP_F64 ? 8 : (d == RSP_F32 ? 4 : 2); }
+
+uint32_t round_up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
+
+constexpr int kMaxN = 32768;  // selection keeps x in shared memory
+
+// k = ceil(s * n) in double (sparsity.cpp:26-27).
+uint32_t keep_count(double s, uint32_t n) {
+  return static_cast<uint32_t>(std::ceil(s * static_cast<double>(n)));
+}
+
+}  // namespace
+
+struct rsp_linear {
+  int device = 0;
+  uint32_t m_in = 0, m_out = 0, rank = 0, k = 0;
+  double keep_fraction = 1.0;
+  uint32_t row_begin = 0, row_end = 0, m = 0, m_pad = 0, r_pad = 0;
+  rsp_dtype wdt = RSP_BF16;
+  int es = 2;
+  void* Wt = nullptr;
+  void* At = nullptr;
+  void* Bt = nullptr;
+  LaunchPlan plan;
+  bool pdl = true;
+  // forward_host staging (lazily created)
+  cudaStream_t stream = nullptr;
+  void* x_dev = nullptr;
+  float* y_dev = nullptr;
+  void* ws = nullptr;
+  void* x_pin = nullptr;
+  float* y_pin = nullptr;
+  uint32_t host_batch = 0;
+};
+
+struct rsp_stack {
+  int device = 0;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  void* ws = nullptr;
+};
+
+namespace {
+
+// Decompose one forward over the GPU: col_tiles column tiles x k_splits
+// K-splits, one CTA per SM.  Column tiles target ~2 KB contiguous row
+// segments (one bulk copy each) and never exceed 15 x 512 B (one 16-byte
+// vector per consumer lane).
+rsp_status make_plan(const rsp_linear& L, const DevProps& dp, LaunchPlan* out) {
+  LaunchPlan p;
+  const uint32_t n = L.m_in, vm = L.m_pad / 8;
+  const uint32_t row_bytes = L.m_pad * L.es;
+  const int stage_bytes = env_int("RSP_STAGE_BYTES", 16384);
+  int nt = std::max(1, static_cast<int>(std::lround(row_bytes / static_cast<double>(
+                                                        env_int("RSP_SEG_BYTES", 2048)))));
+  nt = std::max(nt, static_cast<int>((row_bytes + 7679) / 7680));
+  nt = std::max(nt, static_cast<int>((row_bytes + stage_bytes - 1) / stage_bytes));
+  nt = std::min<int>(nt, static_cast<int>(vm));
+  nt = std::min(nt, dp.sms);
+  int ks = std::max(1, dp.sms / nt);
+  // Small layers: keep >= ~32 KB of streamed bytes per CTA.
+  const double bytes = static_cast<double>(L.k + L.rank) * row_bytes +
+                       static_cast<double>(n - L.k) * L.r_pad * L.es;
+  const int want = std::max(1, static_cast<int>(std::ceil(bytes / 32768.0)));
+  ks = std::min(ks, std::max(1, (want + nt - 1) / nt));
+  p.col_tiles = nt;
+  p.k_splits = ks;
+  p.grid = nt * ks;
+  p.cap_w = static_cast<int>((n + ks - 1) / ks) + 1;  // covers the dense sweep too
+  p.cap_u = static_cast<int>((n - L.k + p.grid - 1) / p.grid) + 1;
+  p.cap_a = static_cast<int>((L.rank + ks - 1) / ks) + 1;
+  p.stage_bytes = stage_bytes;
+  if (static_cast<int>(L.r_pad * L.es) > stage_bytes)
+    return fail(RSP_E_UNSUPPORTED, "rank %u too large for the %d-byte ring stage", L.rank,
+                stage_bytes);
+  if (static_cast<int>(L.r_pad * L.es) > 15 * 512)
+    return fail(RSP_E_UNSUPPORTED, "rank %u exceeds the consumer width", L.rank);
+  p.stages = env_int("RSP_STAGES", 8);
+  size_t smem = rsp::fused_smem_bytes(p, static_cast<int>(n), L.es);
+  while (smem > static_cast<size_t>(dp.smem_optin) && p.stages > 2) {
+    --p.stages;
+    smem = rsp::fused_smem_bytes(p, static_cast<int>(n), L.es);
+  }
+  if (smem > static_cast<size_t>(dp.smem_optin))
+    return fail(RSP_E_UNSUPPORTED, "fused kernel needs %zu B shared memory (> %d)", smem,
+                dp.smem_optin);
+  p.smem = smem;
+  const size_t bars = round_up(4u * (2u + 2u * nt), 256u);
+  p.ws_t_off = bars;
+  p.ws_y_off = p.ws_t_off + round_up(4u * static_cast<uint32_t>(p.grid) * std::max(L.r_pad, 8u), 256u);
+  p.ws_bytes = p.ws_y_off + static_cast<size_t>(4) * ks * L.m_pad;
+  *out = p;
+  return RSP_OK;
+}
+
+FusedParams fused_params(const rsp_linear* h, const void* x, rsp_dtype xdt, float* y, void* ws,
+                         bool dense) {
+  FusedParams p = {};
+  p.Wt = h->Wt;
+  p.At = h->At;
+  p.Bt = h->Bt;
+  p.x = x;
+  p.y = y;
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  p.bars = reinterpret_cast<unsigned*>(w);
+  p.t_part = reinterpret_cast<float*>(w + h->plan.ws_t_off);
+  p.y_part = reinterpret_cast<float*>(w + h->plan.ws_y_off);
+  p.n = static_cast<int>(h->m_in);
+  p.m = static_cast<int>(h->m);
+  p.m_pad = static_cast<int>(h->m_pad);
+  p.r = static_cast<int>(h->rank);
+  p.r_pad = static_cast<int>(h->r_pad);
+  p.k = dense ? static_cast<int>(h->m_in) : static_cast<int>(h->k);
+  p.col_tiles = h->plan.col_tiles;
+  p.k_splits = h->plan.k_splits;
+  p.cap_w = h->plan.cap_w;
+  p.cap_u = h->plan.cap_u;
+  p.cap_a = h->plan.cap_a;
+  p.stage_bytes = h->plan.stage_bytes;
+  p.stages = h->plan.stages;
+  p.x_bf16 = xdt == RSP_BF16 ? 1 : 0;
+  p.dense = dense ? 1 : 0;
+  return p;
+}
+
+rsp_status check_x_dtype(rsp_dtype d) {
+  if (d != RSP_F32 && d != RSP_BF16)
+    return fail(RSP_E_USAGE, "activation dtype must be RSP_F32 or RSP_BF16");
+  return RSP_OK;
+}
+
+rsp_status upload(const rsp_linear_desc* d, rsp_linear* h) {
+  const size_t sz = dtype_size(d->src_dtype);
+  const int sdt = d->src_dtype == RSP_F32 ? 0 : (d->src_dtype == RSP_BF16 ? 1 : 2);
+  const size_t n = h->m_in, mo = h->m_out, r = h->rank, m = h->m;
+  // Stage host sources on the device (in their own dtype) and convert there.
+  auto stage = [&](const void* src, size_t count, void** tmp) -> rsp_status {
+    *tmp = nullptr;
+    if (d->src_memory == RSP_MEM_DEVICE) return RSP_OK;
+    RSP_CUDA(cudaMalloc(tmp, std::max<size_t>(count * sz, 16)));
+    RSP_CUDA(cudaMemcpy(*tmp, src, count * sz, cudaMemcpyHostToDevice));
+    return RSP_OK;
+  };
+  auto src_of = [&](const void* host_or_dev, void* tmp) -> const uint8_t* {
+    return static_cast<const uint8_t*>(tmp ? tmp : host_or_dev);
+  };
+  const int de = h->es;
+  void* tmp = nullptr;
+  rsp_status st;
+  // W -> Wt[n][m_pad]
+  if ((st = stage(d->w, n * mo, &tmp))) return st;
+  {
+    const uint8_t* w = src_of(d->w, tmp);
+    cudaError_t e;
+    if (d->w_layout == RSP_W_ROW_MAJOR)
+      e = rsp::launch_convert(w + h->row_begin * n * sz, sdt, m, n, n, h->Wt, de, h->m_pad, true,
+                              nullptr);
+    else
+      e = rsp::launch_convert(w + h->row_begin * sz, sdt, n, m, mo, h->Wt, de, h->m_pad, false,
+                              nullptr);
+    cudaDeviceSynchronize();
+    if (tmp) cudaFree(tmp);
+    if (e != cudaSuccess) return fail(RSP_E_CUDA, "convert W: %s", cudaGetErrorString(e));
+  }
+  if (r > 0) {
+    // a_r (m_out x r) -> At[r][m_pad]
+    if ((st = stage(d->a_r, mo * r, &tmp))) return st;
+    cudaError_t e = rsp::launch_convert(src_of(d->a_r, tmp) + h->row_begin * r * sz, sdt, m, r, r,
+                                        h->At, de, h->m_pad, true, nullptr);
+    cudaDeviceSynchronize();
+    if (tmp) cudaFree(tmp);
+    if (e != cudaSuccess) return fail(RSP_E_CUDA, "convert a_r: %s", cudaGetErrorString(e));
+    // b_r (r x n) -> Bt[n][r_pad]
+    if ((st = stage(d->b_r, r * n, &tmp))) return st;
+    e = rsp::launch_convert(src_of(d->b_r, tmp), sdt, r, n, n, h->Bt, de, h->r_pad, true, nullptr);
+    cudaDeviceSynchronize();
+    if (tmp) cudaFree(tmp);
+    if (e != cudaSuccess) return fail(RSP_E_CUDA, "convert b_r: %s", cudaGetErrorString(e));
+  }
+  RSP_CUDA(cudaGetLastError());
+  return RSP_OK;
+}
+
+void free_linear(rsp_linear* h) {
+  if (!h) return;
+  DeviceGuard g(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  cudaFree(h->Wt);
+  cudaFree(h->At);
+  cudaFree(h->Bt);
+  cudaFree(h->x_dev);
+  cudaFree(h->y_dev);
+  cudaFree(h->ws);
+  cudaFreeHost(h->x_pin);
+  cudaFreeHost(h->y_pin);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+rsp_status launch_forward(const rsp_linear* h, const void* x, rsp_dtype xdt, float* y, void* ws,
+                          size_t ws_bytes, cudaStream_t stream, bool dense) {
+  if (!ws || ws_bytes < h->plan.ws_bytes)
+    return fail(RSP_E_USAGE, "workspace of %zu bytes is smaller than the %zu required", ws_bytes,
+                h->plan.ws_bytes);
+  const FusedParams p = fused_params(h, x, xdt, y, ws, dense);
+  cudaError_t e = rsp::launch_fused(p, h->es, h->plan.grid, h->plan.smem, stream, h->pdl);
+  if (e != cudaSuccess) return fail(RSP_E_CUDA, "fused forward launch: %s", cudaGetErrorString(e));
+  return RSP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rsp_abi_version(void) { return RSP_ABI_VERSION; }
+
+const char* rsp_last_error(void) { return g_last_error.c_str(); }
+
+int rsp_device_sm_count(int device) { return device_props(device).sms; }
+
+rsp_status rsp_keep_count(double keep_fraction, uint32_t n, uint32_t* k_out) {
+  if (!(keep_fraction >= 0.0 && keep_fraction <= 1.0))
+    return fail(RSP_E_USAGE, "keep_fraction must lie in [0, 1], got %f", keep_fraction);
+  *k_out = keep_count(keep_fraction, n);
+  return RSP_OK;
+}
+
+rsp_status rsp_plan_for(double rho, double budget, uint32_t m_in, uint32_t m_out,
+                        double* keep_fraction, uint32_t* rank) {
+  // search.cpp:14-25, search.hpp:24
+  const double m = static_cast<double>(m_out), n = static_cast<double>(m_in);
+  const double raw = (1.0 - rho) * budget * (m * n) / (m + n);
+  long long r = std::llround(raw);
+  const long long cap = static_cast<long long>(std::min(m_in, m_out));
+  r = std::clamp(r, 0LL, cap);
+  *keep_fraction = rho * budget;
+  *rank = static_cast<uint32_t>(r);
+  return RSP_OK;
+}
+
+rsp_status rsp_shard_rows(uint32_t m_out, uint32_t shard_rank, uint32_t shard_count, uint32_t* begin,
+                          uint32_t* end) {
+  const uint32_t sc = shard_count ? shard_count : 1;
+  if (shard_rank >= sc) return fail(RSP_E_USAGE, "shard_rank %u >= shard_count %u", shard_rank, sc);
+  *begin = static_cast<uint32_t>(static_cast<uint64_t>(m_out) * shard_rank / sc);
+  *end = static_cast<uint32_t>(static_cast<uint64_t>(m_out) * (shard_rank + 1) / sc);
+  return RSP_OK;
+}
+
+rsp_status rsp_linear_create(const rsp_linear_desc* d, rsp_linear** out) {
+  if (!d || !out) return fail(RSP_E_USAGE, "null descriptor or output");
+  *out = nullptr;
+  if (d->m_in == 0 || d->m_out == 0) return fail(RSP_E_USAGE, "m_in and m_out must be positive");
+  if (d->m_in > static_cast<uint32_t>(kMaxN))
+    return fail(RSP_E_UNSUPPORTED, "m_in %u exceeds %d", d->m_in, kMaxN);
+  if (d->rank > std::min(d->m_in, d->m_out))  // layer.cpp:40-44
+    return fail(RSP_E_USAGE, "decompose: rank %u exceeds min(m_in, m_out) = %u", d->rank,
+                std::min(d->m_in, d->m_out));
+  if (!(d->keep_fraction >= 0.0 && d->keep_fraction <= 1.0))  // sparsity.cpp:22-25
+    return fail(RSP_E_USAGE, "keep_fraction must lie in [0, 1], got %f", d->keep_fraction);
+  if (d->k_override > static_cast<int64_t>(d->m_in))  // matrix.cpp:101-104
+    return fail(RSP_E_USAGE, "top_k_by_magnitude: k=%lld exceeds vector length %u",
+                static_cast<long long>(d->k_override), d->m_in);
+  if (d->weight_dtype != RSP_F32 && d->weight_dtype != RSP_BF16)
+    return fail(RSP_E_USAGE, "weight_dtype must be RSP_F32 or RSP_BF16");
+  if (d->src_dtype != RSP_F32 && d->src_dtype != RSP_BF16 && d->src_dtype != RSP_F64)
+    return fail(RSP_E_USAGE, "src_dtype must be F32, BF16 or F64");
+  if (!d->w || (d->rank > 0 && (!d->a_r || !d->b_r)))
+    return fail(RSP_E_USAGE, "missing weight or factor pointer");
+  const uint32_t sc = d->shard_count ? d->shard_count : 1;
+  if (d->shard_rank >= sc) return fail(RSP_E_USAGE, "shard_rank %u >= shard_count %u", d->shard_rank, sc);
+
+  DeviceGuard g(d->device);
+  auto* h = new rsp_linear();
+  h->device = d->device;
+  h->m_in = d->m_in;
+  h->m_out = d->m_out;
+  h->rank = d->rank;
+  h->keep_fraction = d->keep_fraction;
+  h->k = d->k_override >= 0 ? static_cast<uint32_t>(d->k_override) : keep_count(d->keep_fraction, d->m_in);
+  rsp_shard_rows(d->m_out, d->shard_rank, sc, &h->row_begin, &h->row_end);
+  h->m = h->row_end - h->row_begin;
+  if (h->m == 0) {
+    delete h;
+    return fail(RSP_E_USAGE, "shard %u of %u owns no output rows", d->shard_rank, sc);
+  }
+  h->m_pad = round_up(h->m, 8);
+  h->r_pad = d->rank ? round_up(d->rank, 8) : 0;
+  h->wdt = d->weight_dtype;
+  h->es = d->weight_dtype == RSP_F32 ? 4 : 2;
+  h->pdl = env_flag("RSP_PDL", true);
+  const DevProps dp = device_props(d->device);
+  if (dp.sms == 0) {
+    delete h;
+    return fail(RSP_E_CUDA, "no CUDA device %d", d->device);
+  }
+  rsp_status st = make_plan(*h, dp, &h->plan);
+  if (st) {
+    delete h;
+    return st;
+  }
+  const size_t wbytes = static_cast<size_t>(h->m_in) * h->m_pad * h->es;
+  const size_t abytes = static_cast<size_t>(h->rank) * h->m_pad * h->es;
+  const size_t bbytes = static_cast<size_t>(h->m_in) * h->r_pad * h->es;
+  cudaError_t e = cudaMalloc(&h->Wt, wbytes);
+  if (e == cudaSuccess && abytes) e = cudaMalloc(&h->At, abytes);
+  if (e == cudaSuccess && bbytes) e = cudaMalloc(&h->Bt, bbytes);
+  if (e == cudaSuccess) e = cudaMemset(h->Wt, 0, wbytes);
+  if (e == cudaSuccess && abytes) e = cudaMemset(h->At, 0, abytes);
+  if (e == cudaSuccess && bbytes) e = cudaMemset(h->Bt, 0, bbytes);
+  if (e != cudaSuccess) {
+    free_linear(h);
+    return fail(RSP_E_CUDA, "allocating %zu B of operator storage: %s", wbytes + abytes + bbytes,
+                cudaGetErrorString(e));
+  }
+  st = upload(d, h);
+  if (st) {
+    free_linear(h);
+    return st;
+  }
+  e = rsp::fused_set_smem(h->es, h->plan.smem);
+  if (e != cudaSuccess) {
+    free_linear(h);
+    return fail(RSP_E_CUDA, "cudaFuncSetAttribute(smem=%zu): %s", h->plan.smem, cudaGetErrorString(e));
+  }
+  *out = h;
+  return RSP_OK;
+}
+
+void rsp_linear_destroy(rsp_linear* h) { free_linear(h); }
+
+rsp_status rsp_linear_info_get(const rsp_linear* h, rsp_linear_info* o) {
+  if (!h || !o) return fail(RSP_E_USAGE, "null handle");
+  o->m_in = h->m_in;
+  o->m_out = h->m_out;
+  o->rank = h->rank;
+  o->k = h->k;
+  o->row_begin = h->row_begin;
+  o->row_end = h->row_end;
+  o->m_pad = h->m_pad;
+  o->r_pad = h->r_pad;
+  o->col_tiles = static_cast<uint32_t>(h->plan.col_tiles);
+  o->k_splits = static_cast<uint32_t>(h->plan.k_splits);
+  o->grid = static_cast<uint32_t>(h->plan.grid);
+  o->smem_bytes = static_cast<uint32_t>(h->plan.smem);
+  o->weight_dtype = h->wdt;
+  o->device_bytes = (static_cast<uint64_t>(h->m_in) * h->m_pad + static_cast<uint64_t>(h->rank) * h->m_pad +
+                     static_cast<uint64_t>(h->m_in) * h->r_pad) * h->es;
+  return RSP_OK;
+}
+
+size_t rsp_linear_workspace_size(const rsp_linear* h, uint32_t /*batch*/) {
+  return h ? h->plan.ws_bytes : 0;
+}
+
+rsp_status rsp_workspace_init(void* ws, size_t bytes, void* stream) {
+  RSP_CUDA(cudaMemsetAsync(ws, 0, bytes, static_cast<cudaStream_t>(stream)));
+  return RSP_OK;
+}
+
+rsp_status rsp_linear_forward(const rsp_linear* h, const void* x, rsp_dtype xdt, float* y,
+                              uint32_t batch, void* ws, size_t ws_bytes, void* stream) {
+  if (!h || !x || !y) return fail(RSP_E_USAGE, "null handle or buffer");
+  if (rsp_status st = check_x_dtype(xdt)) return st;
+  if (batch == 0) return RSP_OK;
+  DeviceGuard g(h->device);
+  const size_t xs = static_cast<size_t>(h->m_in) * (xdt == RSP_BF16 ? 2 : 4);
+  for (uint32_t t = 0; t < batch; ++t) {
+    rsp_status st = launch_forward(h, static_cast<const uint8_t*>(x) + t * xs, xdt, y + static_cast<size_t>(t) * h->m,
+                                   ws, ws_bytes, static_cast<cudaStream_t>(stream), false);
+    if (st) return st;
+  }
+  return RSP_OK;
+}
+
+rsp_status rsp_linear_dense_forward(const rsp_linear* h, const void* x, rsp_dtype xdt, float* y,
+                                    void* ws, size_t ws_bytes, void* stream) {
+  if (!h || !x || !y) return fail(RSP_E_USAGE, "null handle or buffer");
+  if (rsp_status st = check_x_dtype(xdt)) return st;
+  DeviceGuard g(h->device);
+  return launch_forward(h, x, xdt, y, ws, ws_bytes, static_cast<cudaStream_t>(stream), true);
+}
+
+rsp_status rsp_linear_forward_host(rsp_linear* h, const void* x_host, rsp_dtype xdt, void* y_host,
+                                   rsp_dtype ydt, uint32_t batch) {
+  if (!h || !x_host || !y_host) return fail(RSP_E_USAGE, "null handle or buffer");
+  if (rsp_status st = check_x_dtype(xdt)) return st;
+  if (ydt != RSP_F32 && ydt != RSP_F64) return fail(RSP_E_USAGE, "y dtype must be F32 or F64");
+  if (batch == 0) return RSP_OK;
+  DeviceGuard g(h->device);
+  const size_t xs = static_cast<size_t>(h->m_in) * 4;  // room for fp32
+  if (!h->stream) RSP_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  if (h->host_batch < batch) {
+    cudaFree(h->x_dev);
+    cudaFree(h->y_dev);
+    cudaFreeHost(h->x_pin);
+    cudaFreeHost(h->y_pin);
+    h->x_dev = h->x_pin = nullptr;
+    h->y_dev = h->y_pin = nullptr;
+    RSP_CUDA(cudaMalloc(&h->x_dev, xs * batch));
+    RSP_CUDA(cudaMalloc(&h->y_dev, sizeof(float) * h->m * batch));
+    RSP_CUDA(cudaMallocHost(&h->x_pin, xs * batch));
+    RSP_CUDA(cudaMallocHost(&h->y_pin, sizeof(float) * h->m * batch));
+    h->host_batch = batch;
+  }
+  if (!h->ws) {
+    RSP_CUDA(cudaMalloc(&h->ws, h->plan.ws_bytes));
+    RSP_CUDA(cudaMemsetAsync(h->ws, 0, h->plan.ws_bytes, h->stream));
+  }
+  const size_t xbytes = static_cast<size_t>(h->m_in) * (xdt == RSP_BF16 ? 2 : 4) * batch;
+  std::memcpy(h->x_pin, x_host, xbytes);
+  RSP_CUDA(cudaMemcpyAsync(h->x_dev, h->x_pin, xbytes, cudaMemcpyHostToDevice, h->stream));
+  rsp_status st = rsp_linear_forward(h, h->x_dev, xdt, h->y_dev, batch, h->ws, h->plan.ws_bytes, h->stream);
+  if (st) return st;
+  const size_t ycount = static_cast<size_t>(h->m) * batch;
+  RSP_CUDA(cudaMemcpyAsync(h->y_pin, h->y_dev, ycount * sizeof(float), cudaMemcpyDeviceToHost, h->stream));
+  RSP_CUDA(cudaStreamSynchronize(h->stream));
+  if (ydt == RSP_F32) {
+    std::memcpy(y_host, h->y_pin, ycount * sizeof(float));
+  } else {
+    double* yd = static_cast<double*>(y_host);
+    for (size_t i = 0; i < ycount; ++i) yd[i] = h->y_pin[i];
+  }
+  return RSP_OK;
+}
+
+rsp_status rsp_gather_matvec(const rsp_linear* h, const void* x, rsp_dtype xdt, const int64_t* kept,
+                             uint32_t nkept, float* y, uint64_t* touched_bytes, void* stream) {
+  if (!h || !x || !y || (nkept && !kept)) return fail(RSP_E_USAGE, "null handle or buffer");
+  if (rsp_status st = check_x_dtype(xdt)) return st;
+  std::vector<int32_t> k32(nkept);
+  for (uint32_t t = 0; t < nkept; ++t) {
+    if (kept[t] < 0 || kept[t] >= static_cast<int64_t>(h->m_in))  // layer.cpp:83-86
+      return fail(RSP_E_USAGE, "gather_matvec: kept index %lld out of range for %u columns",
+                  static_cast<long long>(kept[t]), h->m_in);
+    k32[t] = static_cast<int32_t>(kept[t]);
+  }
+  DeviceGuard g(h->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int32_t* kd = nullptr;
+  if (nkept) {
+    RSP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&kd), nkept * sizeof(int32_t), s));
+    RSP_CUDA(cudaMemcpyAsync(kd, k32.data(), nkept * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  }
+  cudaError_t e = rsp::launch_gather(h->Wt, h->es, static_cast<int>(h->m), static_cast<int>(h->m_pad), x,
+                                     xdt == RSP_BF16, kd, static_cast<int>(nkept), y, s);
+  if (kd) cudaFreeAsync(kd, s);
+  RSP_CUDA(cudaStreamSynchronize(s));  // k32 must outlive the async copy
+  if (e != cudaSuccess) return fail(RSP_E_CUDA, "gather launch: %s", cudaGetErrorString(e));
+  if (touched_bytes) *touched_bytes += static_cast<uint64_t>(nkept) * h->m_out * 4u;  // layer.cpp:91
+  return RSP_OK;
+}
+
+rsp_status rsp_top_k_by_magnitude(const void* x, rsp_dtype xdt, uint32_t n, uint32_t k,
+                                  int32_t* kept, int32_t* rest, void* stream) {
+  if (k > n)  // matrix.cpp:101-104
+    return fail(RSP_E_USAGE, "top_k_by_magnitude: k=%u exceeds vector length %u", k, n);
+  if (rsp_status st = check_x_dtype(xdt)) return st;
+  if (n == 0) return RSP_OK;
+  if (!x) return fail(RSP_E_USAGE, "null x");
+  if (n > 48000) return fail(RSP_E_UNSUPPORTED, "selector supports n <= 48000");
+  cudaError_t e = rsp::launch_select(x, xdt == RSP_BF16, static_cast<int>(n), static_cast<int>(k), kept, rest,
+                                     nullptr, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(RSP_E_CUDA, "selector launch: %s", cudaGetErrorString(e));
+  return RSP_OK;
+}
+
+rsp_status rsp_threshold_sparsify(const void* x, rsp_dtype xdt, uint32_t n, double s,
+                                  float* sparse_x, int32_t* kept, uint32_t* k_out, void* stream) {
+  uint32_t k = 0;
+  if (rsp_status st = rsp_keep_count(s, n, &k)) return st;  // sparsity.cpp:22-27
+  if (rsp_status st = check_x_dtype(xdt)) return st;
+  if (k_out) *k_out = k;
+  if (n == 0) return RSP_OK;
+  if (n > 48000) return fail(RSP_E_UNSUPPORTED, "selector supports n <= 48000");
+  cudaError_t e = rsp::launch_select(x, xdt == RSP_BF16, static_cast<int>(n), static_cast<int>(k), kept, nullptr,
+                                     sparse_x, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(RSP_E_CUDA, "selector launch: %s", cudaGetErrorString(e));
+  return RSP_OK;
+}
+
+rsp_status rsp_linear_selected(const rsp_linear* h, const void* x, rsp_dtype xdt, int32_t* S_host,
+                               uint32_t* k_out) {
+  if (!h || !x || !S_host) return fail(RSP_E_USAGE, "null handle or buffer");
+  if (rsp_status st = check_x_dtype(xdt)) return st;
+  DeviceGuard g(h->device);
+  int32_t* kd = nullptr;
+  RSP_CUDA(cudaMalloc(&kd, sizeof(int32_t) * std::max<uint32_t>(h->k, 1)));
+  cudaError_t e = rsp::launch_select(x, xdt == RSP_BF16, static_cast<int>(h->m_in), static_cast<int>(h->k), kd,
+                                     nullptr, nullptr, nullptr);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpy(S_host, kd, sizeof(int32_t) * h->k, cudaMemcpyDeviceToHost);
+  cudaFree(kd);
+  if (e != cudaSuccess) return fail(RSP_E_CUDA, "selected: %s", cudaGetErrorString(e));
+  if (k_out) *k_out = h->k;
+  return RSP_OK;
+}
+
+rsp_status rsp_linear_io_cost(const rsp_linear* h, rsp_io_report* o) {
+  if (!h || !o) return fail(RSP_E_USAGE, "null handle");
+  // layer.cpp:125-140, evaluated on the whole layer
+  const double m = h->m_out, n = h->m_in, r = h->rank;
+  const uint64_t kept_cols = static_cast<uint64_t>(std::ceil(h->keep_fraction * n));
+  o->dense_bytes = static_cast<uint64_t>(h->m_in) * h->m_out * 4u;
+  o->touched_bytes = (kept_cols * h->m_out + static_cast<uint64_t>(h->rank) * (h->m_in + h->m_out)) * 4u;
+  o->relative_cost = r * (m + n) / (m * n) + h->keep_fraction;
+  // what the fused kernel streams for this shard (padded widths)
+  const uint64_t k = h->k, nn = h->m_in;
+  const bool lr = h->rank > 0 && k < nn;
+  o->kernel_weight_bytes = static_cast<uint64_t>(h->es) *
+                           (k * h->m_pad + (lr ? (nn - k) * h->r_pad + static_cast<uint64_t>(h->rank) * h->m_pad : 0));
+  o->kernel_total_bytes = o->kernel_weight_bytes + 4u * nn + 4u * static_cast<uint64_t>(h->m);
+  o->dense_weight_bytes = static_cast<uint64_t>(h->es) * nn * h->m_pad;
+  return RSP_OK;
+}
+
+rsp_status rsp_linear_export(const rsp_linear* h, int which, double* out) {
+  if (!h || !out) return fail(RSP_E_USAGE, "null handle or buffer");
+  DeviceGuard g(h->device);
+  const size_t n = h->m_in, m = h->m, r = h->rank;
+  size_t rows, cols;  // device array shape
+  const void* src;
+  size_t ld;
+  if (which == 0) {
+    rows = n; cols = m; src = h->Wt; ld = h->m_pad;
+  } else if (which == 1) {
+    rows = r; cols = m; src = h->At; ld = h->m_pad;
+  } else if (which == 2) {
+    rows = n; cols = r; src = h->Bt; ld = h->r_pad;
+  } else {
+    return fail(RSP_E_USAGE, "export: which must be 0, 1 or 2");
+  }
+  if (rows * cols == 0) return RSP_OK;
+  std::vector<uint8_t> buf(rows * ld * h->es);
+  RSP_CUDA(cudaMemcpy(buf.data(), src, buf.size(), cudaMemcpyDeviceToHost));
+  auto val = [&](size_t i, size_t j) -> double {
+    const size_t idx = i * ld + j;
+    if (h->es == 4) {
+      float f;
+      std::memcpy(&f, buf.data() + idx * 4, 4);
+      return f;
+    }
+    uint16_t b;
+    std::memcpy(&b, buf.data() + idx * 2, 2);
+    const uint32_t u = static_cast<uint32_t>(b) << 16;
+    float f;
+    std::memcpy(&f, &u, 4);
+    return f;
+  };
+  // device [rows][cols] -> reference row-major transpose
+  for (size_t i = 0; i < rows; ++i)
+    for (size_t j = 0; j < cols; ++j) out[j * rows + i] = val(i, j);
+  return RSP_OK;
+}
+
+rsp_status rsp_stack_create(const rsp_linear* const* layers, uint32_t count, const void* const* x_devs,
+                            rsp_dtype xdt, float* const* y_devs, int dense, rsp_stack** out) {
+  if (!layers || !x_devs || !y_devs || !out || count == 0) return fail(RSP_E_USAGE, "bad stack arguments");
+  if (rsp_status st = check_x_dtype(xdt)) return st;
+  *out = nullptr;
+  const int dev = layers[0]->device;
+  DeviceGuard g(dev);
+  size_t ws = 0;
+  for (uint32_t i = 0; i < count; ++i) {
+    if (layers[i]->device != dev) return fail(RSP_E_USAGE, "stack layers must share one device");
+    ws = std::max(ws, layers[i]->plan.ws_bytes);
+  }
+  auto* s = new rsp_stack();
+  s->device = dev;
+  cudaStream_t cs = nullptr;
+  cudaError_t e = cudaMalloc(&s->ws, ws);
+  if (e == cudaSuccess) e = cudaMemset(s->ws, 0, ws);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+  rsp_status st = RSP_OK;
+  if (e == cudaSuccess) {
+    for (uint32_t i = 0; i < count && !st; ++i)
+      st = launch_forward(layers[i], x_devs[i], xdt, y_devs[i], s->ws, ws, cs, dense != 0);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(cs, &graph);
+    s->graph = graph;
+    if (!st && ec != cudaSuccess) e = ec;
+  }
+  if (e == cudaSuccess && !st) e = cudaGraphInstantiate(&s->exec, s->graph, 0);
+  if (cs) cudaStreamDestroy(cs);
+  if (st || e != cudaSuccess) {
+    rsp_stack_destroy(s);
+    if (st) return st;
+    return fail(RSP_E_CUDA, "stack graph: %s", cudaGetErrorString(e));
+  }
+  *out = s;
+  return RSP_OK;
+}
+
+rsp_status rsp_stack_launch(rsp_stack* s, void* stream) {
+  if (!s) return fail(RSP_E_USAGE, "null stack");
+  DeviceGuard g(s->device);
+  RSP_CUDA(cudaGraphLaunch(s->exec, static_cast<cudaStream_t>(stream)));
+  return RSP_OK;
+}
+
+void rsp_stack_destroy(rsp_stack* s) {
+  if (!s) return;
+  DeviceGuard g(s->device);
+  if (s->exec) cudaGraphExecDestroy(s->exec);
+  if (s->graph) cudaGraphDestroy(s->graph);
+  cudaFree(s->ws);
+  delete s;
+}
+
+}  // extern "C"

@@ -1,0 +1,330 @@
+// rsp_device.cuh -- sm_100a device building blocks for the R-Sparse operator:
+// PTX wrappers (mbarrier, cp.async.bulk, gpu-scope acquire/release), a
+// reusable generation barrier over global memory, block scans, and the
+// block-wide exact top-k selector.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rsp {
+
+constexpr int kThreads = 512;               // every kernel in the fused path
+constexpr int kWarps = kThreads / 32;
+constexpr int kConsumerWarps = kWarps - 1;  // warp 0 produces, 1..15 consume
+constexpr int kConsumerThreads = kConsumerWarps * 32;
+constexpr int kHistBins = 4096;
+
+// ---------------------------------------------------------------------------
+// PTX wrappers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
+// L2 policy for streamed-once weights.
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+// 1-D bulk copy global -> this CTA's shared memory, completion counted in
+// bytes on `bar` (TMA engine; SASS UBLKCP).  dst/src 16 B aligned, bytes % 16 == 0.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ void prefetch_l2_bulk(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;"
+               : "=r"(old)
+               : "l"(p), "r"(v)
+               : "memory");
+  return old;
+}
+
+__device__ __forceinline__ void st_relaxed_gpu(unsigned* p, unsigned v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void griddep_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Reusable generation barrier in global memory: {count, gen}.  One thread per
+// CTA calls arrive (after the CTA's writes are fenced) and later wait.  The
+// last arriver resets count and publishes gen+1 with release semantics, so the
+// words are ready for the next use without any host-side reset.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned gbar_arrive(unsigned* bar, unsigned expected) {
+  const unsigned g = ld_relaxed_gpu(bar + 1);
+  __threadfence();
+  const unsigned old = atom_add_acq_rel_gpu(bar, 1u);
+  if (old == expected - 1) {
+    st_relaxed_gpu(bar, 0u);
+    st_release_gpu(bar + 1, g + 1);
+  }
+  return g;
+}
+
+__device__ __forceinline__ void gbar_wait(const unsigned* bar, unsigned g) {
+  while (ld_acquire_gpu(bar + 1) == g) {
+    __nanosleep(20);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Block-wide exclusive scan of one u32 per thread (all kThreads threads).
+// s_warp needs kWarps + 1 words.  Returns the exclusive prefix; *total gets
+// the block sum.  Contains __syncthreads.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp,
+                                                    uint32_t* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  if (lane == 31) s_warp[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t w = lane < kWarps ? s_warp[lane] : 0u;
+    uint32_t wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += t;
+    }
+    if (lane < kWarps) s_warp[lane] = wi - w;
+    if (lane == kWarps - 1) s_warp[kWarps] = wi;
+  }
+  __syncthreads();
+  const uint32_t res = s_warp[warp] + inc - v;
+  if (total) *total = s_warp[kWarps];
+  __syncthreads();
+  return res;
+}
+
+// ---------------------------------------------------------------------------
+// Exact top-k selection on |x| with the reference's total order
+// (|x| descending, index ascending; matrix.cpp:100-117).
+//
+// Keys are the IEEE-754 fp32 bit patterns with the sign cleared: for finite
+// values that order is exactly the order of fabs() on the values widened to
+// double, and +0/-0 collapse to one key (fabs(-0.0) == 0.0 ties with +0.0,
+// broken by index, as in the reference).  NaN keys order above +inf.
+//
+// The selection is summarised by (T, J):   j in S  <=>  key_j > T  or
+// (key_j == T and j <= J).  T is found by MSB-first radix selection over
+// 12/12/7-bit digits (12/3 for bf16 inputs, whose low 16 bits are zero) with
+// a 4096-bin shared histogram; the tie cut J is the need-th index (in index
+// order) among keys equal to T, found with one block scan.  Every thread of
+// the block returns the same (T, J).  k == 0 -> (0xffffffff, -1) (empty);
+// k == n -> (0, n) (everything).
+// ---------------------------------------------------------------------------
+struct Selection {
+  uint32_t T;
+  int32_t J;
+};
+
+__device__ __forceinline__ uint32_t abs_key(uint32_t bits) { return bits & 0x7fffffffu; }
+
+__device__ __forceinline__ bool is_selected(uint32_t key, int j, Selection s) {
+  return key > s.T || (key == s.T && j <= s.J);
+}
+
+__device__ Selection block_select(const uint32_t* __restrict__ xk, int n, int k, bool bf16_keys,
+                                  uint32_t* hist, uint32_t* s_warp, uint32_t* scratch) {
+  if (k <= 0) return Selection{0xffffffffu, -1};
+  if (k >= n) return Selection{0u, n};
+  const int tid = threadIdx.x;
+  uint32_t prefix = 0, pmask = 0;
+  int need = k;
+  const int npass = bf16_keys ? 2 : 3;
+  for (int p = 0; p < npass; ++p) {
+    const int shift = p == 0 ? 19 : (p == 1 ? (bf16_keys ? 16 : 7) : 0);
+    const int bits = p == 0 ? 12 : (p == 1 ? (bf16_keys ? 3 : 12) : 7);
+    const int nb = 1 << bits;
+    const uint32_t dmask = static_cast<uint32_t>(nb - 1);
+    for (int i = tid; i < nb; i += kThreads) hist[i] = 0u;
+    __syncthreads();
+    for (int j = tid; j < n; j += kThreads) {
+      const uint32_t key = abs_key(xk[j]);
+      if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & dmask], 1u);
+    }
+    __syncthreads();
+    // Thread t owns bins in descending order: d in [t*bpt, (t+1)*bpt), bin = nb-1-d.
+    const int bpt = (nb + kThreads - 1) / kThreads;
+    uint32_t local = 0;
+    for (int d = tid * bpt; d < (tid + 1) * bpt && d < nb; ++d) local += hist[nb - 1 - d];
+    const uint32_t above_me = block_excl_scan(local, s_warp, nullptr);
+    if (above_me < static_cast<uint32_t>(need) && static_cast<uint32_t>(need) <= above_me + local) {
+      uint32_t acc = above_me;
+      for (int d = tid * bpt; d < (tid + 1) * bpt && d < nb; ++d) {
+        const int bin = nb - 1 - d;
+        const uint32_t c = hist[bin];
+        if (acc + c >= static_cast<uint32_t>(need)) {
+          scratch[0] = static_cast<uint32_t>(bin);
+          scratch[1] = acc;
+          scratch[2] = c;
+          break;
+        }
+        acc += c;
+      }
+    }
+    __syncthreads();
+    const uint32_t b = scratch[0], above = scratch[1], cnt = scratch[2];
+    need -= static_cast<int>(above);
+    prefix |= b << shift;
+    pmask |= dmask << shift;
+    if (cnt == static_cast<uint32_t>(need)) {
+      // The whole boundary bin is taken: S = {key >= prefix}.
+      if (prefix == 0u) return Selection{0u, n};
+      return Selection{prefix - 1u, -1};
+    }
+  }
+  // prefix is now the exact k-th largest key T; cut the ties by index.
+  const uint32_t T = prefix;
+  const int E = (n + kThreads - 1) / kThreads;
+  const int j0 = min(n, tid * E), j1 = min(n, j0 + E);
+  uint32_t ties = 0;
+  for (int j = j0; j < j1; ++j) ties += abs_key(xk[j]) == T;
+  const uint32_t before = block_excl_scan(ties, s_warp, nullptr);
+  if (before < static_cast<uint32_t>(need) && static_cast<uint32_t>(need) <= before + ties) {
+    uint32_t acc = before;
+    for (int j = j0; j < j1; ++j) {
+      if (abs_key(xk[j]) == T && ++acc == static_cast<uint32_t>(need)) {
+        scratch[3] = static_cast<uint32_t>(j);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  return Selection{T, static_cast<int32_t>(scratch[3])};
+}
+
+// Load x (fp32 or bf16) into shared memory as fp32 bit patterns.
+__device__ __forceinline__ void load_x_bits(const void* __restrict__ x, bool x_bf16, int n,
+                                            uint32_t* xk) {
+  if (x_bf16) {
+    const uint16_t* xb = static_cast<const uint16_t*>(x);
+    for (int j = threadIdx.x; j < n; j += kThreads) xk[j] = static_cast<uint32_t>(xb[j]) << 16;
+  } else {
+    const uint32_t* xf = static_cast<const uint32_t*>(x);
+    for (int j = threadIdx.x; j < n; j += kThreads) xk[j] = xf[j];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 16-byte weight vectors -> fp32 FMAs
+// ---------------------------------------------------------------------------
+template <typename WT>
+struct Vec;
+
+template <>
+struct Vec<__nv_bfloat16> {
+  static constexpr int kElems = 8;
+  __device__ __forceinline__ static void fma(float (&acc)[8], const uint4 u, float c) {
+    acc[0] = fmaf(c, __uint_as_float(u.x << 16), acc[0]);
+    acc[1] = fmaf(c, __uint_as_float(u.x & 0xffff0000u), acc[1]);
+    acc[2] = fmaf(c, __uint_as_float(u.y << 16), acc[2]);
+    acc[3] = fmaf(c, __uint_as_float(u.y & 0xffff0000u), acc[3]);
+    acc[4] = fmaf(c, __uint_as_float(u.z << 16), acc[4]);
+    acc[5] = fmaf(c, __uint_as_float(u.z & 0xffff0000u), acc[5]);
+    acc[6] = fmaf(c, __uint_as_float(u.w << 16), acc[6]);
+    acc[7] = fmaf(c, __uint_as_float(u.w & 0xffff0000u), acc[7]);
+  }
+};
+
+template <>
+struct Vec<float> {
+  static constexpr int kElems = 4;
+  __device__ __forceinline__ static void fma(float (&acc)[4], const uint4 u, float c) {
+    acc[0] = fmaf(c, __uint_as_float(u.x), acc[0]);
+    acc[1] = fmaf(c, __uint_as_float(u.y), acc[1]);
+    acc[2] = fmaf(c, __uint_as_float(u.z), acc[2]);
+    acc[3] = fmaf(c, __uint_as_float(u.w), acc[3]);
+  }
+};
+
+}  // namespace rsp

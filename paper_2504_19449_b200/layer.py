@@ -1,0 +1,382 @@
+"""Host-side mirror of the reference operator API, over the C ABI.
+
+Names, argument meaning and error behaviour follow the reference's
+``namespace rsparse`` (core/include/rsparse/layer.hpp, sparsity.hpp,
+matrix.hpp, search.hpp) so code written against the reference reads the
+same here:
+
+    reference (C++)                                  here
+    ------------------------------------------------ -------------------------------
+    SparsityPlan{keep_fraction, rank} sparsity.hpp:34 SparsityPlan
+    DecomposedLayer               layer.hpp:38-48     DecomposedLayer
+    forward(layer, x)             layer.hpp:75        forward / DecomposedLayer.forward
+    gather_matvec(w_cols,x,kept)  layer.hpp:69-71     gather_matvec
+    io_cost(layer)                layer.hpp:77        io_cost / DecomposedLayer.io_cost
+    threshold_sparsify(x, s)      sparsity.hpp:43-44  threshold_sparsify
+    top_k_by_magnitude(x, k)      matrix.hpp:63       top_k_by_magnitude
+    Recipe::plan_for / rank_for   search.hpp:17-27    Recipe
+
+Device memory and streams are PyTorch's (plumbing only): activations are
+CUDA tensors, outputs are fp32 CUDA tensors.  All compute happens in
+librsparse_b200.so; nothing here computes a result on the CPU.
+"""
+from __future__ import annotations
+
+import ctypes as ct
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib as L
+from ._lib import check
+
+try:
+    import torch
+except ImportError:  # pragma: no cover - torch is part of the image
+    torch = None
+
+
+@dataclass
+class SparsityPlan:
+    """Per-layer knobs (sparsity.hpp:34-39): fraction of input channels kept
+    exactly, and the rank routed through the low-rank factors."""
+    keep_fraction: float = 1.0
+    rank: int = 0
+
+
+@dataclass
+class IoReport:
+    """io_cost (layer.hpp:51-55) plus the kernel's actual byte counts."""
+    dense_bytes: int
+    touched_bytes: int
+    relative_cost: float
+    kernel_weight_bytes: int
+    kernel_total_bytes: int
+    dense_weight_bytes: int
+
+
+def _stream_ptr(stream=None) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream) if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _x_dtype(x) -> int:
+    if x.dtype == torch.float32:
+        return L.RSP_F32
+    if x.dtype == torch.bfloat16:
+        return L.RSP_BF16
+    raise L.UsageError(L.RSP_E_USAGE, f"activation dtype {x.dtype} unsupported (float32/bfloat16)")
+
+
+def _src(a, name: str):
+    """(pointer, dtype code, memory code, keepalive) for a weight source."""
+    if torch is not None and isinstance(a, torch.Tensor):
+        a = a.contiguous()
+        code = {torch.float64: L.RSP_F64, torch.float32: L.RSP_F32, torch.bfloat16: L.RSP_BF16}.get(a.dtype)
+        if code is None:
+            raise L.UsageError(L.RSP_E_USAGE, f"{name}: dtype {a.dtype} unsupported")
+        mem = L.RSP_MEM_DEVICE if a.is_cuda else L.RSP_MEM_HOST
+        return a.data_ptr(), code, mem, a
+    arr = np.ascontiguousarray(a)
+    if arr.dtype == np.float64:
+        code = L.RSP_F64
+    elif arr.dtype == np.float32:
+        code = L.RSP_F32
+    else:
+        arr = arr.astype(np.float64)
+        code = L.RSP_F64
+    return arr.ctypes.data, code, L.RSP_MEM_HOST, arr
+
+
+class DecomposedLayer:
+    """A B200-resident rsparse::DecomposedLayer.
+
+    ``w`` is the m_out x m_in weight (``w_layout="row"``, rsparse::Matrix) or
+    the reference's column-major ``w_cols`` data as an (m_in, m_out) array
+    (``w_layout="col"``).  ``a_r`` (m_out x r) = U_r sqrt(Sigma_r) and ``b_r``
+    (r x m_in) = sqrt(Sigma_r) Vt_r are the precomputed factors
+    (layer.cpp:61-66).  Sources may be numpy arrays or torch tensors (host or
+    CUDA; f64/f32/bf16).  ``weight_dtype`` is the HBM storage type.
+    """
+
+    def __init__(self, w, a_r=None, b_r=None, plan: Optional[SparsityPlan] = None, *,
+                 keep_fraction: Optional[float] = None, rank: Optional[int] = None,
+                 weight_dtype: str = "bf16", w_layout: str = "row", k: Optional[int] = None,
+                 device: int = 0, shard_rank: int = 0, shard_count: int = 1):
+        if plan is None:
+            plan = SparsityPlan(1.0 if keep_fraction is None else keep_fraction,
+                                0 if rank is None else rank)
+        self.plan = plan
+        shape = tuple(w.shape)
+        if w_layout == "row":
+            m_out, m_in = shape
+        elif w_layout == "col":
+            m_in, m_out = shape
+        else:
+            raise L.UsageError(L.RSP_E_USAGE, "w_layout must be 'row' or 'col'")
+        r = int(plan.rank)
+        wp, wdt, wmem, wk = _src(w, "w")
+        keep = [wk]
+        ap = bp = 0
+        if r > 0:
+            if a_r is None or b_r is None:
+                raise L.UsageError(L.RSP_E_USAGE, "rank > 0 needs a_r and b_r")
+            if tuple(a_r.shape) != (m_out, r) or tuple(b_r.shape) != (r, m_in):
+                raise L.UsageError(L.RSP_E_USAGE, f"factor shapes {tuple(a_r.shape)} / {tuple(b_r.shape)} "
+                                   f"do not match m_out={m_out}, m_in={m_in}, r={r}")
+            ap, adt, amem, ak = _src(a_r, "a_r")
+            bp, bdt, bmem, bk = _src(b_r, "b_r")
+            if not (adt == bdt == wdt and amem == bmem == wmem):
+                raise L.UsageError(L.RSP_E_USAGE, "w, a_r and b_r must share dtype and memory")
+            keep += [ak, bk]
+        d = L.LinearDesc()
+        d.m_in, d.m_out, d.rank = m_in, m_out, r
+        d.keep_fraction = float(plan.keep_fraction)
+        d.k_override = -1 if k is None else int(k)
+        d.weight_dtype = {"bf16": L.RSP_BF16, "f32": L.RSP_F32, "fp32": L.RSP_F32}[weight_dtype]
+        d.src_dtype, d.src_memory = wdt, wmem
+        d.w_layout = L.RSP_W_ROW_MAJOR if w_layout == "row" else L.RSP_W_COL_MAJOR
+        d.w, d.a_r, d.b_r = wp, ap, bp
+        d.device, d.shard_rank, d.shard_count = device, shard_rank, shard_count
+        h = ct.c_void_p()
+        if torch is not None and wmem == L.RSP_MEM_DEVICE:
+            torch.cuda.synchronize(device)
+        check(L.lib().rsp_linear_create(ct.byref(d), ct.byref(h)), "rsp_linear_create")
+        self._h = h
+        self.device = device
+        self.weight_dtype = weight_dtype
+        self.m_in, self.m_out = m_in, m_out
+        info = L.LinearInfo()
+        check(L.lib().rsp_linear_info_get(self._h, ct.byref(info)))
+        self.info = {f: getattr(info, f) for f, _ in L.LinearInfo._fields_}
+        self.k = info.k
+        self.row_begin, self.row_end = info.row_begin, info.row_end
+        self._ws = None
+
+    # -- plumbing ------------------------------------------------------------
+    @property
+    def handle(self) -> ct.c_void_p:
+        return self._h
+
+    def workspace_size(self) -> int:
+        return int(L.lib().rsp_linear_workspace_size(self._h, 1))
+
+    def workspace(self):
+        """A zero-initialised per-layer workspace (torch uint8 CUDA tensor)."""
+        if self._ws is None:
+            self._ws = torch.zeros(self.workspace_size(), dtype=torch.uint8, device=f"cuda:{self.device}")
+        return self._ws
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            L.lib().rsp_linear_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- operator --------------------------------------------------------------
+    def forward(self, x, out=None, workspace=None, stream=None):
+        """rsparse::forward(layer, x) (layer.cpp:95-123) for one token, or a
+        (batch, m_in) tensor of tokens run as independent forwards.  Returns
+        fp32 (m_shard,) or (batch, m_shard) on the layer's device."""
+        if x.shape[-1] != self.m_in:  # layer.cpp:96-99
+            raise L.UsageError(L.RSP_E_USAGE, f"forward: input length {x.shape[-1]} does not match m_in {self.m_in}")
+        x = x.contiguous()
+        batch = 1 if x.dim() == 1 else x.shape[0]
+        m = self.row_end - self.row_begin
+        if out is None:
+            out = torch.empty((m,) if x.dim() == 1 else (batch, m), dtype=torch.float32, device=x.device)
+        ws = self.workspace() if workspace is None else workspace
+        check(L.lib().rsp_linear_forward(self._h, x.data_ptr(), _x_dtype(x), out.data_ptr(), batch,
+                                         ws.data_ptr(), ws.numel(), _stream_ptr(stream)),
+              "rsp_linear_forward")
+        return out
+
+    __call__ = forward
+
+    def dense_forward(self, x, out=None, workspace=None, stream=None):
+        """Dense baseline of the same layer: all m_in channels through W."""
+        x = x.contiguous()
+        m = self.row_end - self.row_begin
+        if out is None:
+            out = torch.empty(m, dtype=torch.float32, device=x.device)
+        ws = self.workspace() if workspace is None else workspace
+        check(L.lib().rsp_linear_dense_forward(self._h, x.data_ptr(), _x_dtype(x), out.data_ptr(),
+                                               ws.data_ptr(), ws.numel(), _stream_ptr(stream)),
+              "rsp_linear_dense_forward")
+        return out
+
+    def forward_host(self, x: np.ndarray, x_dtype: str = "f32") -> np.ndarray:
+        """End-to-end path with host buffers: H2D, fused forward, D2H.
+        Returns float64 like the reference's std::vector<double>."""
+        if x_dtype == "bf16":
+            xt = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(torch.bfloat16)
+            xa = xt.view(torch.int16).numpy()
+            code = L.RSP_BF16
+        else:
+            xa = np.ascontiguousarray(x, dtype=np.float32)
+            code = L.RSP_F32
+        if xa.shape[-1] != self.m_in:
+            raise L.UsageError(L.RSP_E_USAGE, f"forward: input length {xa.shape[-1]} does not match m_in {self.m_in}")
+        batch = 1 if xa.ndim == 1 else xa.shape[0]
+        m = self.row_end - self.row_begin
+        y = np.empty((m,) if xa.ndim == 1 else (batch, m), dtype=np.float64)
+        check(L.lib().rsp_linear_forward_host(self._h, xa.ctypes.data, code, y.ctypes.data, L.RSP_F64, batch),
+              "rsp_linear_forward_host")
+        return y
+
+    def selected(self, x) -> np.ndarray:
+        """The channel set S the forward keeps for x (ascending)."""
+        S = np.empty(max(self.k, 1), dtype=np.int32)
+        kk = ct.c_uint32()
+        check(L.lib().rsp_linear_selected(self._h, x.contiguous().data_ptr(), _x_dtype(x),
+                                          S.ctypes.data_as(ct.POINTER(ct.c_int32)), ct.byref(kk)),
+              "rsp_linear_selected")
+        return S[: kk.value].astype(np.int64)
+
+    def io_cost(self) -> IoReport:
+        rep = L.IoReport()
+        check(L.lib().rsp_linear_io_cost(self._h, ct.byref(rep)))
+        return IoReport(**{f: getattr(rep, f) for f, _ in L.IoReport._fields_})
+
+    def export(self):
+        """(W m_shard x m_in, a_r m_shard x r, b_r r x m_in) as float64: exactly the
+        values the kernels read (after dtype rounding)."""
+        m, n, r = self.row_end - self.row_begin, self.m_in, self.plan.rank
+        outs = []
+        for which, shape in ((0, (m, n)), (1, (m, r)), (2, (r, n))):
+            a = np.zeros(shape, dtype=np.float64)
+            if a.size:
+                check(L.lib().rsp_linear_export(self._h, which, a.ctypes.data_as(ct.POINTER(ct.c_double))))
+            outs.append(a)
+        return tuple(outs)
+
+
+def forward(layer: DecomposedLayer, x, **kw):
+    """rsparse::forward (layer.hpp:75)."""
+    return layer.forward(x, **kw)
+
+
+def io_cost(layer: DecomposedLayer) -> IoReport:
+    """rsparse::io_cost (layer.hpp:77)."""
+    return layer.io_cost()
+
+
+def gather_matvec(layer: DecomposedLayer, x, kept: Sequence[int], stream=None):
+    """rsparse::gather_matvec(w_cols, x, kept, touched_bytes) (layer.hpp:69-71):
+    y = sum over kept (in list order) of x_j * column j.  Returns (y, touched)."""
+    if x.shape[-1] != layer.m_in:
+        raise L.UsageError(L.RSP_E_USAGE, f"gather_matvec: input length {x.shape[-1]} does not match "
+                           f"column count {layer.m_in}")
+    kept = np.ascontiguousarray(np.asarray(kept, dtype=np.int64))
+    y = torch.empty(layer.row_end - layer.row_begin, dtype=torch.float32, device=x.device)
+    touched = ct.c_uint64(0)
+    x = x.contiguous()
+    check(L.lib().rsp_gather_matvec(layer.handle, x.data_ptr(), _x_dtype(x),
+                                    kept.ctypes.data_as(ct.POINTER(ct.c_int64)), kept.size,
+                                    y.data_ptr(), ct.byref(touched), _stream_ptr(stream)),
+          "rsp_gather_matvec")
+    return y, touched.value
+
+
+def top_k_by_magnitude(x, k: int, with_rest: bool = False, stream=None):
+    """rsparse::top_k_by_magnitude (matrix.cpp:100-117) on a CUDA vector:
+    indices of the k largest |x|, ties to the lower index, ascending (int32)."""
+    n = x.numel()
+    x = x.contiguous()
+    kept = torch.empty(max(k, 1), dtype=torch.int32, device=x.device)
+    rest = torch.empty(max(n - k, 1), dtype=torch.int32, device=x.device) if with_rest else None
+    check(L.lib().rsp_top_k_by_magnitude(x.data_ptr(), _x_dtype(x), n, k, kept.data_ptr(),
+                                         rest.data_ptr() if rest is not None else None,
+                                         _stream_ptr(stream)), "rsp_top_k_by_magnitude")
+    kept = kept[:k]
+    return (kept, rest[: n - k]) if with_rest else kept
+
+
+def threshold_sparsify(x, keep_fraction: float, stream=None):
+    """rsparse::threshold_sparsify (sparsity.cpp:20-32): (sparse_x fp32, kept int32)."""
+    n = x.numel()
+    x = x.contiguous()
+    sx = torch.empty(n, dtype=torch.float32, device=x.device)
+    kept = torch.empty(max(n, 1), dtype=torch.int32, device=x.device)
+    kk = ct.c_uint32()
+    check(L.lib().rsp_threshold_sparsify(x.data_ptr(), _x_dtype(x), n, float(keep_fraction),
+                                         sx.data_ptr(), kept.data_ptr(), ct.byref(kk),
+                                         _stream_ptr(stream)), "rsp_threshold_sparsify")
+    return sx, kept[: kk.value]
+
+
+def shard_rows(m_out: int, shard_rank: int, shard_count: int):
+    """Output rows [begin, end) owned by one shard (the partition create() applies)."""
+    b, e = ct.c_uint32(), ct.c_uint32()
+    check(L.lib().rsp_shard_rows(m_out, shard_rank, shard_count, ct.byref(b), ct.byref(e)), "shard_rows")
+    return b.value, e.value
+
+
+def keep_count(keep_fraction: float, n: int) -> int:
+    """k = ceil(s*n) (sparsity.cpp:26-27)."""
+    k = ct.c_uint32()
+    check(L.lib().rsp_keep_count(float(keep_fraction), int(n), ct.byref(k)), "keep_count")
+    return k.value
+
+
+class Recipe:
+    """rsparse::Recipe (search.hpp:17-27): per-layer rho_i (sparse share of
+    the I/O budget) and budget C_i."""
+
+    def __init__(self, rho: Sequence[float], budget: Sequence[float]):
+        if len(rho) != len(budget):
+            raise L.UsageError(L.RSP_E_USAGE, "rho and budget lengths differ")
+        self.rho = [float(v) for v in rho]
+        self.budget = [float(v) for v in budget]
+
+    def num_layers(self) -> int:
+        return len(self.rho)
+
+    def keep_fraction(self, i: int) -> float:
+        return self.rho[i] * self.budget[i]
+
+    def plan_for(self, i: int, m_in: int, m_out: int) -> SparsityPlan:
+        s, r = ct.c_double(), ct.c_uint32()
+        check(L.lib().rsp_plan_for(self.rho[i], self.budget[i], m_in, m_out, ct.byref(s), ct.byref(r)))
+        return SparsityPlan(s.value, r.value)
+
+    def rank_for(self, i: int, m_in: int, m_out: int) -> int:
+        return self.plan_for(i, m_in, m_out).rank
+
+
+class Stack:
+    """A decode-order sequence of forwards captured once into a CUDA graph."""
+
+    def __init__(self, layers: List[DecomposedLayer], xs, ys, dense: bool = False):
+        self.layers = layers
+        self.xs, self.ys = xs, ys
+        n = len(layers)
+        hp = (ct.c_void_p * n)(*[l.handle.value for l in layers])
+        xp = (ct.c_void_p * n)(*[x.data_ptr() for x in xs])
+        yp = (ct.c_void_p * n)(*[y.data_ptr() for y in ys])
+        h = ct.c_void_p()
+        torch.cuda.synchronize()
+        check(L.lib().rsp_stack_create(hp, n, xp, _x_dtype(xs[0]), yp, 1 if dense else 0, ct.byref(h)),
+              "rsp_stack_create")
+        self._h = h
+
+    def launch(self, stream=None) -> None:
+        check(L.lib().rsp_stack_launch(self._h, _stream_ptr(stream)), "rsp_stack_launch")
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            L.lib().rsp_stack_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,318 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the oracle.
+
+Selection is checked bit-exact (set equality, ascending order).  Outputs
+are checked with the max-norm relative error max|dy| / max|y_ref| (SURVEY
+Appendix A.5) and the reference's own L2 rel_error
+(tests/unit/test_helpers.hpp:139-146):
+
+* against the oracle run on the values the device holds (exported weights,
+  activations rounded as the device sees them): only accumulation order and
+  fp32-vs-fp64 arithmetic differ -> TOL_EXACT_INPUTS = 1e-5;
+* against the oracle on the ORIGINAL fp32 weights: fp32 weights -> 1e-5,
+  bf16 weights -> 1e-2 (BASELINE.json north_star tolerances).
+"""
+import numpy as np
+import pytest
+import torch
+
+import paper_2504_19449_b200 as rsp
+from paper_2504_19449_b200 import workloads as wl
+
+pytestmark = pytest.mark.gpu
+
+TOL_FP32 = 1e-5
+TOL_BF16 = 1e-2
+TOL_EXACT_INPUTS = 1e-5
+
+
+def maxrel(got, want):
+    got, want = np.asarray(got, np.float64), np.asarray(want, np.float64)
+    den = np.max(np.abs(want)) if want.size else 0.0
+    num = np.max(np.abs(got - want)) if want.size else 0.0
+    return num / den if den > 0 else num
+
+
+def l2rel(got, want):
+    got, want = np.asarray(got, np.float64), np.asarray(want, np.float64)
+    return np.linalg.norm(got - want) / max(1e-300, np.linalg.norm(want))
+
+
+def device_x(x_np, dtype, dev):
+    t = torch.as_tensor(np.asarray(x_np, dtype=np.float32), device=dev)
+    return t.to(torch.bfloat16) if dtype == "bf16" else t
+
+
+def as_seen(xt):
+    """The activation values the kernel sees, widened to float64."""
+    return xt.float().cpu().numpy().astype(np.float64)
+
+
+def oracle_on_device_values(coracle, layer, xt):
+    W, a, b = layer.export()
+    y, kept = coracle.forward(np.ascontiguousarray(W.T), a, b, layer.plan.keep_fraction,
+                              as_seen(xt), return_kept=True)
+    return y, kept, (W, a, b)
+
+
+# ----------------------------------------------------------------------------- selector
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_selector_golden_kats(golden, coracle, cuda, dtype):
+    for name in [str(s) for s in golden["topk.names"]]:
+        x, k = golden[f"topk.{name}.x"], int(golden[f"topk.{name}.k"][0])
+        xt = device_x(x, dtype, cuda)
+        if int(golden[f"topk.{name}.err"][0]):
+            with pytest.raises(rsp.UsageError):
+                rsp.top_k_by_magnitude(xt, k)
+            continue
+        got = rsp.top_k_by_magnitude(xt, k).cpu().numpy()
+        want = coracle.top_k_by_magnitude(as_seen(xt), k)
+        assert np.array_equal(got, want), name
+        if dtype == "f32" and np.array_equal(as_seen(xt), x):
+            assert np.array_equal(got, golden[f"topk.{name}.idx"]), name
+
+
+def _selector_inputs(rng, n):
+    yield "heavy", wl.heavy_tailed_x(n, rng)
+    yield "normal", rng.standard_normal(n).astype(np.float32)
+    yield "levels", (np.round(rng.standard_normal(n) * 2) / 2).astype(np.float32)
+    yield "all_equal", np.full(n, -0.75, np.float32)
+    z = np.zeros(n, np.float32)
+    z[rng.random(n) < 0.5] = -0.0
+    z[rng.choice(n, size=max(1, n // 10), replace=False)] = 1.0
+    yield "signed_zeros", z
+    yield "sign_dups", np.repeat(rng.standard_normal((n + 1) // 2).astype(np.float32), 2)[:n] * \
+        np.where(np.arange(n) % 2, -1, 1).astype(np.float32)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("n", [1, 2, 31, 511, 512, 513, 4096, 11008, 14336, 32768])
+def test_selector_random_bit_exact(coracle, cuda, dtype, n):
+    rng = np.random.default_rng(n)
+    for kind, x in _selector_inputs(rng, n):
+        xt = device_x(x, dtype, cuda)
+        xs = as_seen(xt)
+        for k in sorted({0, 1, n // 2, (n + 1) // 2, int(rng.integers(0, n + 1)), max(n - 1, 0), n}):
+            kept, rest = rsp.top_k_by_magnitude(xt, k, with_rest=True)
+            want = coracle.top_k_by_magnitude(xs, k)
+            assert np.array_equal(kept.cpu().numpy(), want), (kind, k)
+            comp = np.setdiff1d(np.arange(n), want)
+            assert np.array_equal(rest.cpu().numpy(), comp), (kind, k)
+
+
+def test_threshold_sparsify_gpu(golden, coracle, cuda):
+    for name in [str(s) for s in golden["thr.names"]]:
+        x, s = golden[f"thr.{name}.x"], float(golden[f"thr.{name}.s"][0])
+        xt = device_x(x, "f32", cuda)
+        if int(golden[f"thr.{name}.err"][0]):
+            with pytest.raises(rsp.UsageError):
+                rsp.threshold_sparsify(xt, s)
+            continue
+        sx, kept = rsp.threshold_sparsify(xt, s)
+        wsx, wkept = coracle.threshold_sparsify(as_seen(xt), s)
+        assert np.array_equal(kept.cpu().numpy(), wkept)
+        assert np.array_equal(sx.cpu().numpy().astype(np.float64), wsx)
+
+
+# ----------------------------------------------------------------------------- forward
+@pytest.mark.parametrize("wdt", ["f32", "bf16"])
+def test_forward_golden(golden, coracle, cuda, wdt):
+    for name in [str(s) for s in golden["fwd.names"]]:
+        w, a, b = golden[f"fwd.{name}.w"], golden[f"fwd.{name}.a_r"], golden[f"fwd.{name}.b_r"]
+        s, r = golden[f"fwd.{name}.plan"]
+        r = int(r)
+        layer = rsp.DecomposedLayer(w, a.reshape(w.shape[0], r), b.reshape(r, w.shape[1]),
+                                    rsp.SparsityPlan(float(s), r), weight_dtype=wdt)
+        for i, x in enumerate(golden[f"fwd.{name}.x"]):
+            xt = device_x(x, "f32", cuda)
+            y = layer.forward(xt).cpu().numpy()
+            yo, kept, _ = oracle_on_device_values(coracle, layer, xt)
+            assert np.array_equal(layer.selected(xt), kept), name
+            assert maxrel(y, yo) <= TOL_EXACT_INPUTS, (name, maxrel(y, yo))
+            tol = TOL_FP32 if wdt == "f32" else TOL_BF16
+            yg = golden[f"fwd.{name}.y"][i]
+            assert maxrel(y, yg) <= tol, (name, maxrel(y, yg))
+            if name == "zero_s0_r0":
+                assert np.all(y == 0.0)
+            if np.array_equal(as_seen(xt), x):
+                assert np.array_equal(layer.selected(xt), golden[f"fwd.{name}.kept{i}"])
+
+
+def test_forward_degenerate_plans_gpu(golden, cuda):
+    # test_layer.cpp:92-104: s=1,r=0 is the dense layer; s=0,r=min is W through the factors
+    w = golden["fwd.dense_s1_r0.w"]
+    x = golden["fwd.dense_s1_r0.x"][0]
+    layer = rsp.DecomposedLayer(w, plan=rsp.SparsityPlan(1.0, 0), weight_dtype="f32")
+    y = layer.forward(device_x(x, "f32", cuda)).cpu().numpy()
+    assert l2rel(y, w @ x) < 1e-6
+    w = golden["fwd.factors_s0_rmin.w"]
+    a, b = golden["fwd.factors_s0_rmin.a_r"], golden["fwd.factors_s0_rmin.b_r"]
+    x = golden["fwd.factors_s0_rmin.x"][0]
+    layer = rsp.DecomposedLayer(w, a.reshape(14, 11), b.reshape(11, 11), rsp.SparsityPlan(0.0, 11),
+                                weight_dtype="f32")
+    y = layer.forward(device_x(x, "f32", cuda)).cpu().numpy()
+    assert l2rel(y, w @ x) < 1e-5
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (5, 7), (13, 40), (100, 3), (1000, 777), (4100, 300),
+                                   (20000, 64)])
+@pytest.mark.parametrize("wdt", ["f32", "bf16"])
+def test_forward_ragged_shapes(coracle, cuda, shape, wdt):
+    m, n = shape
+    rng = np.random.default_rng(m * 1000 + n)
+    for s, r in [(0.5, min(m, n) // 2), (0.0, min(m, n)), (1.0, 0), (0.3, 0), (0.77, 1)]:
+        r = min(r, m, n)
+        w = rng.standard_normal((m, n)).astype(np.float32)
+        a = rng.standard_normal((m, r)).astype(np.float32)
+        b = rng.standard_normal((r, n)).astype(np.float32)
+        layer = rsp.DecomposedLayer(w, a, b, rsp.SparsityPlan(s, r), weight_dtype=wdt)
+        xt = device_x(wl.heavy_tailed_x(n, rng, outliers=min(8, n)), "f32", cuda)
+        y = layer.forward(xt).cpu().numpy()
+        yo, kept, _ = oracle_on_device_values(coracle, layer, xt)
+        assert np.array_equal(layer.selected(xt), kept)
+        assert maxrel(y, yo) <= TOL_EXACT_INPUTS, (s, r, maxrel(y, yo))
+
+
+def test_forward_k_override_and_errors(coracle, cuda):
+    rng = np.random.default_rng(3)
+    w = rng.standard_normal((64, 96)).astype(np.float32)
+    a = rng.standard_normal((64, 8)).astype(np.float32)
+    b = rng.standard_normal((8, 96)).astype(np.float32)
+    layer = rsp.DecomposedLayer(w, a, b, rsp.SparsityPlan(0.5, 8), k=17, weight_dtype="f32")
+    xt = device_x(rng.standard_normal(96), "f32", cuda)
+    assert layer.k == 17 and layer.selected(xt).size == 17
+    with pytest.raises(rsp.UsageError):  # layer.cpp:96-99
+        layer.forward(device_x(np.zeros(95), "f32", cuda))
+    with pytest.raises(rsp.UsageError):  # layer.cpp:40-44
+        rsp.DecomposedLayer(w, a, b, rsp.SparsityPlan(0.5, 65))
+    with pytest.raises(rsp.UsageError):  # sparsity.cpp:22-25
+        rsp.DecomposedLayer(w, a, b, rsp.SparsityPlan(1.5, 8))
+
+
+def test_full_size_config0_fp32(coracle, cuda):
+    c = wl.config0(seed=0, device="cuda")
+    for xdt in ("f32", "bf16"):
+        layer = rsp.DecomposedLayer(c["w"], c["a_r"], c["b_r"], rsp.SparsityPlan(c["keep_fraction"], c["rank"]),
+                                    weight_dtype="f32")
+        assert layer.k == 2048
+        xt = c["x"].to(torch.bfloat16) if xdt == "bf16" else c["x"]
+        y = layer.forward(xt).cpu().numpy()
+        yo, kept, _ = oracle_on_device_values(coracle, layer, xt)
+        assert np.array_equal(layer.selected(xt), kept)
+        assert maxrel(y, yo) <= TOL_FP32, maxrel(y, yo)
+        assert l2rel(y, yo) <= TOL_FP32
+
+
+@pytest.mark.parametrize("name,m,n", wl.LLAMA2_7B)
+def test_full_size_config1_bf16(coracle, cuda, name, m, n):
+    c = wl.config1_layer(name, m, n, device="cuda")
+    layer = rsp.DecomposedLayer(c["w"], c["a_r"], c["b_r"], rsp.SparsityPlan(0.5, c["rank"]),
+                                weight_dtype="bf16")
+    w32 = c["w"].double().cpu().numpy()
+    a32, b32 = c["a_r"].double().cpu().numpy(), c["b_r"].double().cpu().numpy()
+    for xdt in ("f32", "bf16"):
+        xt = c["x"].to(torch.bfloat16) if xdt == "bf16" else c["x"]
+        y = layer.forward(xt).cpu().numpy()
+        yo, kept, _ = oracle_on_device_values(coracle, layer, xt)
+        assert np.array_equal(layer.selected(xt), kept)
+        assert maxrel(y, yo) <= TOL_EXACT_INPUTS, maxrel(y, yo)
+        # against the reference on the original (un-rounded) fp32 operands
+        yref = coracle.forward(np.ascontiguousarray(w32.T), a32, b32, 0.5, as_seen(xt))
+        assert maxrel(y, yref) <= TOL_BF16, maxrel(y, yref)
+
+
+def test_scaling_property_full_size(cuda):
+    # power-of-two scaling keeps the selection and scales every product exactly
+    c = wl.config1_layer("gate_proj", 11008, 4096, device="cuda")
+    layer = rsp.DecomposedLayer(c["w"], c["a_r"], c["b_r"], rsp.SparsityPlan(0.5, c["rank"]))
+    y1 = layer.forward(c["x"])
+    y2 = layer.forward(c["x"] * 4.0)
+    assert torch.equal(y2, y1 * 4.0)
+
+
+def test_deterministic_and_host_path(cuda):
+    c = wl.config1_layer("down_proj", 4096, 11008, device="cuda")
+    layer = rsp.DecomposedLayer(c["w"], c["a_r"], c["b_r"], rsp.SparsityPlan(0.5, c["rank"]))
+    ys = [layer.forward(c["x"]).clone() for _ in range(5)]
+    assert all(torch.equal(ys[0], y) for y in ys[1:])  # no float atomics: bit-reproducible
+    yh = layer.forward_host(c["x"].cpu().numpy())
+    assert np.array_equal(yh, ys[0].cpu().numpy().astype(np.float64))
+    xb = c["x"].to(torch.bfloat16)
+    yb = layer.forward_host(c["x"].cpu().numpy(), x_dtype="bf16")
+    assert np.array_equal(yb, layer.forward(xb).cpu().numpy().astype(np.float64))
+
+
+def test_batch_is_per_token(cuda):
+    c = wl.config1_layer("q_proj", 4096, 4096, device="cuda")
+    layer = rsp.DecomposedLayer(c["w"], c["a_r"], c["b_r"], rsp.SparsityPlan(0.5, c["rank"]))
+    rng = np.random.default_rng(5)
+    X = torch.stack([torch.from_numpy(wl.heavy_tailed_x(4096, rng)) for _ in range(4)]).to(cuda)
+    Y = layer.forward(X)
+    for t in range(4):
+        assert torch.equal(Y[t], layer.forward(X[t]))
+
+
+def test_shards_concatenate_to_full(cuda):
+    c = wl.config1_layer("up_proj", 11008, 4096, device="cuda")
+    full = rsp.DecomposedLayer(c["w"], c["a_r"], c["b_r"], rsp.SparsityPlan(0.5, c["rank"]))
+    yf = full.forward(c["x"])
+    for g in (2, 3, 8):
+        parts = []
+        for i in range(g):
+            sh = rsp.DecomposedLayer(c["w"], c["a_r"], c["b_r"], rsp.SparsityPlan(0.5, c["rank"]),
+                                     shard_rank=i, shard_count=g)
+            assert (sh.row_begin, sh.row_end) == rsp.shard_rows(11008, i, g)
+            parts.append(sh.forward(c["x"]))
+        yc = torch.cat(parts)
+        assert maxrel(yc.cpu().numpy(), yf.cpu().numpy()) <= 1e-6
+
+
+def test_gather_matvec_gpu(golden, coracle, cuda):
+    for name in [str(s) for s in golden["gmv.names"]]:
+        w, x, kept = golden[f"gmv.{name}.w"], golden[f"gmv.{name}.x"], golden[f"gmv.{name}.kept"]
+        layer = rsp.DecomposedLayer(w, plan=rsp.SparsityPlan(1.0, 0), weight_dtype="f32")
+        y, touched = rsp.gather_matvec(layer, device_x(x, "f32", cuda), kept)
+        assert touched == int(golden[f"gmv.{name}.touched"][0])
+        assert maxrel(y.cpu().numpy(), golden[f"gmv.{name}.y"]) <= TOL_FP32
+        with pytest.raises(rsp.UsageError):
+            rsp.gather_matvec(layer, device_x(x, "f32", cuda), [w.shape[1]])
+
+
+def test_dense_forward_matches_matvec(coracle, cuda):
+    c = wl.config1_layer("o_proj", 4096, 4096, device="cuda")
+    layer = rsp.DecomposedLayer(c["w"], c["a_r"], c["b_r"], rsp.SparsityPlan(0.5, c["rank"]))
+    y = layer.dense_forward(c["x"]).cpu().numpy()
+    W, _, _ = layer.export()
+    yo = coracle.matvec(W, as_seen(c["x"]))
+    assert maxrel(y, yo) <= TOL_EXACT_INPUTS
+
+
+def test_io_cost_gpu(golden, cuda):
+    rng = np.random.default_rng(0)
+    for (n, m, s, r, db, tb, rc) in golden["io.cases"]:
+        n, m, r = int(n), int(m), int(r)
+        if m * n > 4096 * 4096:
+            continue
+        w = np.zeros((m, n), np.float32)
+        a = rng.standard_normal((m, r)).astype(np.float32)
+        b = rng.standard_normal((r, n)).astype(np.float32)
+        rep = rsp.DecomposedLayer(w, a, b, rsp.SparsityPlan(float(s), r)).io_cost()
+        assert rep.dense_bytes == int(db) and rep.touched_bytes == int(tb) and rep.relative_cost == rc
+
+
+def test_stack_graph_matches_individual_forwards(cuda):
+    rng = np.random.default_rng(9)
+    layers, xs = [], []
+    for (name, m, n) in wl.LLAMA2_7B:
+        w = torch.randn(m, n, device=cuda) * 0.02
+        r = 64
+        a = torch.randn(m, r, device=cuda) * 0.1
+        b = torch.randn(r, n, device=cuda) * 0.1
+        layers.append(rsp.DecomposedLayer(w, a, b, rsp.SparsityPlan(float(rng.uniform(0.15, 0.35)), r)))
+        xs.append(torch.from_numpy(wl.heavy_tailed_x(n, rng)).to(cuda).to(torch.bfloat16))
+    ys = [torch.empty(l.m_out, device=cuda) for l in layers]
+    st = rsp.Stack(layers, xs, ys)
+    for _ in range(3):
+        st.launch()
+    torch.cuda.synchronize()
+    for l, x, y in zip(layers, xs, ys):
+        assert torch.equal(y, l.forward(x))
