@@ -73,7 +73,13 @@ typedef struct rsp_linear_desc {
   int device;               /* CUDA ordinal */
   uint32_t shard_rank;      /* output-row sharding: this handle owns rows   */
   uint32_t shard_count;     /* [m_out*rank/count, m_out*(rank+1)/count)     */
+  uint32_t flags;           /* RSP_FLAG_* */
 } rsp_linear_desc;
+
+/* desc.flags */
+#define RSP_FLAG_DETERMINISTIC 1u /* combine split-K partials of y in a fixed order
+                                     (bit-reproducible, ~1 us slower per forward);
+                                     default: float atomics into y */
 
 typedef struct rsp_linear_info {
   uint32_t m_in, m_out, rank, k;
@@ -193,6 +199,14 @@ rsp_status rsp_stack_create(const rsp_linear* const* layers, uint32_t count,
                             int dense, rsp_stack** out);
 rsp_status rsp_stack_launch(rsp_stack* s, void* stream);
 void rsp_stack_destroy(rsp_stack* s);
+
+/* -- diagnostics ---------------------------------------------------------------- */
+/* rsp_linear_forward (dense=0) or rsp_linear_dense_forward (dense=1) that also
+ * records per-CTA phase timestamps into trace_dev (int64, grid x 16: slot 0 =
+ * %globaltimer at CTA start, slots 1..15 = %clock64 cycles since CTA start). */
+rsp_status rsp_debug_forward_trace(const rsp_linear* h, const void* x_dev, rsp_dtype x_dtype,
+                                   float* y_dev, void* workspace, size_t workspace_bytes,
+                                   int64_t* trace_dev, int dense, void* stream);
 
 /* -- device helpers ------------------------------------------------------------- */
 int rsp_device_sm_count(int device);

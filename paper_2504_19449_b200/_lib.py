@@ -23,7 +23,7 @@ EXPORTS = [
     "rsp_linear_forward_host", "rsp_linear_dense_forward", "rsp_gather_matvec",
     "rsp_linear_selected", "rsp_linear_io_cost", "rsp_linear_export",
     "rsp_top_k_by_magnitude", "rsp_threshold_sparsify", "rsp_stack_create",
-    "rsp_stack_launch", "rsp_stack_destroy", "rsp_device_sm_count",
+    "rsp_stack_launch", "rsp_stack_destroy", "rsp_device_sm_count", "rsp_debug_forward_trace",
 ]
 
 
@@ -34,7 +34,11 @@ class LinearDesc(ct.Structure):
         ("weight_dtype", ct.c_int), ("src_dtype", ct.c_int), ("src_memory", ct.c_int),
         ("w_layout", ct.c_int), ("w", ct.c_void_p), ("a_r", ct.c_void_p), ("b_r", ct.c_void_p),
         ("device", ct.c_int), ("shard_rank", ct.c_uint32), ("shard_count", ct.c_uint32),
+        ("flags", ct.c_uint32),
     ]
+
+
+RSP_FLAG_DETERMINISTIC = 1
 
 
 class LinearInfo(ct.Structure):
@@ -120,6 +124,7 @@ def lib() -> ct.CDLL:
         "rsp_stack_launch": (ct.c_int, [vp, vp]),
         "rsp_stack_destroy": (None, [vp]),
         "rsp_device_sm_count": (ct.c_int, [ct.c_int]),
+        "rsp_debug_forward_trace": (ct.c_int, [vp, vp, ct.c_int, vp, vp, ct.c_size_t, vp, ct.c_int, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -112,6 +112,7 @@ struct rsp_linear {
   void* Bt = nullptr;
   LaunchPlan plan;
   bool pdl = true;
+  bool deterministic = false;  // RSP_FLAG_DETERMINISTIC: fixed-order split-K combine
   // forward_host staging (lazily created)
   cudaStream_t stream = nullptr;
   void* x_dev = nullptr;
@@ -132,51 +133,52 @@ struct rsp_stack {
 namespace {
 
 // Decompose one forward over the GPU: col_tiles column tiles x k_splits
-// K-splits, one CTA per SM.  Column tiles target ~2 KB contiguous row
-// segments (one bulk copy each) and never exceed 15 x 512 B (one 16-byte
-// vector per consumer lane).
+// K-splits, one CTA per SM.  A column tile is a whole number of 16-byte units
+// of a row; tiles of ~512 B per row (one warp-wide 16-byte load) keep the
+// split-K fan-in small (~9) so the last-CTA reduction of y is cheap.
 rsp_status make_plan(const rsp_linear& L, const DevProps& dp, LaunchPlan* out) {
   LaunchPlan p;
-  const uint32_t n = L.m_in, vm = L.m_pad / 8;
-  const uint32_t row_bytes = L.m_pad * L.es;
-  const int stage_bytes = env_int("RSP_STAGE_BYTES", 16384);
-  int nt = std::max(1, static_cast<int>(std::lround(row_bytes / static_cast<double>(
-                                                        env_int("RSP_SEG_BYTES", 2048)))));
-  nt = std::max(nt, static_cast<int>((row_bytes + 7679) / 7680));
-  nt = std::max(nt, static_cast<int>((row_bytes + stage_bytes - 1) / stage_bytes));
-  nt = std::min<int>(nt, static_cast<int>(vm));
-  nt = std::min(nt, dp.sms);
+  const uint32_t n = L.m_in;
+  const int vrow = static_cast<int>(L.m_pad * L.es / 16);   // 16-B units per W^T row
+  const int vb = static_cast<int>(L.r_pad * L.es / 16);     // 16-B units per B_r^T row
+  const int c1 = L.rank ? (vb + 31) / 32 : 0;               // warps per B_r^T row
+  if (c1 > 8)
+    return fail(RSP_E_UNSUPPORTED, "rank %u too large (B_r^T rows limited to 4 KB)", L.rank);
+  const int max_tiles = env_int("RSP_MAX_TILES", 16);
+  int nt = std::max(1, std::min(vrow / 32, max_tiles));
+  nt = std::max(nt, (vrow + 255) / 256);                    // <= 8 warps per tile row
+  nt = std::min(nt, std::min(vrow, dp.sms));
   int ks = std::max(1, dp.sms / nt);
   // Small layers: keep >= ~32 KB of streamed bytes per CTA.
-  const double bytes = static_cast<double>(L.k + L.rank) * row_bytes +
-                       static_cast<double>(n - L.k) * L.r_pad * L.es;
+  const double bytes = static_cast<double>(L.k + L.rank) * vrow * 16.0 +
+                       static_cast<double>(n - L.k) * vb * 16.0;
   const int want = std::max(1, static_cast<int>(std::ceil(bytes / 32768.0)));
   ks = std::min(ks, std::max(1, (want + nt - 1) / nt));
+  ks = std::min(ks, static_cast<int>(std::max(1u, n)));
   p.col_tiles = nt;
   p.k_splits = ks;
   p.grid = nt * ks;
+  p.nb_pad = static_cast<int>(round_up(static_cast<uint32_t>(p.grid), 4u));
   p.cap_w = static_cast<int>((n + ks - 1) / ks) + 1;  // covers the dense sweep too
   p.cap_u = static_cast<int>((n - L.k + p.grid - 1) / p.grid) + 1;
-  p.cap_a = static_cast<int>((L.rank + ks - 1) / ks) + 1;
-  p.stage_bytes = stage_bytes;
-  if (static_cast<int>(L.r_pad * L.es) > stage_bytes)
-    return fail(RSP_E_UNSUPPORTED, "rank %u too large for the %d-byte ring stage", L.rank,
-                stage_bytes);
-  if (static_cast<int>(L.r_pad * L.es) > 15 * 512)
-    return fail(RSP_E_UNSUPPORTED, "rank %u exceeds the consumer width", L.rank);
-  p.stages = env_int("RSP_STAGES", 8);
-  size_t smem = rsp::fused_smem_bytes(p, static_cast<int>(n), L.es);
-  while (smem > static_cast<size_t>(dp.smem_optin) && p.stages > 2) {
-    --p.stages;
-    smem = rsp::fused_smem_bytes(p, static_cast<int>(n), L.es);
-  }
-  if (smem > static_cast<size_t>(dp.smem_optin))
-    return fail(RSP_E_UNSUPPORTED, "fused kernel needs %zu B shared memory (> %d)", smem,
+  p.cap_a = static_cast<int>((L.rank + ks - 1) / ks) + 4;
+  p.a_smem_bytes = 0;
+  const size_t base = rsp::fused_smem_bytes(p, static_cast<int>(n));
+  if (base > static_cast<size_t>(dp.smem_optin))
+    return fail(RSP_E_UNSUPPORTED, "fused kernel needs %zu B shared memory (> %d)", base,
                 dp.smem_optin);
-  p.smem = smem;
-  const size_t bars = round_up(4u * (2u + 2u * nt), 256u);
+  if (L.rank > 0 && env_int("RSP_A_SMEM", 1)) {
+    // Stage this CTA's A_r^T rows in shared memory when they fit (they do not
+    // depend on x, so the copy is issued before the kernel waits for x).
+    const int tw_max = (vrow + nt - 1) / nt;
+    const size_t want_a = static_cast<size_t>(p.cap_a) * tw_max * 16;
+    const size_t room = static_cast<size_t>(dp.smem_optin) - base - 256;
+    p.a_smem_bytes = static_cast<int>(std::min(want_a, room) / 16 * 16);
+  }
+  p.smem = rsp::fused_smem_bytes(p, static_cast<int>(n));
+  const size_t bars = round_up(4u * (2u + static_cast<uint32_t>(nt)), 256u);
   p.ws_t_off = bars;
-  p.ws_y_off = p.ws_t_off + round_up(4u * static_cast<uint32_t>(p.grid) * std::max(L.r_pad, 8u), 256u);
+  p.ws_y_off = p.ws_t_off + round_up(4u * static_cast<uint32_t>(p.nb_pad) * std::max(L.r_pad, 8u), 256u);
   p.ws_bytes = p.ws_y_off + static_cast<size_t>(4) * ks * L.m_pad;
   *out = p;
   return RSP_OK;
@@ -205,8 +207,9 @@ FusedParams fused_params(const rsp_linear* h, const void* x, rsp_dtype xdt, floa
   p.cap_w = h->plan.cap_w;
   p.cap_u = h->plan.cap_u;
   p.cap_a = h->plan.cap_a;
-  p.stage_bytes = h->plan.stage_bytes;
-  p.stages = h->plan.stages;
+  p.a_smem_bytes = h->plan.a_smem_bytes;
+  p.nb_pad = h->plan.nb_pad;
+  p.deterministic = h->deterministic ? 1 : 0;
   p.x_bf16 = xdt == RSP_BF16 ? 1 : 0;
   p.dense = dense ? 1 : 0;
   return p;
@@ -287,11 +290,12 @@ void free_linear(rsp_linear* h) {
 }
 
 rsp_status launch_forward(const rsp_linear* h, const void* x, rsp_dtype xdt, float* y, void* ws,
-                          size_t ws_bytes, cudaStream_t stream, bool dense) {
+                          size_t ws_bytes, cudaStream_t stream, bool dense, long long* trace = nullptr) {
   if (!ws || ws_bytes < h->plan.ws_bytes)
     return fail(RSP_E_USAGE, "workspace of %zu bytes is smaller than the %zu required", ws_bytes,
                 h->plan.ws_bytes);
-  const FusedParams p = fused_params(h, x, xdt, y, ws, dense);
+  FusedParams p = fused_params(h, x, xdt, y, ws, dense);
+  p.trace = trace;
   cudaError_t e = rsp::launch_fused(p, h->es, h->plan.grid, h->plan.smem, stream, h->pdl);
   if (e != cudaSuccess) return fail(RSP_E_CUDA, "fused forward launch: %s", cudaGetErrorString(e));
   return RSP_OK;
@@ -378,6 +382,7 @@ rsp_status rsp_linear_create(const rsp_linear_desc* d, rsp_linear** out) {
   h->wdt = d->weight_dtype;
   h->es = d->weight_dtype == RSP_F32 ? 4 : 2;
   h->pdl = env_flag("RSP_PDL", true);
+  h->deterministic = (d->flags & RSP_FLAG_DETERMINISTIC) != 0 || env_flag("RSP_DETERMINISTIC", false);
   const DevProps dp = device_props(d->device);
   if (dp.sms == 0) {
     delete h;
@@ -407,7 +412,9 @@ rsp_status rsp_linear_create(const rsp_linear_desc* d, rsp_linear** out) {
     free_linear(h);
     return st;
   }
-  e = rsp::fused_set_smem(h->es, h->plan.smem);
+  // The attribute is per kernel, not per launch: raise it to the opt-in
+  // maximum once so every handle's plan fits regardless of creation order.
+  e = rsp::fused_set_smem(h->es, static_cast<size_t>(dp.smem_optin));
   if (e != cudaSuccess) {
     free_linear(h);
     return fail(RSP_E_CUDA, "cudaFuncSetAttribute(smem=%zu): %s", h->plan.smem, cudaGetErrorString(e));
@@ -468,6 +475,15 @@ rsp_status rsp_linear_dense_forward(const rsp_linear* h, const void* x, rsp_dtyp
   if (rsp_status st = check_x_dtype(xdt)) return st;
   DeviceGuard g(h->device);
   return launch_forward(h, x, xdt, y, ws, ws_bytes, static_cast<cudaStream_t>(stream), true);
+}
+
+rsp_status rsp_debug_forward_trace(const rsp_linear* h, const void* x, rsp_dtype xdt, float* y, void* ws,
+                                   size_t ws_bytes, int64_t* trace, int dense, void* stream) {
+  if (!h || !x || !y || !trace) return fail(RSP_E_USAGE, "null handle or buffer");
+  if (rsp_status st = check_x_dtype(xdt)) return st;
+  DeviceGuard g(h->device);
+  return launch_forward(h, x, xdt, y, ws, ws_bytes, static_cast<cudaStream_t>(stream), dense != 0,
+                        reinterpret_cast<long long*>(trace));
 }
 
 rsp_status rsp_linear_forward_host(rsp_linear* h, const void* x_host, rsp_dtype xdt, void* y_host,

@@ -12,8 +12,6 @@ namespace rsp {
 
 constexpr int kThreads = 512;               // every kernel in the fused path
 constexpr int kWarps = kThreads / 32;
-constexpr int kConsumerWarps = kWarps - 1;  // warp 0 produces, 1..15 consume
-constexpr int kConsumerThreads = kConsumerWarps * 32;
 constexpr int kHistBins = 4096;
 
 // ---------------------------------------------------------------------------
@@ -146,8 +144,12 @@ __device__ __forceinline__ unsigned gbar_arrive(unsigned* bar, unsigned expected
 }
 
 __device__ __forceinline__ void gbar_wait(const unsigned* bar, unsigned g) {
+  // Watchdog: a barrier that cannot complete (CTAs not co-resident, corrupted
+  // workspace) traps after ~seconds instead of hanging the device.
+  unsigned long long spins = 0;
   while (ld_acquire_gpu(bar + 1) == g) {
-    __nanosleep(20);
+    __nanosleep(64);
+    if (++spins > (1ull << 26)) __trap();
   }
 }
 
@@ -185,114 +187,34 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp
   return res;
 }
 
-// ---------------------------------------------------------------------------
-// Exact top-k selection on |x| with the reference's total order
-// (|x| descending, index ascending; matrix.cpp:100-117).
-//
-// Keys are the IEEE-754 fp32 bit patterns with the sign cleared: for finite
-// values that order is exactly the order of fabs() on the values widened to
-// double, and +0/-0 collapse to one key (fabs(-0.0) == 0.0 ties with +0.0,
-// broken by index, as in the reference).  NaN keys order above +inf.
-//
-// The selection is summarised by (T, J):   j in S  <=>  key_j > T  or
-// (key_j == T and j <= J).  T is found by MSB-first radix selection over
-// 12/12/7-bit digits (12/3 for bf16 inputs, whose low 16 bits are zero) with
-// a 4096-bin shared histogram; the tie cut J is the need-th index (in index
-// order) among keys equal to T, found with one block scan.  Every thread of
-// the block returns the same (T, J).  k == 0 -> (0xffffffff, -1) (empty);
-// k == n -> (0, n) (everything).
-// ---------------------------------------------------------------------------
-struct Selection {
-  uint32_t T;
-  int32_t J;
-};
-
-__device__ __forceinline__ uint32_t abs_key(uint32_t bits) { return bits & 0x7fffffffu; }
-
-__device__ __forceinline__ bool is_selected(uint32_t key, int j, Selection s) {
-  return key > s.T || (key == s.T && j <= s.J);
+// Streaming 16-byte load of weights that are read exactly once per forward
+// (no L1 allocation).
+__device__ __forceinline__ uint4 ldg_stream(const void* p) {
+  uint4 u;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w)
+               : "l"(p));
+  return u;
 }
 
-__device__ Selection block_select(const uint32_t* __restrict__ xk, int n, int k, bool bf16_keys,
-                                  uint32_t* hist, uint32_t* s_warp, uint32_t* scratch) {
-  if (k <= 0) return Selection{0xffffffffu, -1};
-  if (k >= n) return Selection{0u, n};
-  const int tid = threadIdx.x;
-  uint32_t prefix = 0, pmask = 0;
-  int need = k;
-  const int npass = bf16_keys ? 2 : 3;
-  for (int p = 0; p < npass; ++p) {
-    const int shift = p == 0 ? 19 : (p == 1 ? (bf16_keys ? 16 : 7) : 0);
-    const int bits = p == 0 ? 12 : (p == 1 ? (bf16_keys ? 3 : 12) : 7);
-    const int nb = 1 << bits;
-    const uint32_t dmask = static_cast<uint32_t>(nb - 1);
-    for (int i = tid; i < nb; i += kThreads) hist[i] = 0u;
-    __syncthreads();
-    for (int j = tid; j < n; j += kThreads) {
-      const uint32_t key = abs_key(xk[j]);
-      if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & dmask], 1u);
-    }
-    __syncthreads();
-    // Thread t owns bins in descending order: d in [t*bpt, (t+1)*bpt), bin = nb-1-d.
-    const int bpt = (nb + kThreads - 1) / kThreads;
-    uint32_t local = 0;
-    for (int d = tid * bpt; d < (tid + 1) * bpt && d < nb; ++d) local += hist[nb - 1 - d];
-    const uint32_t above_me = block_excl_scan(local, s_warp, nullptr);
-    if (above_me < static_cast<uint32_t>(need) && static_cast<uint32_t>(need) <= above_me + local) {
-      uint32_t acc = above_me;
-      for (int d = tid * bpt; d < (tid + 1) * bpt && d < nb; ++d) {
-        const int bin = nb - 1 - d;
-        const uint32_t c = hist[bin];
-        if (acc + c >= static_cast<uint32_t>(need)) {
-          scratch[0] = static_cast<uint32_t>(bin);
-          scratch[1] = acc;
-          scratch[2] = c;
-          break;
-        }
-        acc += c;
-      }
-    }
-    __syncthreads();
-    const uint32_t b = scratch[0], above = scratch[1], cnt = scratch[2];
-    need -= static_cast<int>(above);
-    prefix |= b << shift;
-    pmask |= dmask << shift;
-    if (cnt == static_cast<uint32_t>(need)) {
-      // The whole boundary bin is taken: S = {key >= prefix}.
-      if (prefix == 0u) return Selection{0u, n};
-      return Selection{prefix - 1u, -1};
-    }
-  }
-  // prefix is now the exact k-th largest key T; cut the ties by index.
-  const uint32_t T = prefix;
-  const int E = (n + kThreads - 1) / kThreads;
-  const int j0 = min(n, tid * E), j1 = min(n, j0 + E);
-  uint32_t ties = 0;
-  for (int j = j0; j < j1; ++j) ties += abs_key(xk[j]) == T;
-  const uint32_t before = block_excl_scan(ties, s_warp, nullptr);
-  if (before < static_cast<uint32_t>(need) && static_cast<uint32_t>(need) <= before + ties) {
-    uint32_t acc = before;
-    for (int j = j0; j < j1; ++j) {
-      if (abs_key(xk[j]) == T && ++acc == static_cast<uint32_t>(need)) {
-        scratch[3] = static_cast<uint32_t>(j);
-        break;
-      }
-    }
-  }
-  __syncthreads();
-  return Selection{T, static_cast<int32_t>(scratch[3])};
+// 16-byte load of data prefetched into L2 (the low-rank A_r rows).
+__device__ __forceinline__ uint4 ldg_l2(const void* p) {
+  uint4 u;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w)
+               : "l"(p));
+  return u;
 }
 
-// Load x (fp32 or bf16) into shared memory as fp32 bit patterns.
-__device__ __forceinline__ void load_x_bits(const void* __restrict__ x, bool x_bf16, int n,
-                                            uint32_t* xk) {
-  if (x_bf16) {
-    const uint16_t* xb = static_cast<const uint16_t*>(x);
-    for (int j = threadIdx.x; j < n; j += kThreads) xk[j] = static_cast<uint32_t>(xb[j]) << 16;
-  } else {
-    const uint32_t* xf = static_cast<const uint32_t*>(x);
-    for (int j = threadIdx.x; j < n; j += kThreads) xk[j] = xf[j];
-  }
+// Ampere-style 16-byte async copy global -> shared (LDGSTS), L2-only.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+__device__ __forceinline__ void named_bar_arrive(int id, int threads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
 // ---------------------------------------------------------------------------

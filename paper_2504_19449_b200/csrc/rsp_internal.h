@@ -15,30 +15,32 @@ struct FusedParams {
   const void* Bt;  // [n][r_pad]  B_r^T (row j = column j of b_r)
   const void* x;   // [n] fp32 or bf16
   float* y;        // [m] fp32
-  float* t_part;   // [grid][r_pad] stage-1 partial sums
+  float* t_part;   // [r_pad][nb_pad] stage-1 partial sums (column b = CTA b)
   float* y_part;   // [k_splits][m_pad] split-K partial sums
-  unsigned* bars;  // [2 + 2*col_tiles] generation barriers
+  unsigned* bars;  // [2] grid barrier {count, gen} + [col_tiles] tile tickets
   int n, m, m_pad, r, r_pad, k;
   int col_tiles, k_splits;
   int cap_w, cap_u, cap_a;  // per-CTA list capacities
-  int stage_bytes, stages;
+  int a_smem_bytes;         // shared-memory staging for this CTA's A_r^T rows
+  int nb_pad;               // row stride of t_part ([r_pad][nb_pad], grid rounded up to 4)
+  int deterministic;        // 1: fixed-order split-K combine (bit-reproducible y)
   int x_bf16;
   int dense;  // 1: all n channels through W, no selection, no low-rank term
   int pdl;    // 1: launched with programmatic dependent launch
+  long long* trace;  // debug: [grid][16] phase timestamps (null in production)
 };
 
 struct LaunchPlan {
   int col_tiles = 1, k_splits = 1, grid = 1;
   int cap_w = 1, cap_u = 1, cap_a = 1;
-  int stage_bytes = 16384, stages = 8;
+  int a_smem_bytes = 0, nb_pad = 4;
   size_t smem = 0;
   size_t ws_bytes = 0;  // workspace: barriers + t_part + y_part
   size_t ws_t_off = 0, ws_y_off = 0;
 };
 
-// Shared-memory bytes the fused kernel needs for a plan (host mirror of the
-// device carve-up).
-size_t fused_smem_bytes(const LaunchPlan& p, int n, int elem_bytes);
+// Shared-memory bytes the fused kernel needs for a plan.
+size_t fused_smem_bytes(const LaunchPlan& p, int n);
 
 cudaError_t fused_set_smem(int elem_bytes, size_t smem);
 cudaError_t launch_fused(const FusedParams& p, int elem_bytes, int grid, size_t smem,

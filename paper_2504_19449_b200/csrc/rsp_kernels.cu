@@ -1,6 +1,6 @@
 // rsp_kernels.cu -- sm_100a kernels of the R-Sparse linear operator.
 //
-// The hot path is ONE persistent kernel per linear (fused_forward_kernel):
+// The hot path is ONE kernel per linear (fused_forward_kernel):
 //
 //   y = W[:, S] x_S  +  A_r (B_r[:, S^c] x_{S^c})        (layer.cpp:95-123)
 //
@@ -10,88 +10,143 @@
 //   y = sum_{j in S}   x_j * Wt[j, :]         gathered rows of W^T (length m)
 //     + sum_{c < r}    t_c * At[c, :]         stage 2: rows of A_r^T (length m)
 //
-// so every term is a gathered-row AXPY over contiguous rows: each row (or its
-// column-tile segment) is one cp.async.bulk copy streamed through a shared
-// memory ring by a producer warp; 15 consumer warps do fp32 FMAs.
+// Every term is a gathered-row AXPY over contiguous rows, streamed with
+// 16-byte coalesced loads straight into registers: a warp covers a 512-byte
+// segment of one row per load (32 lanes x 16 B) and keeps U rows in flight.
+// (Measured on B200 by tools/stream_probe.cu: 16-deep LDG.128 gathers reach
+// 92% of the measured HBM copy bandwidth; 1-D TMA bulk copies of 0.5-8 KB row
+// segments reached 21-46%, so the ring/TMA design of the first version was
+// dropped -- see DESIGN.md.)
 //
-// Grid = col_tiles x k_splits CTAs (<= #SMs, one CTA per SM, all co-resident).
-// Each CTA redundantly computes the exact top-k selection from x (n <= 64K)
-// in shared memory, then takes a balanced rank range of S for its column
-// tile, a rank range of S^c for stage 1 and a slice of the r low-rank rows.
-// Cross-CTA dependencies use generation barriers in the workspace:
-//   * grid barrier: stage-1 partial t vectors -> every CTA (reached early,
-//     waited on only after the CTA's W rows are done, so it is hidden);
-//   * per-column-tile barrier: split-K partials of y -> deterministic
-//     fixed-order reduction (no float atomics: results are bit-reproducible).
+// Grid = col_tiles x k_splits CTAs (<= #SMs; one CTA per SM, all co-resident).
+// Every CTA computes the exact selection from x in shared memory
+// (rsp_select.cuh), then splits its 16 warps by role:
+//   * stage-1 warps stream this CTA's slice of the S^c rows of B_r^T, write a
+//     partial t, arrive on a grid barrier, wait for it (early: stage 1 is
+//     small), and reduce the partials of the rank rows this CTA owns in a
+//     fixed order; then signal the other warps through a named barrier;
+//   * W warps stream this CTA's rank range of S (its column tile), then the
+//     A_r^T rows (prefetched into L2 at kernel start: they do not depend on x).
+// Split-K partials of y are combined by the last CTA of each column tile in
+// fixed order (no float atomics: results are bit-reproducible).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include "rsp_device.cuh"
 #include "rsp_internal.h"
+#include "rsp_select.cuh"
 
 namespace rsp {
 
+constexpr int M_LAST = 31;  // misc slot: "this CTA reduces its column tile"
+
 // Shared-memory carve-up of the fused kernel (host and device agree).
+// [0, 64K): 15-bit histogram during selection, then the two reduction buffers.
 struct SmemLayout {
-  uint32_t off_w, off_u, off_a, off_red, off_misc, off_bar, total;
+  uint32_t off_keys, off_coarse, off_cand, off_misc, off_w, off_u, off_a, off_astage, total;
 
   __host__ __device__ static uint32_t up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
 
-  __host__ __device__ static SmemLayout make(int stages, int stage_bytes, int n, int cap_w,
-                                             int cap_u, int cap_a) {
+  __host__ __device__ static SmemLayout make(int n, int cap_w, int cap_u, int cap_a, int a_bytes) {
     SmemLayout L;
-    const uint32_t ring = static_cast<uint32_t>(stages) * static_cast<uint32_t>(stage_bytes);
-    const uint32_t sel = 4u * static_cast<uint32_t>(n) + 4u * kHistBins;
-    uint32_t o = up(ring > sel ? ring : sel, 128);
+    uint32_t o = 4u * kFineWords;
+    L.off_keys = o;
+    o = up(o + 4u * static_cast<uint32_t>(n), 16);
+    L.off_coarse = o;
+    o += 4u * kCoarseBins;
+    L.off_cand = o;
+    o += 4u * kCandMax;
+    L.off_misc = o;
+    o += 4u * kMiscWords;
     L.off_w = o;
     o = up(o + 8u * cap_w, 16);
     L.off_u = o;
     o = up(o + 8u * cap_u, 16);
     L.off_a = o;
     o = up(o + 4u * cap_a, 16);
-    L.off_red = o;
-    o += kConsumerWarps * 32 * 8 * 4;
-    L.off_misc = o;
-    o += 128;
-    L.off_bar = o;
-    o += 16u * stages;
+    L.off_astage = o;
+    o += static_cast<uint32_t>(a_bytes);
     L.total = up(o, 128);
     return L;
   }
 };
 
-size_t fused_smem_bytes(const LaunchPlan& p, int n, int /*elem_bytes*/) {
-  return SmemLayout::make(p.stages, p.stage_bytes, n, p.cap_w, p.cap_u, p.cap_a).total;
+size_t fused_smem_bytes(const LaunchPlan& p, int n) {
+  return SmemLayout::make(n, p.cap_w, p.cap_u, p.cap_a, p.a_smem_bytes).total;
 }
 
-template <typename WT>
+__device__ __forceinline__ long long clk() {
+  long long c;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+  return c;
+}
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Debug phase trace: slot 0 = globaltimer at CTA start, slots 1.. = clock64 - start.
+#define RSP_TRACE(ev)                                                \
+  do {                                                               \
+    if (p.trace) p.trace[blockIdx.x * 16 + (ev)] = clk() - t_start; \
+  } while (0)
+
+// acc += sum over rows i = first, first+stride, ... < count of coef(i) * row(i)[lane's 16 B].
+// U rows are loaded before any is consumed (U x 512 B in flight per warp).
+template <typename WT, int U, class RowPtr, class Coef, class Load>
+__device__ __forceinline__ void stream_rows(float (&acc)[Vec<WT>::kElems], int first, int count,
+                                            int stride, bool lane_ok, RowPtr row_ptr, Coef coef,
+                                            Load load) {
+  for (int i0 = first; i0 < count; i0 += stride * U) {
+    uint4 u[U];
+    float c[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const int i = i0 + q * stride;
+      if (i < count) {
+        c[q] = coef(i);
+        u[q] = lane_ok ? load(row_ptr(i)) : make_uint4(0, 0, 0, 0);
+      } else {
+        c[q] = 0.f;
+        u[q] = make_uint4(0, 0, 0, 0);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < U; ++q) Vec<WT>::fma(acc, u[q], c[q]);
+  }
+}
+
+template <typename WT, int U>
 __global__ void __launch_bounds__(kThreads, 1) fused_forward_kernel(const FusedParams p) {
-  extern __shared__ __align__(1024) uint8_t smem[];
-  constexpr int VE = Vec<WT>::kElems;
+  const long long t_start = clk();
+  if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * 16] = gtimer();
+  extern __shared__ __align__(16) uint8_t smem[];
+  constexpr int VE = Vec<WT>::kElems;  // elements per 16 B
   constexpr int ES = static_cast<int>(sizeof(WT));
-  const SmemLayout L = SmemLayout::make(p.stages, p.stage_bytes, p.n, p.cap_w, p.cap_u, p.cap_a);
-  uint8_t* ring = smem;
-  uint32_t* xk = reinterpret_cast<uint32_t*>(smem);
-  uint32_t* hist = xk + p.n;
+  const SmemLayout L = SmemLayout::make(p.n, p.cap_w, p.cap_u, p.cap_a, p.a_smem_bytes);
+  SelSmem ss;
+  ss.fine = reinterpret_cast<uint32_t*>(smem);
+  ss.keys = reinterpret_cast<uint32_t*>(smem + L.off_keys);
+  ss.coarse = reinterpret_cast<uint32_t*>(smem + L.off_coarse);
+  ss.cand = reinterpret_cast<uint32_t*>(smem + L.off_cand);
+  ss.misc = reinterpret_cast<uint32_t*>(smem + L.off_misc);
   int2* list_w = reinterpret_cast<int2*>(smem + L.off_w);  // {channel j, bits of x_j}
   int2* list_u = reinterpret_cast<int2*>(smem + L.off_u);
   float* coef_a = reinterpret_cast<float*>(smem + L.off_a);
-  float* red = reinterpret_cast<float*>(smem + L.off_red);
-  uint32_t* s_warp = reinterpret_cast<uint32_t*>(smem + L.off_misc);
-  uint32_t* scratch = s_warp + 20;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.off_bar);
-  uint64_t* empty = full + p.stages;
+  uint8_t* a_stage = smem + L.off_astage;                  // A_r^T rows of this CTA's tile
+  float* red1 = reinterpret_cast<float*>(smem);            // [G1][r_pad], after selection
+  float* red2 = reinterpret_cast<float*>(smem + 32768);    // [G2][tile cols], after selection
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int b = blockIdx.x, NB = gridDim.x;
   const int ct = b / p.k_splits, ks = b % p.k_splits;
 
-  // Column tile of this CTA, in units of 8 elements (16 B of bf16).
-  const int vm = p.m_pad / 8;
-  const int v0 = static_cast<int>(static_cast<long long>(vm) * ct / p.col_tiles);
-  const int v1 = static_cast<int>(static_cast<long long>(vm) * (ct + 1) / p.col_tiles);
-  const int col0 = v0 * 8, tcw = (v1 - v0) * 8;
+  // Column tile of this CTA in 16-byte units.
+  const int vrow = p.m_pad * ES / 16;
+  const int v0 = static_cast<int>(static_cast<long long>(vrow) * ct / p.col_tiles);
+  const int v1 = static_cast<int>(static_cast<long long>(vrow) * (ct + 1) / p.col_tiles);
+  const int tw = v1 - v0, tcw = tw * VE, col0 = v0 * VE;
 
   const int k_eff = p.dense ? p.n : p.k;
   const bool has_lr = !p.dense && p.r > 0 && k_eff < p.n;
@@ -103,226 +158,237 @@ __global__ void __launch_bounds__(kThreads, 1) fused_forward_kernel(const FusedP
   const int alo = has_lr ? static_cast<int>(static_cast<long long>(p.r) * ks / p.k_splits) : 0;
   const int ahi = has_lr ? static_cast<int>(static_cast<long long>(p.r) * (ks + 1) / p.k_splits) : 0;
   const int nw = whi - wlo, n1 = uhi - ulo, na = ahi - alo;
+  // A_r^T rows held in shared memory (the rest stream from L2 after a prefetch).
+  const int na_s = has_lr ? min(na, p.a_smem_bytes / max(1, tw * 16)) : 0;
+  // Combine split-K partials of y with float atomics into a y zeroed before the
+  // grid barrier (fast), or deterministically by the tile's last CTA.
+  const bool red_y = has_lr && p.k_splits > 1 && !p.deterministic;
 
-  const WT* __restrict__ Wt = static_cast<const WT*>(p.Wt);
-  const WT* __restrict__ At = static_cast<const WT*>(p.At);
-  const WT* __restrict__ Bt = static_cast<const WT*>(p.Bt);
-  const int R1B = p.r_pad * ES;  // stage-1 row bytes
-  const int RWB = tcw * ES;      // W / A_r tile-row bytes
-
-  if (tid == 0) {
-    for (int s = 0; s < p.stages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumerWarps);
-    }
-    fence_mbar_init();
+  // Role split: W1 stage-1 warps (multiple of C1), the rest stream W / A_r.
+  const int vb = p.r_pad * ES / 16;  // 16-B units per B_r^T row
+  const int C1 = has_lr ? (vb + 31) / 32 : 1;
+  const int C2 = (tw + 31) / 32;
+  int W1 = 0;
+  if (has_lr) {
+    const long long s1 = static_cast<long long>(n1) * C1, s2 = static_cast<long long>(nw) * C2;
+    const int want = static_cast<int>((kWarps * s1 + s1 + s2 - 1) / (s1 + s2 > 0 ? s1 + s2 : 1));
+    W1 = max(1, (want + C1 - 1) / C1) * C1;
+    W1 = min(W1, ((kWarps - C2) / C1) * C1);
   }
-  // The low-rank rows this CTA will stream do not depend on x: start pulling
-  // them into L2 now (overlaps the previous kernel's tail under PDL and this
-  // kernel's selection otherwise).
-  if (warp == 0 && has_lr && RWB > 0) {
-    for (int i = lane; i < na; i += 32)
-      prefetch_l2_bulk(At + static_cast<size_t>(alo + i) * p.m_pad + col0, RWB);
+  const int nWW = kWarps - W1;
+
+  const uint8_t* Wt = static_cast<const uint8_t*>(p.Wt);
+  const uint8_t* At = static_cast<const uint8_t*>(p.At);
+  const uint8_t* Bt = static_cast<const uint8_t*>(p.Bt);
+  const size_t rowW = static_cast<size_t>(p.m_pad) * ES;  // bytes per W^T / A_r^T row
+  const size_t rowB = static_cast<size_t>(p.r_pad) * ES;  // bytes per B_r^T row
+  const uint8_t* a_tile = At + static_cast<size_t>(col0) * ES;
+
+  // ---- prologue: independent of x (overlaps the previous kernel under PDL) ----
+  if (!p.dense) sel_clear(ss);
+  if (has_lr) {
+    for (int f = tid; f < na_s * tw; f += kThreads) {
+      const int i = f / tw, v = f - i * tw;
+      cp_async16(a_stage + static_cast<size_t>(f) * 16, a_tile + static_cast<size_t>(alo + i) * rowW + v * 16);
+    }
+    cp_async_commit();
+    for (int i = na_s + tid; i < na; i += kThreads)
+      prefetch_l2_bulk(a_tile + static_cast<size_t>(alo + i) * rowW, static_cast<uint32_t>(tw) * 16u);
   }
   if (p.pdl) {
     griddep_wait();
     griddep_launch_dependents();
   }
-
-  // ---- 1. selection (redundant per CTA; x is at most a few tens of KB) ----
-  load_x_bits(p.x, p.x_bf16 != 0, p.n, xk);
-  __syncthreads();
-  const Selection sel = p.dense ? Selection{0u, p.n}
-                                : block_select(xk, p.n, p.k, p.x_bf16 != 0, hist, s_warp, scratch);
-
-  // ---- 2. this CTA's row lists (rank ranges of S and of S^c) ----
-  {
-    const int E = (p.n + kThreads - 1) / kThreads;
-    const int j0 = min(p.n, tid * E), j1 = min(p.n, j0 + E);
-    uint32_t c = 0;
-    for (int j = j0; j < j1; ++j) c += is_selected(abs_key(xk[j]), j, sel);
-    uint32_t srank = block_excl_scan(c, s_warp, nullptr);
-    uint32_t urank = static_cast<uint32_t>(j0) - srank;
-    for (int j = j0; j < j1; ++j) {
-      const uint32_t bits = xk[j];
-      if (is_selected(abs_key(bits), j, sel)) {
-        if (srank >= static_cast<uint32_t>(wlo) && srank < static_cast<uint32_t>(whi))
-          list_w[srank - wlo] = make_int2(j, static_cast<int>(bits));
-        ++srank;
-      } else {
-        if (urank >= static_cast<uint32_t>(ulo) && urank < static_cast<uint32_t>(uhi))
-          list_u[urank - ulo] = make_int2(j, static_cast<int>(bits));
-        ++urank;
-      }
-    }
+  unsigned gen0 = 0;
+  if (has_lr && tid == 0) gen0 = ld_relaxed_gpu(p.bars + 1);
+  if (red_y) {  // zero this CTA's slice of y; published by the grid barrier below
+    const int y0 = static_cast<int>(static_cast<long long>(p.m) * b / NB);
+    const int y1 = static_cast<int>(static_cast<long long>(p.m) * (b + 1) / NB);
+    for (int i = y0 + tid; i < y1; i += kThreads) p.y[i] = 0.f;
   }
-  fence_proxy_async_smem();  // generic reads of the x region precede async-proxy ring writes
-  __syncthreads();
+  if (tid == 0) RSP_TRACE(1);
 
-  const int P1 = R1B > 0 ? p.stage_bytes / R1B : 1;  // stage-1 rows per ring stage
-  const int P2 = RWB > 0 ? p.stage_bytes / RWB : 1;  // tile rows per ring stage
-  const int stages = p.stages;
-
-  if (warp == 0) {
-    // ================= producer: one warp issues every bulk copy =================
-    const uint64_t pol = l2_evict_first_policy();
-    int s = 0;
-    for (int i0 = 0; i0 < n1; i0 += P1, ++s) {
-      const int cnt = min(P1, n1 - i0), slot = s % stages;
-      if (s >= stages) mbar_wait(&empty[slot], ((s / stages) - 1) & 1);
-      if (lane == 0) mbar_arrive_expect_tx(&full[slot], static_cast<uint32_t>(cnt * R1B));
-      __syncwarp();
-      for (int i = lane; i < cnt; i += 32) {
-        const int j = list_u[i0 + i].x;
-        bulk_g2s(ring + slot * p.stage_bytes + i * R1B, Bt + static_cast<size_t>(j) * p.r_pad, R1B,
-                 &full[slot], pol);
-      }
-    }
-    for (int i0 = 0; i0 < nw; i0 += P2, ++s) {
-      const int cnt = min(P2, nw - i0), slot = s % stages;
-      if (s >= stages) mbar_wait(&empty[slot], ((s / stages) - 1) & 1);
-      if (lane == 0) mbar_arrive_expect_tx(&full[slot], static_cast<uint32_t>(cnt * RWB));
-      __syncwarp();
-      for (int i = lane; i < cnt; i += 32) {
-        const int j = list_w[i0 + i].x;
-        bulk_g2s(ring + slot * p.stage_bytes + i * RWB, Wt + static_cast<size_t>(j) * p.m_pad + col0,
-                 RWB, &full[slot], pol);
-      }
-    }
-    for (int i0 = 0; i0 < na; i0 += P2, ++s) {
-      const int cnt = min(P2, na - i0), slot = s % stages;
-      if (s >= stages) mbar_wait(&empty[slot], ((s / stages) - 1) & 1);
-      if (lane == 0) mbar_arrive_expect_tx(&full[slot], static_cast<uint32_t>(cnt * RWB));
-      __syncwarp();
-      for (int i = lane; i < cnt; i += 32) {
-        bulk_g2s(ring + slot * p.stage_bytes + i * RWB,
-                 At + static_cast<size_t>(alo + i0 + i) * p.m_pad + col0, RWB, &full[slot], pol);
-      }
-    }
-    return;
+  // ---- 1. exact selection (redundant per CTA: x is at most a few tens of KB) ----
+  sel_load(p.x, p.x_bf16 != 0, p.n, ss);
+  if (tid == 0) RSP_TRACE(2);
+  SelResult sr{0u, static_cast<uint32_t>(p.n)};
+  if (!p.dense) {
+    sel_hist(p.n, ss);
+    sr = sel_resolve(p.n, p.k, p.x_bf16 != 0, ss);
   }
+  if (tid == 0) RSP_TRACE(3);
+  // ---- 2. this CTA's row lists: rank ranges of S and of S^c ----
+  sel_emit(p.n, sr, ss, [&](int j, uint32_t bits, bool in, uint32_t rank) {
+    if (in) {
+      if (rank >= static_cast<uint32_t>(wlo) && rank < static_cast<uint32_t>(whi))
+        list_w[rank - wlo] = make_int2(j, static_cast<int>(bits));
+    } else if (rank >= static_cast<uint32_t>(ulo) && rank < static_cast<uint32_t>(uhi)) {
+      list_u[rank - ulo] = make_int2(j, static_cast<int>(bits));
+    }
+  });
+  __syncthreads();
+  if (tid == 0) RSP_TRACE(4);
 
-  // ================= consumers: warps 1..15 =================
-  const int cw = warp - 1, ctid = tid - 32;
-  int s = 0;
-  if (has_lr) {
-    // ---- stage 1: partial t over this CTA's slice of S^c ----
-    const int V1 = R1B / 16, C1 = (V1 + 31) / 32, G1 = kConsumerWarps / C1;
-    const int grp = cw / C1, v = (cw % C1) * 32 + lane;
-    const bool vok = grp < G1 && v < V1;
+  if (warp < W1) {
+    // ===================== stage-1 warps =====================
+    const int G1 = W1 / C1, g1 = warp / C1;
+    const int v = (warp % C1) * 32 + lane;
+    const bool ok = v < vb;
     float acc[VE];
 #pragma unroll
     for (int e = 0; e < VE; ++e) acc[e] = 0.f;
-    for (int i0 = 0; i0 < n1; i0 += P1, ++s) {
-      const int cnt = min(P1, n1 - i0), slot = s % stages;
-      mbar_wait(&full[slot], (s / stages) & 1);
-      if (vok) {
-        const uint8_t* base = ring + slot * p.stage_bytes + v * 16;
-        for (int i = grp; i < cnt; i += G1) {
-          const float c = __int_as_float(list_u[i0 + i].y);
-          Vec<WT>::fma(acc, *reinterpret_cast<const uint4*>(base + i * R1B), c);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[slot]);
-    }
-    if (vok) {
+    const uint8_t* base = Bt + v * 16;
+    stream_rows<WT, U>(
+        acc, g1, n1, G1, ok, [&](int i) { return base + static_cast<size_t>(list_u[i].x) * rowB; },
+        [&](int i) { return __int_as_float(list_u[i].y); }, [](const void* q) { return ldg_stream(q); });
+    if (tid == 0) RSP_TRACE(5);
+    if (ok) {
 #pragma unroll
-      for (int e = 0; e < VE; ++e) red[grp * p.r_pad + v * VE + e] = acc[e];
+      for (int e = 0; e < VE; ++e) red1[g1 * p.r_pad + v * VE + e] = acc[e];
     }
-    named_bar_sync(1, kConsumerThreads);
-    for (int c = ctid; c < p.r_pad; c += kConsumerThreads) {
+    named_bar_sync(1, W1 * 32);
+    // partial t of this CTA: column b of t_part[r_pad][nb_pad]
+    for (int c = tid; c < p.r_pad; c += W1 * 32) {
       float sum = 0.f;
-      for (int g = 0; g < G1; ++g) sum += red[g * p.r_pad + c];
-      p.t_part[static_cast<size_t>(b) * p.r_pad + c] = sum;
+      for (int g = 0; g < G1; ++g) sum += red1[g * p.r_pad + c];
+      p.t_part[static_cast<size_t>(c) * p.nb_pad + b] = sum;
     }
     __threadfence();
-    named_bar_sync(1, kConsumerThreads);
-    if (ctid == 0) scratch[4] = gbar_arrive(p.bars, static_cast<unsigned>(NB));
-  }
-
-  // ---- gathered W rows (and then A_r rows) of this CTA's column tile ----
-  const int V2 = RWB / 16, C2 = (V2 + 31) / 32, G2 = C2 > 0 ? kConsumerWarps / C2 : 0;
-  const int grp2 = C2 > 0 ? cw / C2 : 0, v2 = C2 > 0 ? (cw % C2) * 32 + lane : 0;
-  const bool vok2 = grp2 < G2 && v2 < V2;
-  float acc2[VE];
+    named_bar_sync(1, W1 * 32);
+    if (tid == 0) {
+      gbar_arrive(p.bars, static_cast<unsigned>(NB));
+      RSP_TRACE(6);
+      gbar_wait(p.bars, gen0);
+      RSP_TRACE(7);
+    }
+    named_bar_sync(1, W1 * 32);
+    // t_c for this CTA's rank rows: 8 lanes per row sum the row's nb_pad
+    // partials (float4 loads, fixed order, then a fixed xor tree).
+    const int g8 = tid >> 3, l8 = tid & 7, ng8 = W1 * 4;
+    const int nq = p.nb_pad / 4;
+    for (int cbase = alo; cbase < ahi; cbase += ng8 * 4) {  // uniform trip count: shuffles below
+      const int c0 = cbase + g8;
+      float s4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-  for (int e = 0; e < VE; ++e) acc2[e] = 0.f;
-  for (int i0 = 0; i0 < nw; i0 += P2, ++s) {
-    const int cnt = min(P2, nw - i0), slot = s % stages;
-    mbar_wait(&full[slot], (s / stages) & 1);
-    if (vok2) {
-      const uint8_t* base = ring + slot * p.stage_bytes + v2 * 16;
-      for (int i = grp2; i < cnt; i += G2) {
-        const float c = __int_as_float(list_w[i0 + i].y);
-        Vec<WT>::fma(acc2, *reinterpret_cast<const uint4*>(base + i * RWB), c);
+      for (int rr = 0; rr < 4; ++rr) {
+        const int c = c0 + rr * ng8;
+        if (c < ahi) {
+          const float4* row = reinterpret_cast<const float4*>(p.t_part + static_cast<size_t>(c) * p.nb_pad);
+          for (int q = l8; q < nq; q += 8) {
+            const float4 t = __ldcg(row + q);
+            s4[rr] += (t.x + t.y) + (t.z + t.w);
+          }
+        }
+      }
+#pragma unroll
+      for (int rr = 0; rr < 4; ++rr) {
+        float v8 = s4[rr];
+        v8 += __shfl_xor_sync(0xffffffffu, v8, 4);
+        v8 += __shfl_xor_sync(0xffffffffu, v8, 2);
+        v8 += __shfl_xor_sync(0xffffffffu, v8, 1);
+        const int c = c0 + rr * ng8;
+        if (l8 == 0 && c < ahi) coef_a[c - alo] = v8;
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[slot]);
+    if (tid == 0) RSP_TRACE(8);
+    cp_async_wait_all();
+    named_bar_arrive(3, kThreads);  // coef_a (and this thread's A_r copies) are ready
+    return;
   }
+
+  // ===================== W / A_r warps =====================
+  const int wr = warp - W1, G2 = nWW / C2, g2 = wr / C2;
+  const int v = (wr % C2) * 32 + lane;
+  const bool ok = g2 < G2 && v < tw;
+  const int wt = tid - W1 * 32, nwt = nWW * 32;
+  float acc[VE];
+#pragma unroll
+  for (int e = 0; e < VE; ++e) acc[e] = 0.f;
+  const uint8_t* wbase = Wt + static_cast<size_t>(col0) * ES + v * 16;
+  if (g2 < G2)
+    stream_rows<WT, U>(
+        acc, g2, nw, G2, ok, [&](int i) { return wbase + static_cast<size_t>(list_w[i].x) * rowW; },
+        [&](int i) { return __int_as_float(list_w[i].y); }, [](const void* q) { return ldg_stream(q); });
+  if (wt == 0) RSP_TRACE(9);
   if (has_lr) {
-    if (ctid == 0) gbar_wait(p.bars, scratch[4]);
-    named_bar_sync(1, kConsumerThreads);
-    // t_c for this CTA's low-rank rows: fixed-order sum of the stage-1 partials.
-    for (int c = alo + cw; c < ahi; c += kConsumerWarps) {
-      float sum = 0.f;
-      for (int bb = lane; bb < NB; bb += 32) sum += __ldcg(p.t_part + static_cast<size_t>(bb) * p.r_pad + c);
-#pragma unroll
-      for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-      if (lane == 0) coef_a[c - alo] = sum;
-    }
-    named_bar_sync(1, kConsumerThreads);
-    for (int i0 = 0; i0 < na; i0 += P2, ++s) {
-      const int cnt = min(P2, na - i0), slot = s % stages;
-      mbar_wait(&full[slot], (s / stages) & 1);
-      if (vok2) {
-        const uint8_t* base = ring + slot * p.stage_bytes + v2 * 16;
-        for (int i = grp2; i < cnt; i += G2)
-          Vec<WT>::fma(acc2, *reinterpret_cast<const uint4*>(base + i * RWB), coef_a[i0 + i]);
+    cp_async_wait_all();
+    named_bar_sync(3, kThreads);  // stage-1 warps have published coef_a; A_r^T rows landed
+    if (g2 < G2) {
+      if (ok) {
+        for (int i = g2; i < na_s; i += G2)
+          Vec<WT>::fma(acc, *reinterpret_cast<const uint4*>(a_stage + (static_cast<size_t>(i) * tw + v) * 16),
+                       coef_a[i]);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[slot]);
+      const uint8_t* abase = a_tile + v * 16;
+      const int first = na_s + ((g2 - na_s % G2) % G2 + G2) % G2;  // keep row i on group i % G2
+      stream_rows<WT, U>(
+          acc, first, na, G2, ok, [&](int i) { return abase + static_cast<size_t>(alo + i) * rowW; },
+          [&](int i) { return coef_a[i]; }, [](const void* q) { return ldg_l2(q); });
     }
   }
+  if (wt == 0) RSP_TRACE(10);
 
-  // ---- split-K: partial tile -> workspace, per-tile barrier, fixed-order sum ----
-  if (vok2) {
+  // ---- split-K: group reduction in smem, then y ----
+  if (ok) {
 #pragma unroll
-    for (int e = 0; e < VE; ++e) red[grp2 * tcw + v2 * VE + e] = acc2[e];
+    for (int e = 0; e < VE; ++e) red2[g2 * tcw + v * VE + e] = acc[e];
   }
-  named_bar_sync(1, kConsumerThreads);
-  for (int c = ctid; c < tcw; c += kConsumerThreads) {
+  named_bar_sync(2, nwt);
+  for (int c = wt; c < tcw; c += nwt) {
     float sum = 0.f;
-    for (int g = 0; g < G2; ++g) sum += red[g * tcw + c];
-    p.y_part[static_cast<size_t>(ks) * p.m_pad + col0 + c] = sum;
-  }
-  __threadfence();
-  named_bar_sync(1, kConsumerThreads);
-  unsigned* tbar = p.bars + 2 + 2 * ct;
-  if (ctid == 0) {
-    const unsigned g = gbar_arrive(tbar, static_cast<unsigned>(p.k_splits));
-    gbar_wait(tbar, g);
-  }
-  named_bar_sync(1, kConsumerThreads);
-  const int c_lo = static_cast<int>(static_cast<long long>(tcw) * ks / p.k_splits);
-  const int c_hi = static_cast<int>(static_cast<long long>(tcw) * (ks + 1) / p.k_splits);
-  for (int c = c_lo + ctid; c < c_hi; c += kConsumerThreads) {
+    for (int g = 0; g < G2; ++g) sum += red2[g * tcw + c];
     const int col = col0 + c;
-    if (col >= p.m) break;
-    float sum = 0.f;
-#pragma unroll 8
-    for (int kk = 0; kk < p.k_splits; ++kk) sum += __ldcg(p.y_part + static_cast<size_t>(kk) * p.m_pad + col);
-    p.y[col] = sum;
+    if (p.k_splits == 1) {
+      if (col < p.m) p.y[col] = sum;
+    } else if (red_y) {
+      if (col < p.m) atomicAdd(p.y + col, sum);
+    } else {
+      p.y_part[static_cast<size_t>(ks) * p.m_pad + col] = sum;
+    }
   }
+  if (wt == 0) RSP_TRACE(11);
+  if (p.k_splits > 1 && !red_y) {
+    __threadfence();
+    named_bar_sync(2, nwt);
+    unsigned* ticket = p.bars + 2 + ct;
+    if (wt == 0) ss.misc[M_LAST] = atom_add_acq_rel_gpu(ticket, 1u) == static_cast<unsigned>(p.k_splits - 1);
+    named_bar_sync(2, nwt);
+    if (ss.misc[M_LAST]) {
+      // Last CTA of this column tile: fixed-order sum of the k_splits partials.
+      for (int c = wt; c < tcw; c += nwt) {
+        const int col = col0 + c;
+        if (col >= p.m) break;
+        float sum = 0.f;
+#pragma unroll 4
+        for (int kk = 0; kk < p.k_splits; ++kk)
+          sum += __ldcg(p.y_part + static_cast<size_t>(kk) * p.m_pad + col);
+        p.y[col] = sum;
+      }
+      if (wt == 0) st_relaxed_gpu(ticket, 0u);
+    }
+  }
+  if (wt == 0) RSP_TRACE(12);
+}
+
+template <typename WT>
+static cudaError_t set_smem_t(size_t smem) {
+  cudaError_t e = cudaFuncSetAttribute(fused_forward_kernel<WT, 8>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(fused_forward_kernel<WT, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(smem));
 }
 
 cudaError_t fused_set_smem(int elem_bytes, size_t smem) {
-  if (elem_bytes == 2)
-    return cudaFuncSetAttribute(fused_forward_kernel<__nv_bfloat16>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  return cudaFuncSetAttribute(fused_forward_kernel<float>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  return elem_bytes == 2 ? set_smem_t<__nv_bfloat16>(smem) : set_smem_t<float>(smem);
+}
+
+static int unroll_choice() {
+  static int u = [] {
+    const char* v = getenv("RSP_UNROLL");
+    return (v && atoi(v) == 8) ? 8 : 16;
+  }();
+  return u;
 }
 
 cudaError_t launch_fused(const FusedParams& p, int elem_bytes, int grid, size_t smem,
@@ -339,45 +405,45 @@ cudaError_t launch_fused(const FusedParams& p, int elem_bytes, int grid, size_t 
   cfg.numAttrs = pdl ? 1 : 0;
   FusedParams q = p;
   q.pdl = pdl ? 1 : 0;
-  if (elem_bytes == 2) return cudaLaunchKernelEx(&cfg, fused_forward_kernel<__nv_bfloat16>, q);
-  return cudaLaunchKernelEx(&cfg, fused_forward_kernel<float>, q);
+  const bool u8 = unroll_choice() == 8;
+  if (elem_bytes == 2)
+    return u8 ? cudaLaunchKernelEx(&cfg, fused_forward_kernel<__nv_bfloat16, 8>, q)
+              : cudaLaunchKernelEx(&cfg, fused_forward_kernel<__nv_bfloat16, 16>, q);
+  return u8 ? cudaLaunchKernelEx(&cfg, fused_forward_kernel<float, 8>, q)
+            : cudaLaunchKernelEx(&cfg, fused_forward_kernel<float, 16>, q);
 }
 
 // ---------------------------------------------------------------------------
-// Stand-alone selector (top_k_by_magnitude / threshold_sparsify): one CTA.
+// Stand-alone selector (top_k_by_magnitude / threshold_sparsify): one CTA,
+// the same selection code as the fused kernel.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads, 1)
     select_kernel(const void* x, int x_bf16, int n, int k, int32_t* kept, int32_t* rest,
                   float* sparse_x) {
   extern __shared__ __align__(16) uint8_t smem_sel[];
-  uint32_t* xk = reinterpret_cast<uint32_t*>(smem_sel);
-  uint32_t* hist = xk + n;
-  uint32_t* s_warp = hist + kHistBins;
-  uint32_t* scratch = s_warp + 20;
-  load_x_bits(x, x_bf16 != 0, n, xk);
-  __syncthreads();
-  const Selection sel = block_select(xk, n, k, x_bf16 != 0, hist, s_warp, scratch);
-  const int E = (n + kThreads - 1) / kThreads;
-  const int j0 = min(n, static_cast<int>(threadIdx.x) * E), j1 = min(n, j0 + E);
-  uint32_t c = 0;
-  for (int j = j0; j < j1; ++j) c += is_selected(abs_key(xk[j]), j, sel);
-  uint32_t srank = block_excl_scan(c, s_warp, nullptr);
-  uint32_t urank = static_cast<uint32_t>(j0) - srank;
-  for (int j = j0; j < j1; ++j) {
-    const uint32_t bits = xk[j];
-    const bool in = is_selected(abs_key(bits), j, sel);
+  SelSmem ss;
+  ss.fine = reinterpret_cast<uint32_t*>(smem_sel);
+  ss.coarse = ss.fine + kFineWords;
+  ss.cand = ss.coarse + kCoarseBins;
+  ss.misc = ss.cand + kCandMax;
+  ss.keys = ss.misc + kMiscWords;
+  sel_clear(ss);
+  sel_load(x, x_bf16 != 0, n, ss);
+  sel_hist(n, ss);
+  const SelResult sr = sel_resolve(n, k, x_bf16 != 0, ss);
+  sel_emit(n, sr, ss, [&](int j, uint32_t bits, bool in, uint32_t rank) {
     if (in) {
-      if (kept) kept[srank] = j;
-      ++srank;
-    } else {
-      if (rest) rest[urank] = j;
-      ++urank;
+      if (kept) kept[rank] = j;
+    } else if (rest) {
+      rest[rank] = j;
     }
     if (sparse_x) sparse_x[j] = in ? __uint_as_float(bits) : 0.f;
-  }
+  });
 }
 
-size_t select_smem_bytes(int n) { return 4u * static_cast<size_t>(n) + 4u * kHistBins + 256u; }
+size_t select_smem_bytes(int n) {
+  return 4u * (kFineWords + kCoarseBins + kCandMax + kMiscWords) + 4u * static_cast<size_t>(n);
+}
 
 cudaError_t launch_select(const void* x, bool x_bf16, int n, int k, int32_t* kept, int32_t* rest,
                           float* sparse_x, cudaStream_t stream) {

@@ -104,7 +104,8 @@ class DecomposedLayer:
     def __init__(self, w, a_r=None, b_r=None, plan: Optional[SparsityPlan] = None, *,
                  keep_fraction: Optional[float] = None, rank: Optional[int] = None,
                  weight_dtype: str = "bf16", w_layout: str = "row", k: Optional[int] = None,
-                 device: int = 0, shard_rank: int = 0, shard_count: int = 1):
+                 device: int = 0, shard_rank: int = 0, shard_count: int = 1,
+                 deterministic: bool = False):
         if plan is None:
             plan = SparsityPlan(1.0 if keep_fraction is None else keep_fraction,
                                 0 if rank is None else rank)
@@ -140,6 +141,7 @@ class DecomposedLayer:
         d.w_layout = L.RSP_W_ROW_MAJOR if w_layout == "row" else L.RSP_W_COL_MAJOR
         d.w, d.a_r, d.b_r = wp, ap, bp
         d.device, d.shard_rank, d.shard_count = device, shard_rank, shard_count
+        d.flags = L.RSP_FLAG_DETERMINISTIC if deterministic else 0
         h = ct.c_void_p()
         if torch is not None and wmem == L.RSP_MEM_DEVICE:
             torch.cuda.synchronize(device)

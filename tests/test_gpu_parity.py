@@ -223,7 +223,8 @@ def test_full_size_config1_bf16(coracle, cuda, name, m, n):
 def test_scaling_property_full_size(cuda):
     # power-of-two scaling keeps the selection and scales every product exactly
     c = wl.config1_layer("gate_proj", 11008, 4096, device="cuda")
-    layer = rsp.DecomposedLayer(c["w"], c["a_r"], c["b_r"], rsp.SparsityPlan(0.5, c["rank"]))
+    layer = rsp.DecomposedLayer(c["w"], c["a_r"], c["b_r"], rsp.SparsityPlan(0.5, c["rank"]),
+                                deterministic=True)
     y1 = layer.forward(c["x"])
     y2 = layer.forward(c["x"] * 4.0)
     assert torch.equal(y2, y1 * 4.0)
@@ -231,9 +232,13 @@ def test_scaling_property_full_size(cuda):
 
 def test_deterministic_and_host_path(cuda):
     c = wl.config1_layer("down_proj", 4096, 11008, device="cuda")
-    layer = rsp.DecomposedLayer(c["w"], c["a_r"], c["b_r"], rsp.SparsityPlan(0.5, c["rank"]))
+    layer = rsp.DecomposedLayer(c["w"], c["a_r"], c["b_r"], rsp.SparsityPlan(0.5, c["rank"]),
+                                deterministic=True)
     ys = [layer.forward(c["x"]).clone() for _ in range(5)]
-    assert all(torch.equal(ys[0], y) for y in ys[1:])  # no float atomics: bit-reproducible
+    assert all(torch.equal(ys[0], y) for y in ys[1:])  # fixed-order combine: bit-reproducible
+    fast = rsp.DecomposedLayer(c["w"], c["a_r"], c["b_r"], rsp.SparsityPlan(0.5, c["rank"]))
+    for _ in range(3):  # float-atomic combine: same value up to summation order
+        assert maxrel(fast.forward(c["x"]).cpu().numpy(), ys[0].cpu().numpy()) <= 1e-6
     yh = layer.forward_host(c["x"].cpu().numpy())
     assert np.array_equal(yh, ys[0].cpu().numpy().astype(np.float64))
     xb = c["x"].to(torch.bfloat16)
@@ -248,7 +253,7 @@ def test_batch_is_per_token(cuda):
     X = torch.stack([torch.from_numpy(wl.heavy_tailed_x(4096, rng)) for _ in range(4)]).to(cuda)
     Y = layer.forward(X)
     for t in range(4):
-        assert torch.equal(Y[t], layer.forward(X[t]))
+        assert maxrel(Y[t].cpu().numpy(), layer.forward(X[t]).cpu().numpy()) <= 1e-6
 
 
 def test_shards_concatenate_to_full(cuda):
@@ -315,4 +320,4 @@ def test_stack_graph_matches_individual_forwards(cuda):
         st.launch()
     torch.cuda.synchronize()
     for l, x, y in zip(layers, xs, ys):
-        assert torch.equal(y, l.forward(x))
+        assert maxrel(y.cpu().numpy(), l.forward(x).cpu().numpy()) <= 1e-6
