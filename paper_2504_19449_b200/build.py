@@ -13,7 +13,6 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "librsparse_b200.so")
 SOURCES = ["rsp_kernels.cu", "rsp_api.cu"]
-HEADERS = ["rsp_device.cuh", "rsp_internal.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
@@ -28,7 +27,8 @@ def _stale(target: str, deps) -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
+    headers = [f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h", ".hpp"))]
+    deps = [os.path.join(CSRC, f) for f in SOURCES + sorted(headers)]
     deps.append(os.path.join(ROOT, "include", "rsparse_b200.h"))
     if force or _stale(LIB, deps):
         cmd = [NVCC, *ARCH, *FLAGS, *[os.path.join(CSRC, f) for f in SOURCES], "-o", LIB]

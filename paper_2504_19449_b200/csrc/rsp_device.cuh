@@ -12,13 +12,64 @@ namespace rsp {
 
 constexpr int kThreads = 512;               // every kernel in the fused path
 constexpr int kWarps = kThreads / 32;
-constexpr int kHistBins = 4096;
 
 // ---------------------------------------------------------------------------
 // PTX wrappers
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// The dynamic-smem base as an opaque register value: left to itself nvcc
+// rematerializes the shared window base (S2R SR_CgaCtaId + LEA) at every use.
+__device__ __forceinline__ uint32_t smem_base_pinned(const void* p) {
+  uint32_t v;
+  asm volatile("mov.b32 %0, %1;" : "=r"(v) : "r"(smem_u32(p)));
+  return v;
+}
+
+// Shared-memory accesses through 32-bit shared-window addresses.  Deriving
+// a shared address from a generic pointer costs an S2R SR_CgaCtaId that the
+// compiler re-issues for every predicated access in a loop (measured: ~130
+// cycles per loop iteration in the selector); converting the dynamic smem base
+// once and addressing explicitly keeps every access a plain LDS/STS/ATOMS.
+__device__ __forceinline__ uint32_t lds(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ float ldsf(uint32_t a) { return __uint_as_float(lds(a)); }
+__device__ __forceinline__ uint2 lds2(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint4 lds4(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(a)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void stsf(uint32_t a, float v) { sts(a, __float_as_uint(v)); }
+__device__ __forceinline__ void sts2(uint32_t a, uint32_t x, uint32_t y) {
+  asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(x), "r"(y) : "memory");
+}
+__device__ __forceinline__ void sts4(uint32_t a, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ uint32_t atoms_add(uint32_t a, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void reds_add(uint32_t a, uint32_t v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -155,11 +206,10 @@ __device__ __forceinline__ void gbar_wait(const unsigned* bar, unsigned g) {
 
 // ---------------------------------------------------------------------------
 // Block-wide exclusive scan of one u32 per thread (all kThreads threads).
-// s_warp needs kWarps + 1 words.  Returns the exclusive prefix; *total gets
-// the block sum.  Contains __syncthreads.
+// s_warp: shared address of kWarps scratch words.  Returns the exclusive
+// prefix; *total gets the block sum.  Contains two __syncthreads.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp,
-                                                    uint32_t* total) {
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t s_warp, uint32_t* total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t inc = v;
 #pragma unroll
@@ -167,24 +217,19 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp
     const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
     if (lane >= o) inc += t;
   }
-  if (lane == 31) s_warp[warp] = inc;
+  if (lane == 31) sts(s_warp + 4u * warp, inc);
   __syncthreads();
-  if (warp == 0) {
-    const uint32_t w = lane < kWarps ? s_warp[lane] : 0u;
-    uint32_t wi = w;
+  const uint32_t w = lane < kWarps ? lds(s_warp + 4u * lane) : 0u;
+  uint32_t wi = w;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t t = __shfl_up_sync(0xffffffffu, wi, o);
-      if (lane >= o) wi += t;
-    }
-    if (lane < kWarps) s_warp[lane] = wi - w;
-    if (lane == kWarps - 1) s_warp[kWarps] = wi;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, wi, o);
+    if (lane >= o) wi += t;
   }
-  __syncthreads();
-  const uint32_t res = s_warp[warp] + inc - v;
-  if (total) *total = s_warp[kWarps];
-  __syncthreads();
-  return res;
+  const uint32_t base = __shfl_sync(0xffffffffu, wi - w, warp);
+  if (total) *total = __shfl_sync(0xffffffffu, wi, kWarps - 1);
+  __syncthreads();  // the scratch words may be reused right after
+  return base + inc - v;
 }
 
 // Streaming 16-byte load of weights that are read exactly once per forward

@@ -39,24 +39,22 @@
 
 namespace rsp {
 
-constexpr int M_LAST = 31;  // misc slot: "this CTA reduces its column tile"
-
 // Shared-memory carve-up of the fused kernel (host and device agree).
-// [0, 64K): 15-bit histogram during selection, then the two reduction buffers.
+// Selection region [hist 16K | candidates 4K | keys 4n]; after selection its
+// first 32 KB hold the two reduction buffers (red1 at 0, red2 at 16K).
 struct SmemLayout {
-  uint32_t off_keys, off_coarse, off_cand, off_misc, off_w, off_u, off_a, off_astage, total;
+  uint32_t off_cand, off_keys, off_misc, off_w, off_u, off_a, off_astage, total;
 
   __host__ __device__ static uint32_t up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
 
   __host__ __device__ static SmemLayout make(int n, int cap_w, int cap_u, int cap_a, int a_bytes) {
     SmemLayout L;
-    uint32_t o = 4u * kFineWords;
+    uint32_t o = 4u * kHistBins;
+    L.off_cand = o;
+    o += 4u * kCandWords;
     L.off_keys = o;
     o = up(o + 4u * static_cast<uint32_t>(n), 16);
-    L.off_coarse = o;
-    o += 4u * kCoarseBins;
-    L.off_cand = o;
-    o += 4u * kCandMax;
+    o = o > 32768u ? o : 32768u;
     L.off_misc = o;
     o += 4u * kMiscWords;
     L.off_w = o;
@@ -94,23 +92,19 @@ __device__ __forceinline__ long long gtimer() {
 
 // acc += sum over rows i = first, first+stride, ... < count of coef(i) * row(i)[lane's 16 B].
 // U rows are loaded before any is consumed (U x 512 B in flight per warp).
-template <typename WT, int U, class RowPtr, class Coef, class Load>
+// Out-of-range slots reuse the last valid row with a zero coefficient, so the
+// loads are unconditional (no predicated shared/global accesses in the body).
+template <typename WT, int U, class Row>
 __device__ __forceinline__ void stream_rows(float (&acc)[Vec<WT>::kElems], int first, int count,
-                                            int stride, bool lane_ok, RowPtr row_ptr, Coef coef,
-                                            Load load) {
+                                            int stride, bool lane_ok, Row row) {
   for (int i0 = first; i0 < count; i0 += stride * U) {
     uint4 u[U];
     float c[U];
 #pragma unroll
     for (int q = 0; q < U; ++q) {
       const int i = i0 + q * stride;
-      if (i < count) {
-        c[q] = coef(i);
-        u[q] = lane_ok ? load(row_ptr(i)) : make_uint4(0, 0, 0, 0);
-      } else {
-        c[q] = 0.f;
-        u[q] = make_uint4(0, 0, 0, 0);
-      }
+      row(min(i, count - 1), lane_ok, u[q], c[q]);
+      if (i >= count) c[q] = 0.f;
     }
 #pragma unroll
     for (int q = 0; q < U; ++q) Vec<WT>::fma(acc, u[q], c[q]);
@@ -125,18 +119,19 @@ __global__ void __launch_bounds__(kThreads, 1) fused_forward_kernel(const FusedP
   constexpr int VE = Vec<WT>::kElems;  // elements per 16 B
   constexpr int ES = static_cast<int>(sizeof(WT));
   const SmemLayout L = SmemLayout::make(p.n, p.cap_w, p.cap_u, p.cap_a, p.a_smem_bytes);
+  const uint32_t sb = smem_base_pinned(smem);  // shared-window base: every access below is LDS/STS
   SelSmem ss;
-  ss.fine = reinterpret_cast<uint32_t*>(smem);
-  ss.keys = reinterpret_cast<uint32_t*>(smem + L.off_keys);
-  ss.coarse = reinterpret_cast<uint32_t*>(smem + L.off_coarse);
-  ss.cand = reinterpret_cast<uint32_t*>(smem + L.off_cand);
-  ss.misc = reinterpret_cast<uint32_t*>(smem + L.off_misc);
-  int2* list_w = reinterpret_cast<int2*>(smem + L.off_w);  // {channel j, bits of x_j}
-  int2* list_u = reinterpret_cast<int2*>(smem + L.off_u);
-  float* coef_a = reinterpret_cast<float*>(smem + L.off_a);
-  uint8_t* a_stage = smem + L.off_astage;                  // A_r^T rows of this CTA's tile
-  float* red1 = reinterpret_cast<float*>(smem);            // [G1][r_pad], after selection
-  float* red2 = reinterpret_cast<float*>(smem + 32768);    // [G2][tile cols], after selection
+  ss.hist = sb;
+  ss.cand = sb + L.off_cand;
+  ss.keys = sb + L.off_keys;
+  ss.misc = sb + L.off_misc;
+  const uint32_t list_w = sb + L.off_w;  // int2 {channel j, bits of x_j} per rank
+  const uint32_t list_u = sb + L.off_u;
+  const uint32_t coef_a = sb + L.off_a;  // f32 t_c per rank row
+  const uint32_t a_stage = sb + L.off_astage;
+  uint8_t* a_stage_ptr = smem + L.off_astage;  // cp.async destination
+  const uint32_t red1 = sb;             // [G1][r_pad] f32, after selection
+  const uint32_t red2 = sb + 16384u;    // [G2][tile cols] f32, after selection
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int b = blockIdx.x, NB = gridDim.x;
@@ -189,7 +184,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_forward_kernel(const FusedP
   if (has_lr) {
     for (int f = tid; f < na_s * tw; f += kThreads) {
       const int i = f / tw, v = f - i * tw;
-      cp_async16(a_stage + static_cast<size_t>(f) * 16, a_tile + static_cast<size_t>(alo + i) * rowW + v * 16);
+      cp_async16(a_stage_ptr + static_cast<size_t>(f) * 16, a_tile + static_cast<size_t>(alo + i) * rowW + v * 16);
     }
     cp_async_commit();
     for (int i = na_s + tid; i < na; i += kThreads)
@@ -209,23 +204,18 @@ __global__ void __launch_bounds__(kThreads, 1) fused_forward_kernel(const FusedP
   if (tid == 0) RSP_TRACE(1);
 
   // ---- 1. exact selection (redundant per CTA: x is at most a few tens of KB) ----
-  sel_load(p.x, p.x_bf16 != 0, p.n, ss);
+  __syncthreads();  // histogram zeroed (prologue) before the load adds to it
+  sel_load(p.x, p.x_bf16 != 0, p.n, ss, !p.dense);
   if (tid == 0) RSP_TRACE(2);
   SelResult sr{0u, static_cast<uint32_t>(p.n)};
-  if (!p.dense) {
-    sel_hist(p.n, ss);
-    sr = sel_resolve(p.n, p.k, p.x_bf16 != 0, ss);
-  }
+  if (!p.dense) sr = sel_resolve(p.n, p.k, p.x_bf16 != 0, ss);
   if (tid == 0) RSP_TRACE(3);
   // ---- 2. this CTA's row lists: rank ranges of S and of S^c ----
-  sel_emit(p.n, sr, ss, [&](int j, uint32_t bits, bool in, uint32_t rank) {
-    if (in) {
-      if (rank >= static_cast<uint32_t>(wlo) && rank < static_cast<uint32_t>(whi))
-        list_w[rank - wlo] = make_int2(j, static_cast<int>(bits));
-    } else if (rank >= static_cast<uint32_t>(ulo) && rank < static_cast<uint32_t>(uhi)) {
-      list_u[rank - ulo] = make_int2(j, static_cast<int>(bits));
-    }
-  });
+  sel_count(p.n, sr, ss);
+  sel_range_emit(p.n, sr, ss, true, static_cast<uint32_t>(wlo), static_cast<uint32_t>(whi),
+                 [&](int j, uint32_t bits, uint32_t i) { sts2(list_w + 8u * i, static_cast<uint32_t>(j), bits); });
+  sel_range_emit(p.n, sr, ss, false, static_cast<uint32_t>(ulo), static_cast<uint32_t>(uhi),
+                 [&](int j, uint32_t bits, uint32_t i) { sts2(list_u + 8u * i, static_cast<uint32_t>(j), bits); });
   __syncthreads();
   if (tid == 0) RSP_TRACE(4);
 
@@ -238,19 +228,21 @@ __global__ void __launch_bounds__(kThreads, 1) fused_forward_kernel(const FusedP
 #pragma unroll
     for (int e = 0; e < VE; ++e) acc[e] = 0.f;
     const uint8_t* base = Bt + v * 16;
-    stream_rows<WT, U>(
-        acc, g1, n1, G1, ok, [&](int i) { return base + static_cast<size_t>(list_u[i].x) * rowB; },
-        [&](int i) { return __int_as_float(list_u[i].y); }, [](const void* q) { return ldg_stream(q); });
+    stream_rows<WT, U>(acc, g1, n1, G1, ok, [&](int i, bool lok, uint4& u, float& c) {
+      const uint2 e = lds2(list_u + 8u * i);
+      c = __uint_as_float(e.y);
+      u = lok ? ldg_stream(base + static_cast<size_t>(e.x) * rowB) : make_uint4(0, 0, 0, 0);
+    });
     if (tid == 0) RSP_TRACE(5);
     if (ok) {
 #pragma unroll
-      for (int e = 0; e < VE; ++e) red1[g1 * p.r_pad + v * VE + e] = acc[e];
+      for (int e = 0; e < VE; ++e) stsf(red1 + 4u * (g1 * p.r_pad + v * VE + e), acc[e]);
     }
     named_bar_sync(1, W1 * 32);
     // partial t of this CTA: column b of t_part[r_pad][nb_pad]
     for (int c = tid; c < p.r_pad; c += W1 * 32) {
       float sum = 0.f;
-      for (int g = 0; g < G1; ++g) sum += red1[g * p.r_pad + c];
+      for (int g = 0; g < G1; ++g) sum += ldsf(red1 + 4u * (g * p.r_pad + c));
       p.t_part[static_cast<size_t>(c) * p.nb_pad + b] = sum;
     }
     __threadfence();
@@ -287,7 +279,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_forward_kernel(const FusedP
         v8 += __shfl_xor_sync(0xffffffffu, v8, 2);
         v8 += __shfl_xor_sync(0xffffffffu, v8, 1);
         const int c = c0 + rr * ng8;
-        if (l8 == 0 && c < ahi) coef_a[c - alo] = v8;
+        if (l8 == 0 && c < ahi) stsf(coef_a + 4u * (c - alo), v8);
       }
     }
     if (tid == 0) RSP_TRACE(8);
@@ -306,9 +298,11 @@ __global__ void __launch_bounds__(kThreads, 1) fused_forward_kernel(const FusedP
   for (int e = 0; e < VE; ++e) acc[e] = 0.f;
   const uint8_t* wbase = Wt + static_cast<size_t>(col0) * ES + v * 16;
   if (g2 < G2)
-    stream_rows<WT, U>(
-        acc, g2, nw, G2, ok, [&](int i) { return wbase + static_cast<size_t>(list_w[i].x) * rowW; },
-        [&](int i) { return __int_as_float(list_w[i].y); }, [](const void* q) { return ldg_stream(q); });
+    stream_rows<WT, U>(acc, g2, nw, G2, ok, [&](int i, bool lok, uint4& u, float& c) {
+      const uint2 e = lds2(list_w + 8u * i);
+      c = __uint_as_float(e.y);
+      u = lok ? ldg_stream(wbase + static_cast<size_t>(e.x) * rowW) : make_uint4(0, 0, 0, 0);
+    });
   if (wt == 0) RSP_TRACE(9);
   if (has_lr) {
     cp_async_wait_all();
@@ -316,14 +310,14 @@ __global__ void __launch_bounds__(kThreads, 1) fused_forward_kernel(const FusedP
     if (g2 < G2) {
       if (ok) {
         for (int i = g2; i < na_s; i += G2)
-          Vec<WT>::fma(acc, *reinterpret_cast<const uint4*>(a_stage + (static_cast<size_t>(i) * tw + v) * 16),
-                       coef_a[i]);
+          Vec<WT>::fma(acc, lds4(a_stage + (static_cast<uint32_t>(i) * tw + v) * 16u), ldsf(coef_a + 4u * i));
       }
       const uint8_t* abase = a_tile + v * 16;
       const int first = na_s + ((g2 - na_s % G2) % G2 + G2) % G2;  // keep row i on group i % G2
-      stream_rows<WT, U>(
-          acc, first, na, G2, ok, [&](int i) { return abase + static_cast<size_t>(alo + i) * rowW; },
-          [&](int i) { return coef_a[i]; }, [](const void* q) { return ldg_l2(q); });
+      stream_rows<WT, U>(acc, first, na, G2, ok, [&](int i, bool lok, uint4& u, float& c) {
+        c = ldsf(coef_a + 4u * i);
+        u = lok ? ldg_l2(abase + static_cast<size_t>(alo + i) * rowW) : make_uint4(0, 0, 0, 0);
+      });
     }
   }
   if (wt == 0) RSP_TRACE(10);
@@ -331,12 +325,12 @@ __global__ void __launch_bounds__(kThreads, 1) fused_forward_kernel(const FusedP
   // ---- split-K: group reduction in smem, then y ----
   if (ok) {
 #pragma unroll
-    for (int e = 0; e < VE; ++e) red2[g2 * tcw + v * VE + e] = acc[e];
+    for (int e = 0; e < VE; ++e) stsf(red2 + 4u * (g2 * tcw + v * VE + e), acc[e]);
   }
   named_bar_sync(2, nwt);
   for (int c = wt; c < tcw; c += nwt) {
     float sum = 0.f;
-    for (int g = 0; g < G2; ++g) sum += red2[g * tcw + c];
+    for (int g = 0; g < G2; ++g) sum += ldsf(red2 + 4u * (g * tcw + c));
     const int col = col0 + c;
     if (p.k_splits == 1) {
       if (col < p.m) p.y[col] = sum;
@@ -351,9 +345,9 @@ __global__ void __launch_bounds__(kThreads, 1) fused_forward_kernel(const FusedP
     __threadfence();
     named_bar_sync(2, nwt);
     unsigned* ticket = p.bars + 2 + ct;
-    if (wt == 0) ss.misc[M_LAST] = atom_add_acq_rel_gpu(ticket, 1u) == static_cast<unsigned>(p.k_splits - 1);
+    if (wt == 0) ss.set_m(M_LAST, atom_add_acq_rel_gpu(ticket, 1u) == static_cast<unsigned>(p.k_splits - 1));
     named_bar_sync(2, nwt);
-    if (ss.misc[M_LAST]) {
+    if (ss.m(M_LAST)) {
       // Last CTA of this column tile: fixed-order sum of the k_splits partials.
       for (int c = wt; c < tcw; c += nwt) {
         const int col = col0 + c;
@@ -421,28 +415,29 @@ __global__ void __launch_bounds__(kThreads, 1)
     select_kernel(const void* x, int x_bf16, int n, int k, int32_t* kept, int32_t* rest,
                   float* sparse_x) {
   extern __shared__ __align__(16) uint8_t smem_sel[];
+  const uint32_t sb = smem_base_pinned(smem_sel);
   SelSmem ss;
-  ss.fine = reinterpret_cast<uint32_t*>(smem_sel);
-  ss.coarse = ss.fine + kFineWords;
-  ss.cand = ss.coarse + kCoarseBins;
-  ss.misc = ss.cand + kCandMax;
-  ss.keys = ss.misc + kMiscWords;
+  ss.hist = sb;
+  ss.cand = sb + 4u * kHistBins;
+  ss.misc = ss.cand + 4u * kCandWords;
+  ss.keys = ss.misc + 4u * kMiscWords;
   sel_clear(ss);
-  sel_load(x, x_bf16 != 0, n, ss);
-  sel_hist(n, ss);
+  __syncthreads();
+  sel_load(x, x_bf16 != 0, n, ss, true);
   const SelResult sr = sel_resolve(n, k, x_bf16 != 0, ss);
-  sel_emit(n, sr, ss, [&](int j, uint32_t bits, bool in, uint32_t rank) {
-    if (in) {
-      if (kept) kept[rank] = j;
-    } else if (rest) {
-      rest[rank] = j;
-    }
-    if (sparse_x) sparse_x[j] = in ? __uint_as_float(bits) : 0.f;
+  sel_count(n, sr, ss);
+  sel_range_emit(n, sr, ss, true, 0u, static_cast<uint32_t>(k), [&](int j, uint32_t bits, uint32_t i) {
+    if (kept) kept[i] = j;
+    if (sparse_x) sparse_x[j] = __uint_as_float(bits);
+  });
+  sel_range_emit(n, sr, ss, false, 0u, static_cast<uint32_t>(n - k), [&](int j, uint32_t, uint32_t i) {
+    if (rest) rest[i] = j;
+    if (sparse_x) sparse_x[j] = 0.f;
   });
 }
 
 size_t select_smem_bytes(int n) {
-  return 4u * (kFineWords + kCoarseBins + kCandMax + kMiscWords) + 4u * static_cast<size_t>(n);
+  return 4u * (kHistBins + kCandWords + kMiscWords) + 4u * static_cast<size_t>(n);
 }
 
 cudaError_t launch_select(const void* x, bool x_bf16, int n, int k, int32_t* kept, int32_t* rest,

@@ -11,54 +11,61 @@
 // are widened exactly (bits << 16).  NaN keys order above +inf (the
 // reference's std::sort on NaN is undefined).
 //
-// The result is (T, need):  j in S  <=>  key_j > T  or  (key_j == T and
-// tie_rank(j) < need), tie_rank(j) = #{i < j : key_i == T}.
+// The result is (T, need): T is the exact k-th largest key and
+//   j in S  <=>  key_j > T  or  (key_j == T and tie_rank(j) < need),
+// tie_rank(j) = #{i < j : key_i == T}  (lower index wins the tie).
 //
-// Algorithm (one pass over x, no per-pass syncs beyond four):
-//   1. load x -> keys in shared memory; shared atomics build a 15-bit
-//      histogram of key>>16 (32768 u16 bins packed in 16384 words); the 8-bit
-//      coarse histogram of key>>23 is summed from it;
-//   2. a 256-entry block scan on the coarse histogram finds the coarse bin
-//      holding the k-th largest key; one warp scans that bin's 128 fine bins;
-//   3. for bf16 inputs the fine bin IS the key: done.  For fp32 inputs the
-//      (usually few) candidates inside the fine bin are ranked by value
-//      directly (<= 256), else resolved by two 8-bit radix passes;
-//   4. emit: two ballot passes in index order give every element its rank
-//      in S or S^c (the tie cut falls out of the tie ballots).
+// Algorithm (per-phase cycle costs are measured by tools/select_probe.cu):
+//   1. load x -> keys in shared memory, one shared atomic per element into a
+//      12-bit histogram of key >> 19 (exponent + 4 mantissa bits, 16 KB);
+//   2. a block scan (8 bins per thread, descending) finds the boundary bin
+//      holding the k-th largest key;
+//   3. the boundary bin's elements (typically 1-3% of n) are gathered; radix
+//      descent over their remaining 19 bits (8/8/3-bit digits, histograms of
+//      the candidate list only, one-warp scans) yields the exact T.  More than
+//      kCandCap candidates (heavy ties) descend over all keys instead;
+//   4. count: ballots give every chunk of 32 indices its (greater, tie) counts;
+//      one block scan turns them into per-chunk S offsets (tie cut included);
+//   5. emit: a CTA re-visits only the chunks overlapping the rank ranges it
+//      owns (binary search on the monotone offsets) and ranks those elements
+//      with ballot/popc arithmetic.
+// All shared memory is addressed through 32-bit shared-window addresses
+// (rsp_device.cuh: lds/sts/atoms_add).
 #pragma once
 
 #include <stdint.h>
 
 #include "rsp_device.cuh"
 
+#ifndef RSP_SEL_DEBUG
+#define RSP_SEL_DEBUG(level, prefix, need, cnt, extra)
+#endif
+
 namespace rsp {
 
-constexpr int kFineWords = 16384;  // 32768 15-bit bins as packed u16 pairs
-constexpr int kCoarseBins = 256;   // key >> 23
-constexpr int kCandMax = 256;
-constexpr int kMiscWords = 64;
+constexpr int kHistBins = 4096;  // key >> 19
+constexpr int kCandCap = 1024;
+constexpr int kCandWords = kCandCap + 64;  // also holds the per-chunk prefix (n/32 + 1 <= 1025)
+constexpr int kMiscWords = 96;
 
-// misc[] slots
+// misc[] word slots
 enum : int {
-  M_SCAN = 0,       // [0, 17): block-scan scratch
-  M_CB = 20,        // coarse bin
-  M_NEED1 = 21,
-  M_FB = 22,        // fine bin
-  M_NEED2 = 23,
-  M_CNTFB = 24,
-  M_T = 25,
-  M_NEED = 26,
-  M_CC = 27,        // candidate counter
-  M_BIN = 28, M_ABOVE = 29, M_CNT = 30,
-  M_WARP = 32,      // [32, 64): per-warp (gt, tie) counts for emit
+  M_SCAN = 0,  // [0, 16): block-scan scratch
+  M_BIN = 20, M_ABOVE = 21, M_CNT = 22,
+  M_CC = 25,    // candidate counter
+  M_LAST = 31,  // fused kernel: "this CTA combines its column tile"
+  M_WARP = 32,  // [32, 64): per-warp (strictly-greater, tie) counts for emit
 };
 
+// Shared-window byte addresses of the selector's arrays.
 struct SelSmem {
-  uint32_t* keys;    // [n] raw fp32 bit patterns of x
-  uint32_t* fine;    // [kFineWords]
-  uint32_t* coarse;  // [kCoarseBins]
-  uint32_t* cand;    // [kCandMax]
-  uint32_t* misc;    // [kMiscWords]
+  uint32_t keys;  // [n] u32: raw fp32 bit patterns of x
+  uint32_t hist;  // [kHistBins] u32
+  uint32_t cand;  // [kCandWords] u32: candidate keys, then per-chunk prefix
+  uint32_t misc;  // [kMiscWords] u32
+  __device__ __forceinline__ uint32_t key(int j) const { return lds(keys + 4u * j); }
+  __device__ __forceinline__ uint32_t m(int slot) const { return lds(misc + 4u * slot); }
+  __device__ __forceinline__ void set_m(int slot, uint32_t v) const { sts(misc + 4u * slot, v); }
 };
 
 struct SelResult {
@@ -74,209 +81,304 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return m;
 }
 
-// Zero the fine histogram (independent of x: may run before griddepcontrol.wait).
+
+// Zero the histogram (independent of x: may run before griddepcontrol.wait).
+// Callers __syncthreads before sel_load.
 __device__ __forceinline__ void sel_clear(const SelSmem& s) {
-  uint4* f = reinterpret_cast<uint4*>(s.fine);
-  for (int i = threadIdx.x; i < kFineWords / 4; i += kThreads) f[i] = make_uint4(0, 0, 0, 0);
-  if (threadIdx.x == 0) s.misc[M_CC] = 0u;
+  for (int i = threadIdx.x; i < kHistBins / 4; i += kThreads) sts4(s.hist + 16u * i, make_uint4(0, 0, 0, 0));
+  if (threadIdx.x == 0) s.set_m(M_CC, 0u);
 }
 
-// x (fp32 or bf16, any alignment) -> keys[] as fp32 bit patterns.  Vector
-// loads when 16-byte aligned.  Ends with __syncthreads.
+__device__ __forceinline__ void hist_add(const SelSmem& s, uint32_t bits) {
+  reds_add(s.hist + 4u * (abs_key(bits) >> 19), 1u);
+}
+
+// x (fp32 or bf16, any alignment) -> keys[] as fp32 bit patterns, and the
+// 12-bit histogram (needs sel_clear + barrier first; skipped when `hist` is
+// false).  All of a thread's 16-byte loads are issued before any is consumed
+// (one memory round trip for n <= 16384 bf16 / 8192 fp32).  Ends with
+// __syncthreads.
 __device__ __forceinline__ void sel_load(const void* __restrict__ x, bool x_bf16, int n,
-                                         const SelSmem& s) {
+                                         const SelSmem& s, bool hist) {
   const uintptr_t a = reinterpret_cast<uintptr_t>(x);
-  if (x_bf16) {
-    const uint16_t* xb = static_cast<const uint16_t*>(x);
-    if ((a & 15u) == 0 && (n & 7) == 0) {
-      const uint4* xv = reinterpret_cast<const uint4*>(x);
-      for (int i = threadIdx.x; i < n / 8; i += kThreads) {
-        const uint4 u = __ldg(xv + i);
-        uint4* d = reinterpret_cast<uint4*>(s.keys + 8 * i);
-        d[0] = make_uint4(u.x << 16, u.x & 0xffff0000u, u.y << 16, u.y & 0xffff0000u);
-        d[1] = make_uint4(u.z << 16, u.z & 0xffff0000u, u.w << 16, u.w & 0xffff0000u);
-      }
-    } else {
-      for (int j = threadIdx.x; j < n; j += kThreads) s.keys[j] = static_cast<uint32_t>(xb[j]) << 16;
-    }
-  } else {
-    const uint32_t* xf = static_cast<const uint32_t*>(x);
-    if ((a & 15u) == 0 && (n & 3) == 0) {
-      const uint4* xv = reinterpret_cast<const uint4*>(x);
-      uint4* d = reinterpret_cast<uint4*>(s.keys);
-      for (int i = threadIdx.x; i < n / 4; i += kThreads) d[i] = __ldg(xv + i);
-    } else {
-      for (int j = threadIdx.x; j < n; j += kThreads) s.keys[j] = __ldg(xf + j);
-    }
-  }
-  __syncthreads();
-}
-
-// 15-bit histogram of key >> 16 (packed u16 shared atomics), then the 8-bit
-// coarse histogram key >> 23 as sums of 128 fine bins.  Ends with __syncthreads.
-__device__ __forceinline__ void sel_hist(int n, const SelSmem& s) {
-  for (int j = threadIdx.x; j < n; j += kThreads) {
-    const uint32_t fb = abs_key(s.keys[j]) >> 16;
-    atomicAdd(&s.fine[fb >> 1], 1u << ((fb & 1u) * 16u));
-  }
-  __syncthreads();
-  // Two threads per coarse bin, 32 words each, bank-rotated reads.
-  const int cbin = threadIdx.x >> 1, half = threadIdx.x & 1;
-  const uint32_t* w = s.fine + cbin * 64 + half * 32;
-  uint32_t sum = 0;
-#pragma unroll 8
-  for (int i = 0; i < 32; ++i) {
-    const uint32_t v = w[(i + cbin) & 31];
-    sum += (v & 0xffffu) + (v >> 16);
-  }
-  sum += __shfl_xor_sync(0xffffffffu, sum, 1);
-  if (half == 0) s.coarse[cbin] = sum;
-  __syncthreads();
-}
-
-// Descending-bin block search over a 256-bin histogram: returns (bin, count
-// above it, its count) for the need-th largest.  All threads participate.
-__device__ __forceinline__ void scan256_desc(const uint32_t* hist, uint32_t need, uint32_t* misc) {
-  const int tid = threadIdx.x;
-  const uint32_t c = tid < 256 ? hist[255 - tid] : 0u;
-  const uint32_t above = block_excl_scan(c, misc + M_SCAN, nullptr);
-  if (tid < 256 && above < need && need <= above + c) {
-    misc[M_BIN] = 255u - tid;
-    misc[M_ABOVE] = above;
-    misc[M_CNT] = c;
-  }
-  __syncthreads();
-}
-
-__device__ SelResult sel_resolve(int n, int k, bool bf16_keys, const SelSmem& s) {
-  if (k <= 0) return SelResult{0xffffffffu, 0u};
-  if (k >= n) return SelResult{0u, static_cast<uint32_t>(n)};
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  uint32_t* misc = s.misc;
-  // coarse bin
-  scan256_desc(s.coarse, static_cast<uint32_t>(k), misc);
-  const uint32_t cb = misc[M_BIN];
-  const uint32_t need1 = static_cast<uint32_t>(k) - misc[M_ABOVE];
-  // fine bin inside cb: bins [cb*128, cb*128+128) = words [cb*64, cb*64+64)
-  if (warp == 0) {
-    const uint32_t wa = s.fine[cb * 64 + 63 - 2 * lane];  // bins top-4l (hi half), top-4l-1
-    const uint32_t wb = s.fine[cb * 64 + 62 - 2 * lane];  // bins top-4l-2, top-4l-3
-    const uint32_t c0 = wa >> 16, c1 = wa & 0xffffu, c2 = wb >> 16, c3 = wb & 0xffffu;
-    const uint32_t sum = c0 + c1 + c2 + c3;
-    uint32_t inc = sum;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += t;
-    }
-    const uint32_t ex = inc - sum;
-    if (ex < need1 && need1 <= inc) {
-      const uint32_t top = cb * 128 + 127 - 4 * lane;
-      const uint32_t cs[4] = {c0, c1, c2, c3};
-      uint32_t acc = ex;
+  const int per16 = x_bf16 ? 8 : 4;  // elements per 16 B
+  if ((a & 15u) == 0 && (n % per16) == 0) {
+    const uint4* xv = reinterpret_cast<const uint4*>(x);
+    const int nv = n / per16;
+    for (int base = 0; base < nv; base += 4 * kThreads) {
+      uint4 u[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        if (acc + cs[q] >= need1) {
-          misc[M_FB] = top - q;
-          misc[M_NEED2] = need1 - acc;
-          misc[M_CNTFB] = cs[q];
-          break;
-        }
-        acc += cs[q];
+        const int i = base + q * kThreads + threadIdx.x;
+        u[q] = i < nv ? __ldg(xv + i) : make_uint4(0, 0, 0, 0);
       }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int i = base + q * kThreads + threadIdx.x;
+        if (i >= nv) continue;
+        if (x_bf16) {
+          const uint4 d0 = make_uint4(u[q].x << 16, u[q].x & 0xffff0000u, u[q].y << 16, u[q].y & 0xffff0000u);
+          const uint4 d1 = make_uint4(u[q].z << 16, u[q].z & 0xffff0000u, u[q].w << 16, u[q].w & 0xffff0000u);
+          sts4(s.keys + 32u * i, d0);
+          sts4(s.keys + 32u * i + 16u, d1);
+          if (hist) {
+            hist_add(s, d0.x); hist_add(s, d0.y); hist_add(s, d0.z); hist_add(s, d0.w);
+            hist_add(s, d1.x); hist_add(s, d1.y); hist_add(s, d1.z); hist_add(s, d1.w);
+          }
+        } else {
+          sts4(s.keys + 16u * i, u[q]);
+          if (hist) {
+            hist_add(s, u[q].x); hist_add(s, u[q].y); hist_add(s, u[q].z); hist_add(s, u[q].w);
+          }
+        }
+      }
+    }
+  } else {
+    for (int j = threadIdx.x; j < n; j += kThreads) {
+      const uint32_t b = x_bf16 ? static_cast<uint32_t>(static_cast<const uint16_t*>(x)[j]) << 16
+                                : __ldg(static_cast<const uint32_t*>(x) + j);
+      sts(s.keys + 4u * j, b);
+      if (hist) hist_add(s, b);
     }
   }
   __syncthreads();
-  const uint32_t fb = misc[M_FB], need2 = misc[M_NEED2], cntfb = misc[M_CNTFB];
-  if (cntfb == need2) return SelResult{(fb << 16) - 1u, 0u};  // whole bin taken (fb > 0 since k < n)
-  if (bf16_keys) return SelResult{fb << 16, need2};
-  // fp32: rank the candidates (key >> 16 == fb) by their low 16 bits.
-  if (cntfb <= static_cast<uint32_t>(kCandMax)) {
-    for (int j = tid; j < n; j += kThreads) {
-      const uint32_t key = abs_key(s.keys[j]);
-      if ((key >> 16) == fb) s.cand[atomicAdd(&misc[M_CC], 1u)] = key & 0xffffu;
-    }
-    __syncthreads();
-    const int c = static_cast<int>(cntfb);
-    for (int i = tid; i < c; i += kThreads) {
-      const uint32_t v = s.cand[i];
-      uint32_t gt = 0, ge = 0;
-      for (int q = 0; q < c; ++q) {
-        const uint32_t u = s.cand[q];
-        gt += u > v;
-        ge += u >= v;
-      }
-      if (gt < need2 && need2 <= ge) {  // every candidate with this value agrees
-        misc[M_T] = (fb << 16) | v;
-        misc[M_NEED] = need2 - gt;
-      }
-    }
-    __syncthreads();
-    return SelResult{misc[M_T], misc[M_NEED]};
-  }
-  // Many candidates: two 8-bit radix passes over the low 16 bits.
-  uint32_t prefix = fb << 16, pmask = 0xffff0000u, need = need2;
-  for (int shift = 8; shift >= 0; shift -= 8) {
-    for (int i = tid; i < kCoarseBins; i += kThreads) s.coarse[i] = 0u;
-    __syncthreads();
-    for (int j = tid; j < n; j += kThreads) {
-      const uint32_t key = abs_key(s.keys[j]);
-      if ((key & pmask) == prefix) atomicAdd(&s.coarse[(key >> shift) & 255u], 1u);
-    }
-    __syncthreads();
-    scan256_desc(s.coarse, need, misc);
-    need -= misc[M_ABOVE];
-    prefix |= misc[M_BIN] << shift;
-    pmask |= 255u << shift;
-    if (misc[M_CNT] == need) return SelResult{prefix - 1u, 0u};
-  }
-  return SelResult{prefix, need};
 }
 
-// Emit every index with its membership and rank: f(j, bits, in_S, rank),
-// rank = position in S (ascending) when in_S, else position in S^c.
-// Warp w owns a contiguous range of indices; two ballot passes.  Contains
-// one __syncthreads; callers must sync before reading what f wrote.
-template <class F>
-__device__ __forceinline__ void sel_emit(int n, SelResult r, const SelSmem& s, F&& f) {
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int chunks = (n + 31) / 32;
-  const int per = (chunks + kWarps - 1) / kWarps;
-  const int j_lo = min(n, warp * per * 32), j_hi = min(n, (warp + 1) * per * 32);
-  uint32_t cgt = 0, ctie = 0;
-  for (int base = j_lo; base < j_hi; base += 32) {
-    const int j = base + lane;
-    const uint32_t key = j < j_hi ? abs_key(s.keys[j]) : 0u;
-    cgt += __popc(__ballot_sync(0xffffffffu, j < j_hi && key > r.T));
-    ctie += __popc(__ballot_sync(0xffffffffu, j < j_hi && key == r.T));
+// One warp: descending search of a histogram of nb <= 256 bins for the
+// need-th largest -> misc[M_BIN/M_ABOVE/M_CNT].  Caller syncs afterwards.
+__device__ __forceinline__ void warp_scan_desc(const SelSmem& s, int nb, uint32_t need) {
+  const int lane = threadIdx.x & 31;
+  const int per = (nb + 31) / 32;  // bins per lane (<= 8)
+  uint32_t c[8];
+  uint32_t local = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int bin = nb - 1 - (lane * per + q);
+    c[q] = (q < per && bin >= 0) ? lds(s.hist + 4u * max(bin, 0)) : 0u;
+    local += c[q];
   }
-  if (lane == 0) {
-    s.misc[M_WARP + 2 * warp] = cgt;
-    s.misc[M_WARP + 2 * warp + 1] = ctie;
+  uint32_t inc = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  uint32_t acc = inc - local;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    if (acc < need && need <= acc + c[q]) {
+      s.set_m(M_BIN, static_cast<uint32_t>(nb - 1 - (lane * per + q)));
+      s.set_m(M_ABOVE, acc);
+      s.set_m(M_CNT, c[q]);
+    }
+    acc += c[q];
+  }
+}
+
+__device__ __forceinline__ SelResult sel_resolve(int n, int k, bool bf16_keys, const SelSmem& s) {
+  if (k <= 0) return SelResult{0xffffffffu, 0u};
+  if (k >= n) return SelResult{0u, static_cast<uint32_t>(n)};
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const uint32_t kk = static_cast<uint32_t>(k);
+  // ---- boundary 12-bit bin: thread t owns bins [4088-8t, 4095-8t], descending
+  {
+    const uint32_t h = s.hist + 4u * ((kHistBins - 8) - 8 * tid);
+    const uint4 lo = lds4(h), hi = lds4(h + 16u);
+    const uint32_t c[8] = {hi.w, hi.z, hi.y, hi.x, lo.w, lo.z, lo.y, lo.x};
+    uint32_t local = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) local += c[q];
+    const uint32_t above = block_excl_scan(local, s.misc + 4u * M_SCAN, nullptr);
+    if (above < kk && kk <= above + local) {
+      uint32_t acc = above;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (acc < kk && kk <= acc + c[q]) {
+          s.set_m(M_BIN, static_cast<uint32_t>(kHistBins - 1 - 8 * tid - q));
+          s.set_m(M_ABOVE, acc);
+          s.set_m(M_CNT, c[q]);
+        }
+        acc += c[q];
+      }
+    }
+    __syncthreads();
+  }
+  uint32_t prefix = s.m(M_BIN) << 19, pmask = 0xfff80000u;
+  uint32_t need = kk - s.m(M_ABOVE);
+  uint32_t cnt = s.m(M_CNT);
+  RSP_SEL_DEBUG(0, prefix, need, cnt, 0u);
+  if (cnt == need) return SelResult{prefix - 1u, 0u};  // whole bin taken (prefix > 0 since k < n)
+  // ---- gather the boundary bin's keys (when they fit)
+  const int ncand = static_cast<int>(cnt);
+  const bool gathered = cnt <= static_cast<uint32_t>(kCandCap);
+  if (gathered) {
+    for (int j = tid; j < n; j += kThreads) {
+      const uint32_t key = abs_key(s.key(j));
+      if ((key & pmask) == prefix) sts(s.cand + 4u * atoms_add(s.misc + 4u * M_CC, 1u), key);
+    }
+  }
+  __syncthreads();  // candidates complete before anyone reads them
+  // ---- radix descent over the remaining 19 bits (digits 18..11, 10..3, 2..0);
+  // as soon as the surviving candidates fit in one warp they are ranked
+  // directly by value (gathered case only).
+#pragma unroll 1
+  for (int p = 0; p < 4; ++p) {
+    if (gathered && cnt <= 32u) {
+      if (warp == 0) {
+        // compact the survivors into lanes, then count greater / equal values
+        const int lane = tid & 31;
+        uint32_t mine = 0u, have = 0u;
+        for (int i0 = 0; i0 < ncand; i0 += 32) {
+          const int i = i0 + lane;
+          const uint32_t key = i < ncand ? lds(s.cand + 4u * i) : 0u;
+          const bool match = i < ncand && (key & pmask) == prefix;
+          const uint32_t bal = __ballot_sync(0xffffffffu, match);
+          const uint32_t pos = have + __popc(bal & lanemask_lt());
+          // lane `pos` receives this key
+#pragma unroll 1
+          for (uint32_t bb = bal; bb; bb &= bb - 1) {
+            const int src = __ffs(bb) - 1;
+            const uint32_t v = __shfl_sync(0xffffffffu, key, src);
+            const uint32_t dst = have + __popc(bal & ((1u << src) - 1u));
+            if (lane == static_cast<int>(dst)) mine = v;
+          }
+          (void)pos;
+          have += __popc(bal);
+        }
+        uint32_t gt = 0, ge = 0;
+#pragma unroll 1
+        for (int q = 0; q < static_cast<int>(have); ++q) {
+          const uint32_t o = __shfl_sync(0xffffffffu, mine, q);
+          gt += o > mine;
+          ge += o >= mine;
+        }
+        if (lane < static_cast<int>(have) && gt < need && need <= ge) {
+          s.set_m(M_BIN, mine);
+          s.set_m(M_ABOVE, need - gt);
+        }
+      }
+      __syncthreads();
+      return SelResult{s.m(M_BIN), s.m(M_ABOVE)};
+    }
+    if (p == 3) break;
+    const int shift = p == 0 ? 11 : (p == 1 ? 3 : 0), nb = p < 2 ? 256 : 8;
+    const uint32_t dmask = static_cast<uint32_t>(nb - 1);
+    if (tid < 256) sts(s.hist + 4u * tid, 0u);
+    __syncthreads();
+    if (gathered) {
+      for (int i = tid; i < ncand; i += kThreads) {
+        const uint32_t key = lds(s.cand + 4u * i);
+        if ((key & pmask) == prefix) reds_add(s.hist + 4u * ((key >> shift) & dmask), 1u);
+      }
+    } else {
+      for (int j = tid; j < n; j += kThreads) {
+        const uint32_t key = abs_key(s.key(j));
+        if ((key & pmask) == prefix) reds_add(s.hist + 4u * ((key >> shift) & dmask), 1u);
+      }
+    }
+    __syncthreads();
+    if (warp == 0) warp_scan_desc(s, nb, need);
+    __syncthreads();
+    need -= s.m(M_ABOVE);
+    prefix |= s.m(M_BIN) << shift;
+    pmask |= dmask << shift;
+    cnt = s.m(M_CNT);
+    RSP_SEL_DEBUG(p + 1, prefix, need, cnt, s.m(M_CC));
+    if (cnt == need) return SelResult{prefix - 1u, 0u};  // whole sub-bin taken
+    if (bf16_keys && p == 0) return SelResult{prefix, need};  // bits 15..0 are zero: exact
+  }
+  return SelResult{prefix, need};  // exact key T; `need` of its ties (lowest indices) are in S
+}
+
+// Lowest `k` set bits of m.
+__device__ __forceinline__ uint32_t lowest_bits(uint32_t m, uint32_t k) {
+  if (k >= static_cast<uint32_t>(__popc(m))) return m;
+  uint32_t r = 0;
+  for (uint32_t i = 0; i < k; ++i) {
+    const uint32_t b = m & (0u - m);
+    r |= b;
+    m ^= b;
+  }
+  return r;
+}
+
+// Per-chunk counts and their exclusive prefix (one block scan).  Chunk c =
+// indices [32c, 32c+32).  pk[c] (shared u32 array at s.cand, chunks+1 words)
+// = (#keys > T before chunk c) | (#keys == T before chunk c) << 16, so the
+// number of S elements before chunk c is lo16 + min(need, hi16).  Counts fit
+// 16 bits because n <= 32768.  Contains __syncthreads.
+__device__ __forceinline__ void sel_count(int n, SelResult r, const SelSmem& s) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int chunks = (n + 31) / 32;
+  // pass A: per-chunk packed counts (warp w walks chunks w, w+16, ...)
+#pragma unroll 4
+  for (int c = warp; c < chunks; c += kWarps) {
+    const int j = c * 32 + lane;
+    const uint32_t key = abs_key(lds(s.keys + 4u * min(j, n - 1)));
+    const uint32_t gm = __ballot_sync(0xffffffffu, j < n && key > r.T);
+    const uint32_t tm = __ballot_sync(0xffffffffu, j < n && key == r.T);
+    if (lane == 0) sts(s.cand + 4u * c, __popc(gm) | (static_cast<uint32_t>(__popc(tm)) << 16));
   }
   __syncthreads();
-  uint32_t tie_before = 0, sel_before = 0;
-  for (int w = 0; w < warp; ++w) {
-    const uint32_t g = s.misc[M_WARP + 2 * w], t = s.misc[M_WARP + 2 * w + 1];
-    const uint32_t take = r.need > tie_before ? min(r.need - tie_before, t) : 0u;
-    sel_before += g + take;
-    tie_before += t;
+  // exclusive prefix over chunks: thread t owns chunks 2t, 2t+1
+  const int c0 = 2 * threadIdx.x;
+  const uint32_t a0 = c0 < chunks ? lds(s.cand + 4u * c0) : 0u;
+  const uint32_t a1 = c0 + 1 < chunks ? lds(s.cand + 4u * (c0 + 1)) : 0u;
+  uint32_t total;
+  const uint32_t ex = block_excl_scan(a0 + a1, s.misc + 4u * M_SCAN, &total);
+  if (c0 < chunks) sts(s.cand + 4u * c0, ex);
+  if (c0 + 1 < chunks) sts(s.cand + 4u * (c0 + 1), ex + a0);
+  if (threadIdx.x == 0) sts(s.cand + 4u * chunks, total);
+  __syncthreads();
+}
+
+__device__ __forceinline__ uint32_t sel_before(uint32_t pk, uint32_t need) {
+  return (pk & 0xffffu) + min(need, pk >> 16);
+}
+
+// Emit the elements whose rank in S (in_s) or in S^c (!in_s) lies in
+// [lo, hi), ascending rank order: f(j, bits, rank - lo).  Requires sel_count.
+// Only the chunks overlapping the rank range are visited (warp-strided).
+template <class F>
+__device__ __forceinline__ void sel_range_emit(int n, SelResult r, const SelSmem& s, bool in_s,
+                                               uint32_t lo, uint32_t hi, F&& f) {
+  if (lo >= hi) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int chunks = (n + 31) / 32;
+  // number of (S or S^c) elements before chunk c, monotone in c
+  auto before = [&](int c) -> uint32_t {
+    const uint32_t sb = sel_before(lds(s.cand + 4u * c), r.need);
+    return in_s ? sb : static_cast<uint32_t>(min(32 * c, n)) - sb;
+  };
+  // first chunk with before(c+1) > lo, last chunk with before(c) < hi
+  int a = 0, b = chunks;  // invariant: answer in [a, b)
+  while (a + 1 < b) {
+    const int mid = (a + b) >> 1;
+    if (before(mid) <= lo) a = mid; else b = mid;
   }
-  for (int base = j_lo; base < j_hi; base += 32) {
-    const int j = base + lane;
-    const bool valid = j < j_hi;
-    const uint32_t bits = valid ? s.keys[j] : 0u;
+  const int c_first = a;
+  a = c_first;
+  b = chunks;
+  while (a + 1 < b) {
+    const int mid = (a + b) >> 1;
+    if (before(mid) < hi) a = mid; else b = mid;
+  }
+  const int c_last = a;
+  const uint32_t lt = lanemask_lt();
+  for (int c = c_first + warp; c <= c_last; c += kWarps) {
+    const int j = c * 32 + lane;
+    const uint32_t bits = lds(s.keys + 4u * min(j, n - 1));
     const uint32_t key = abs_key(bits);
-    const bool gt = valid && key > r.T;
-    const bool tie = valid && key == r.T;
-    const uint32_t tmask = __ballot_sync(0xffffffffu, tie);
-    const uint32_t trank = tie_before + __popc(tmask & lanemask_lt());
-    const bool in = gt || (tie && trank < r.need);
-    const uint32_t smask = __ballot_sync(0xffffffffu, in);
-    const uint32_t srank = sel_before + __popc(smask & lanemask_lt());
-    if (valid) f(j, bits, in, in ? srank : static_cast<uint32_t>(j) - srank);
-    tie_before += __popc(tmask);
-    sel_before += __popc(smask);
+    const uint32_t gm = __ballot_sync(0xffffffffu, j < n && key > r.T);
+    const uint32_t tm = __ballot_sync(0xffffffffu, j < n && key == r.T);
+    const uint32_t pk = lds(s.cand + 4u * c);
+    const uint32_t tie_pre = pk >> 16;
+    const uint32_t take = r.need > tie_pre ? min(r.need - tie_pre, static_cast<uint32_t>(__popc(tm))) : 0u;
+    const uint32_t smask = gm | lowest_bits(tm, take);
+    const bool in = (smask >> lane) & 1u;
+    const uint32_t srank = sel_before(pk, r.need) + __popc(smask & lt);
+    const uint32_t rank = in ? srank : static_cast<uint32_t>(j) - srank;
+    if (j < n && in == in_s && rank >= lo && rank < hi) f(j, bits, rank - lo);
   }
 }
 
