@@ -142,7 +142,7 @@ rsp_status make_plan(const rsp_linear& L, const DevProps& dp, LaunchPlan* out) {
   const int vrow = static_cast<int>(L.m_pad * L.es / 16);   // 16-B units per W^T row
   const int vb = static_cast<int>(L.r_pad * L.es / 16);     // 16-B units per B_r^T row
   const int c1 = L.rank ? (vb + 31) / 32 : 0;               // warps per B_r^T row
-  if (c1 > 8)
+  if (c1 > 8 || L.r_pad > rsp::kTAccCap)
     return fail(RSP_E_UNSUPPORTED, "rank %u too large (B_r^T rows limited to 4 KB)", L.rank);
   const int max_tiles = env_int("RSP_MAX_TILES", 16);
   int nt = std::max(1, std::min(vrow / 32, max_tiles));
@@ -159,8 +159,8 @@ rsp_status make_plan(const rsp_linear& L, const DevProps& dp, LaunchPlan* out) {
   p.k_splits = ks;
   p.grid = nt * ks;
   p.nb_pad = static_cast<int>(round_up(static_cast<uint32_t>(p.grid), 4u));
-  p.cap_w = static_cast<int>((n + ks - 1) / ks) + 1;  // covers the dense sweep too
-  p.cap_u = static_cast<int>((n - L.k + p.grid - 1) / p.grid) + 1;
+  p.cap_w = static_cast<int>((n + ks - 1) / ks) + 1;  // W channel range of one CTA
+  p.cap_u = static_cast<int>((n + p.grid - 1) / p.grid) + 1;  // stage-1 channel range of one CTA
   p.cap_a = static_cast<int>((L.rank + ks - 1) / ks) + 4;
   p.a_smem_bytes = 0;
   const size_t base = rsp::fused_smem_bytes(p, static_cast<int>(n));
@@ -176,8 +176,12 @@ rsp_status make_plan(const rsp_linear& L, const DevProps& dp, LaunchPlan* out) {
     p.a_smem_bytes = static_cast<int>(std::min(want_a, room) / 16 * 16);
   }
   p.smem = rsp::fused_smem_bytes(p, static_cast<int>(n));
-  const size_t bars = round_up(4u * (2u + static_cast<uint32_t>(nt)), 256u);
-  p.ws_t_off = bars;
+  // Workspace: the barrier words and the double-buffered stage-1 sums sit at
+  // fixed offsets, so layers of any shape may share one workspace (the t
+  // buffers carry state from one launch to the next); per-launch scratch follows.
+  static_assert(4 * (2 + 148) <= rsp::kWsBarBytes, "barrier region");
+  p.ws_acc_off = rsp::kWsBarBytes;
+  p.ws_t_off = p.ws_acc_off + 2u * 4u * rsp::kTAccCap;
   p.ws_y_off = p.ws_t_off + round_up(4u * static_cast<uint32_t>(p.nb_pad) * std::max(L.r_pad, 8u), 256u);
   p.ws_bytes = p.ws_y_off + static_cast<size_t>(4) * ks * L.m_pad;
   *out = p;
@@ -195,6 +199,7 @@ FusedParams fused_params(const rsp_linear* h, const void* x, rsp_dtype xdt, floa
   uint8_t* w = static_cast<uint8_t*>(ws);
   p.bars = reinterpret_cast<unsigned*>(w);
   p.t_part = reinterpret_cast<float*>(w + h->plan.ws_t_off);
+  p.t_acc = reinterpret_cast<float*>(w + h->plan.ws_acc_off);
   p.y_part = reinterpret_cast<float*>(w + h->plan.ws_y_off);
   p.n = static_cast<int>(h->m_in);
   p.m = static_cast<int>(h->m);

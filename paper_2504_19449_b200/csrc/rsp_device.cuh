@@ -132,6 +132,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// One 128-byte line into L2 (LSU path; cheap to issue, unlike TMA bulk ops,
+// which an SM processes one at a time at ~25 ns each).
+__device__ __forceinline__ void prefetch_l2_line(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 __device__ __forceinline__ void prefetch_l2_bulk(const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
@@ -183,15 +189,15 @@ __device__ __forceinline__ void griddep_launch_dependents() {
 // last arriver resets count and publishes gen+1 with release semantics, so the
 // words are ready for the next use without any host-side reset.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ unsigned gbar_arrive(unsigned* bar, unsigned expected) {
-  const unsigned g = ld_relaxed_gpu(bar + 1);
+// `g` is the generation the caller read before any CTA of this use could
+// have arrived (e.g. right after griddepcontrol.wait).
+__device__ __forceinline__ void gbar_arrive(unsigned* bar, unsigned expected, unsigned g) {
   __threadfence();
   const unsigned old = atom_add_acq_rel_gpu(bar, 1u);
   if (old == expected - 1) {
     st_relaxed_gpu(bar, 0u);
     st_release_gpu(bar + 1, g + 1);
   }
-  return g;
 }
 
 __device__ __forceinline__ void gbar_wait(const unsigned* bar, unsigned g) {

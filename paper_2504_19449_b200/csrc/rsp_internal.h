@@ -8,6 +8,10 @@
 
 namespace rsp {
 
+// Workspace regions at fixed offsets (shared by every layer using a workspace).
+constexpr unsigned kWsBarBytes = 1024;  // {count, gen} + per-column-tile tickets
+constexpr unsigned kTAccCap = 2048;     // floats per stage-1 t buffer (r_pad <= 2048)
+
 // Parameters of one fused R-Sparse forward launch (see rsp_kernels.cu).
 struct FusedParams {
   const void* Wt;  // [n][m_pad]  input-channel-major W (row j = W[:, j])
@@ -15,7 +19,8 @@ struct FusedParams {
   const void* Bt;  // [n][r_pad]  B_r^T (row j = column j of b_r)
   const void* x;   // [n] fp32 or bf16
   float* y;        // [m] fp32
-  float* t_part;   // [r_pad][nb_pad] stage-1 partial sums (column b = CTA b)
+  float* t_part;   // [r_pad][nb_pad] stage-1 partial sums (column b = CTA b; deterministic mode)
+  float* t_acc;    // [2][kTAccCap] stage-1 sums by float atomics (fast mode; buffer = barrier gen & 1)
   float* y_part;   // [k_splits][m_pad] split-K partial sums
   unsigned* bars;  // [2] grid barrier {count, gen} + [col_tiles] tile tickets
   int n, m, m_pad, r, r_pad, k;
@@ -36,7 +41,7 @@ struct LaunchPlan {
   int a_smem_bytes = 0, nb_pad = 4;
   size_t smem = 0;
   size_t ws_bytes = 0;  // workspace: barriers + t_part + y_part
-  size_t ws_t_off = 0, ws_y_off = 0;
+  size_t ws_t_off = 0, ws_acc_off = 0, ws_y_off = 0;
 };
 
 // Shared-memory bytes the fused kernel needs for a plan.

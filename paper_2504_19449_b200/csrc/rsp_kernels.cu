@@ -40,28 +40,38 @@
 namespace rsp {
 
 // Shared-memory carve-up of the fused kernel (host and device agree).
-// Selection region [hist 16K | candidates 4K | keys 4n]; after selection its
-// first 32 KB hold the two reduction buffers (red1 at 0, red2 at 16K).
+// cap_w / cap_u: channels in this CTA's W / stage-1 ranges (each range is
+// split into a definite list and a boundary list of at most that length).
 struct SmemLayout {
-  uint32_t off_cand, off_keys, off_misc, off_w, off_u, off_a, off_astage, total;
+  uint32_t off_red1, off_red2, off_cand, off_misc, off_wscr, off_keys, off_w, off_wb, off_u, off_a,
+      off_b, off_astage, total;
 
   __host__ __device__ static uint32_t up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
 
   __host__ __device__ static SmemLayout make(int n, int cap_w, int cap_u, int cap_a, int a_bytes) {
     SmemLayout L;
-    uint32_t o = 4u * kHistBins;
+    uint32_t o = 4u * kHistBins;  // hist at 0
+    L.off_red1 = o;
+    o += 16384u;
+    L.off_red2 = o;
+    o += 16384u;
     L.off_cand = o;
     o += 4u * kCandWords;
-    L.off_keys = o;
-    o = up(o + 4u * static_cast<uint32_t>(n), 16);
-    o = o > 32768u ? o : 32768u;
     L.off_misc = o;
     o += 4u * kMiscWords;
+    L.off_wscr = o;
+    o += 4u * (256 + 64);
+    L.off_keys = o;
+    o = up(o + 4u * static_cast<uint32_t>(n), 16);
     L.off_w = o;
+    o = up(o + 8u * cap_w, 16);
+    L.off_wb = o;
     o = up(o + 8u * cap_w, 16);
     L.off_u = o;
     o = up(o + 8u * cap_u, 16);
     L.off_a = o;
+    o = up(o + 4u * cap_a, 16);
+    L.off_b = o;
     o = up(o + 4u * cap_a, 16);
     L.off_astage = o;
     o += static_cast<uint32_t>(a_bytes);
@@ -90,25 +100,82 @@ __device__ __forceinline__ long long gtimer() {
     if (p.trace) p.trace[blockIdx.x * 16 + (ev)] = clk() - t_start; \
   } while (0)
 
-// acc += sum over rows i = first, first+stride, ... < count of coef(i) * row(i)[lane's 16 B].
-// U rows are loaded before any is consumed (U x 512 B in flight per warp).
-// Out-of-range slots reuse the last valid row with a zero coefficient, so the
-// loads are unconditional (no predicated shared/global accesses in the body).
-template <typename WT, int U, class Row>
-__device__ __forceinline__ void stream_rows(float (&acc)[Vec<WT>::kElems], int first, int count,
-                                            int stride, bool lane_ok, Row row) {
-  for (int i0 = first; i0 < count; i0 += stride * U) {
-    uint4 u[U];
-    float c[U];
+// Partial sums of one lane's 16-byte column slice, returned in registers.
+struct Acc {
+  float v[8];
+};
+
+// Gathered rows from a shared-memory list of {channel j, coefficient bits}:
+// sum over i = first, first+stride, ... < count of coef_i * row(j_i)[lane's 16 B],
+// row(j) = base + j * row_bytes.  U rows are loaded before any is consumed
+// (U x 512 B in flight per warp); out-of-range slots reuse the last valid row
+// with a zero coefficient so every load is unconditional.  Out of line: every
+// warp role shares this one copy of the hot loop (instruction-cache footprint).
+template <typename WT, int U>
+__device__ __noinline__ Acc stream_list(uint32_t list, int first, int count, int stride, bool lane_ok,
+                                        const uint8_t* base, uint32_t row_bytes) {
+  float acc[Vec<WT>::kElems];
 #pragma unroll
-    for (int q = 0; q < U; ++q) {
-      const int i = i0 + q * stride;
-      row(min(i, count - 1), lane_ok, u[q], c[q]);
-      if (i >= count) c[q] = 0.f;
+  for (int e = 0; e < Vec<WT>::kElems; ++e) acc[e] = 0.f;
+  if (lane_ok) {
+    for (int i0 = first; i0 < count; i0 += stride * U) {
+      uint4 u[U];
+      float c[U];
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int i = i0 + q * stride;
+        const uint2 e = lds2(list + 8u * static_cast<uint32_t>(min(i, count - 1)));
+        c[q] = i < count ? __uint_as_float(e.y) : 0.f;
+        u[q] = ldg_stream(base + static_cast<size_t>(e.x) * row_bytes);
+      }
+#pragma unroll
+      for (int q = 0; q < U; ++q) Vec<WT>::fma(acc, u[q], c[q]);
     }
-#pragma unroll
-    for (int q = 0; q < U; ++q) Vec<WT>::fma(acc, u[q], c[q]);
   }
+  Acc r;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) r.v[e] = e < Vec<WT>::kElems ? acc[e] : 0.f;
+  return r;
+}
+
+// Consecutive rows (the low-rank A_r^T rows, prefetched into L2):
+// sum over i of coef[i] * (base + i * row_bytes)[lane's 16 B].
+template <typename WT, int U>
+__device__ __noinline__ Acc stream_seq(uint32_t coef, int first, int count, int stride, bool lane_ok,
+                                       const uint8_t* base, uint32_t row_bytes) {
+  float acc[Vec<WT>::kElems];
+#pragma unroll
+  for (int e = 0; e < Vec<WT>::kElems; ++e) acc[e] = 0.f;
+  if (lane_ok) {
+    for (int i0 = first; i0 < count; i0 += stride * U) {
+      uint4 u[U];
+      float c[U];
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int i = min(i0 + q * stride, count - 1);
+        c[q] = i0 + q * stride < count ? ldsf(coef + 4u * i) : 0.f;
+        u[q] = ldg_l2(base + static_cast<size_t>(i) * row_bytes);
+      }
+#pragma unroll
+      for (int q = 0; q < U; ++q) Vec<WT>::fma(acc, u[q], c[q]);
+    }
+  }
+  Acc r;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) r.v[e] = e < Vec<WT>::kElems ? acc[e] : 0.f;
+  return r;
+}
+
+template <int VE>
+__device__ __forceinline__ void acc_add(float (&acc)[VE], const Acc& a) {
+#pragma unroll
+  for (int e = 0; e < VE; ++e) acc[e] += a.v[e];
+}
+
+// floor(total * i / parts) in 32-bit arithmetic (total * parts < 2^32 for every
+// shape this kernel accepts; 64-bit division is a ~100-instruction subroutine).
+__device__ __forceinline__ int part(int total, int i, int parts) {
+  return static_cast<int>(static_cast<uint32_t>(total) * static_cast<uint32_t>(i) / static_cast<uint32_t>(parts));
 }
 
 template <typename WT, int U>
@@ -118,6 +185,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_forward_kernel(const FusedP
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr int VE = Vec<WT>::kElems;  // elements per 16 B
   constexpr int ES = static_cast<int>(sizeof(WT));
+  constexpr int M_GEN = 28;            // misc slot: barrier generation at kernel start
   const SmemLayout L = SmemLayout::make(p.n, p.cap_w, p.cap_u, p.cap_a, p.a_smem_bytes);
   const uint32_t sb = smem_base_pinned(smem);  // shared-window base: every access below is LDS/STS
   SelSmem ss;
@@ -125,13 +193,15 @@ __global__ void __launch_bounds__(kThreads, 1) fused_forward_kernel(const FusedP
   ss.cand = sb + L.off_cand;
   ss.keys = sb + L.off_keys;
   ss.misc = sb + L.off_misc;
-  const uint32_t list_w = sb + L.off_w;  // int2 {channel j, bits of x_j} per rank
-  const uint32_t list_u = sb + L.off_u;
-  const uint32_t coef_a = sb + L.off_a;  // f32 t_c per rank row
+  const uint32_t list_w = sb + L.off_w;    // int2 {channel j, bits of x_j}: definitely in S
+  const uint32_t list_wb = sb + L.off_wb;  // boundary channels of the W range (-> those in S)
+  const uint32_t list_u = sb + L.off_u;    // definitely in S^c (stage-1 range)
+  const uint32_t coef_a = sb + L.off_a;    // f32 t_c per rank row of this CTA
+  const uint32_t coef_b = sb + L.off_b;    // f32 boundary-bin part of t_c (local)
   const uint32_t a_stage = sb + L.off_astage;
   uint8_t* a_stage_ptr = smem + L.off_astage;  // cp.async destination
-  const uint32_t red1 = sb;             // [G1][r_pad] f32, after selection
-  const uint32_t red2 = sb + 16384u;    // [G2][tile cols] f32, after selection
+  const uint32_t red1 = sb + L.off_red1;   // [G1][r_pad] f32
+  const uint32_t red2 = sb + L.off_red2;   // [G2][tile cols] f32
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int b = blockIdx.x, NB = gridDim.x;
@@ -139,38 +209,23 @@ __global__ void __launch_bounds__(kThreads, 1) fused_forward_kernel(const FusedP
 
   // Column tile of this CTA in 16-byte units.
   const int vrow = p.m_pad * ES / 16;
-  const int v0 = static_cast<int>(static_cast<long long>(vrow) * ct / p.col_tiles);
-  const int v1 = static_cast<int>(static_cast<long long>(vrow) * (ct + 1) / p.col_tiles);
+  const int v0 = part(vrow, ct, p.col_tiles), v1 = part(vrow, ct + 1, p.col_tiles);
   const int tw = v1 - v0, tcw = tw * VE, col0 = v0 * VE;
 
   const int k_eff = p.dense ? p.n : p.k;
   const bool has_lr = !p.dense && p.r > 0 && k_eff < p.n;
-  const int nu = p.n - k_eff;
-  const int wlo = static_cast<int>(static_cast<long long>(k_eff) * ks / p.k_splits);
-  const int whi = static_cast<int>(static_cast<long long>(k_eff) * (ks + 1) / p.k_splits);
-  const int ulo = has_lr ? static_cast<int>(static_cast<long long>(nu) * b / NB) : 0;
-  const int uhi = has_lr ? static_cast<int>(static_cast<long long>(nu) * (b + 1) / NB) : 0;
-  const int alo = has_lr ? static_cast<int>(static_cast<long long>(p.r) * ks / p.k_splits) : 0;
-  const int ahi = has_lr ? static_cast<int>(static_cast<long long>(p.r) * (ks + 1) / p.k_splits) : 0;
-  const int nw = whi - wlo, n1 = uhi - ulo, na = ahi - alo;
+  // Static channel ranges: the W rows of S in [wc0, wc1) for this column
+  // tile, the stage-1 rows of S^c in [uc0, uc1).
+  const int wc0 = part(p.n, ks, p.k_splits), wc1 = part(p.n, ks + 1, p.k_splits);
+  const int uc0 = has_lr ? part(p.n, b, NB) : 0, uc1 = has_lr ? part(p.n, b + 1, NB) : 0;
+  const int alo = has_lr ? part(p.r, ks, p.k_splits) : 0, ahi = has_lr ? part(p.r, ks + 1, p.k_splits) : 0;
+  const int na = ahi - alo;
   // A_r^T rows held in shared memory (the rest stream from L2 after a prefetch).
   const int na_s = has_lr ? min(na, p.a_smem_bytes / max(1, tw * 16)) : 0;
-  // Combine split-K partials of y with float atomics into a y zeroed before the
-  // grid barrier (fast), or deterministically by the tile's last CTA.
-  const bool red_y = has_lr && p.k_splits > 1 && !p.deterministic;
-
-  // Role split: W1 stage-1 warps (multiple of C1), the rest stream W / A_r.
-  const int vb = p.r_pad * ES / 16;  // 16-B units per B_r^T row
-  const int C1 = has_lr ? (vb + 31) / 32 : 1;
-  const int C2 = (tw + 31) / 32;
-  int W1 = 0;
-  if (has_lr) {
-    const long long s1 = static_cast<long long>(n1) * C1, s2 = static_cast<long long>(nw) * C2;
-    const int want = static_cast<int>((kWarps * s1 + s1 + s2 - 1) / (s1 + s2 > 0 ? s1 + s2 : 1));
-    W1 = max(1, (want + C1 - 1) / C1) * C1;
-    W1 = min(W1, ((kWarps - C2) / C1) * C1);
-  }
-  const int nWW = kWarps - W1;
+  // Fast mode: stage-1 sums and split-K partials of y are combined with float
+  // atomics.  Deterministic mode: fixed-order partial sums (bit-reproducible).
+  const bool fast = !p.deterministic;
+  const bool red_y = has_lr && p.k_splits > 1 && fast;
 
   const uint8_t* Wt = static_cast<const uint8_t*>(p.Wt);
   const uint8_t* At = static_cast<const uint8_t*>(p.At);
@@ -187,137 +242,294 @@ __global__ void __launch_bounds__(kThreads, 1) fused_forward_kernel(const FusedP
       cp_async16(a_stage_ptr + static_cast<size_t>(f) * 16, a_tile + static_cast<size_t>(alo + i) * rowW + v * 16);
     }
     cp_async_commit();
-    for (int i = na_s + tid; i < na; i += kThreads)
-      prefetch_l2_bulk(a_tile + static_cast<size_t>(alo + i) * rowW, static_cast<uint32_t>(tw) * 16u);
+    const int la = (tw * 16 + 127) / 128;
+    for (int f = tid; f < (na - na_s) * la; f += kThreads) {
+      const int i = na_s + f / la, l = f % la;
+      prefetch_l2_line(a_tile + static_cast<size_t>(alo + i) * rowW + 128 * l);
+    }
   }
   if (p.pdl) {
     griddep_wait();
     griddep_launch_dependents();
   }
-  unsigned gen0 = 0;
-  if (has_lr && tid == 0) gen0 = ld_relaxed_gpu(p.bars + 1);
+  if (has_lr && tid == 0) {
+    const unsigned g = ld_relaxed_gpu(p.bars + 1);  // stable: nobody of this launch has arrived yet
+    ss.set_m(M_GEN, g);
+  }
   if (red_y) {  // zero this CTA's slice of y; published by the grid barrier below
-    const int y0 = static_cast<int>(static_cast<long long>(p.m) * b / NB);
-    const int y1 = static_cast<int>(static_cast<long long>(p.m) * (b + 1) / NB);
+    const int y0 = part(p.m, b, NB), y1 = part(p.m, b + 1, NB);
     for (int i = y0 + tid; i < y1; i += kThreads) p.y[i] = 0.f;
   }
   if (tid == 0) RSP_TRACE(1);
 
-  // ---- 1. exact selection (redundant per CTA: x is at most a few tens of KB) ----
+  // ---- 1. x -> shared keys + 12-bit histogram; the boundary bin ----
   __syncthreads();  // histogram zeroed (prologue) before the load adds to it
   sel_load(p.x, p.x_bf16 != 0, p.n, ss, !p.dense);
   if (tid == 0) RSP_TRACE(2);
-  SelResult sr{0u, static_cast<uint32_t>(p.n)};
-  if (!p.dense) sr = sel_resolve(p.n, p.k, p.x_bf16 != 0, ss);
+  const Boundary bd = p.dense ? Boundary{0u, 0u, 0u, true} : sel_boundary(p.n, p.k, ss);
+  if (tid == 0) RSP_TRACE(14);
+  const bool bnd = !bd.all_in && bd.b12 != 0xffffffffu;  // a boundary bin must be cut
+  const bool gathered = bnd && bd.cnt <= static_cast<uint32_t>(kCandWords / 2);
+  const uint32_t gen0 = has_lr ? ss.m(M_GEN) : 0u;
+  float* t_cur = p.t_acc + (gen0 & 1u) * kTAccCap;
+  if (has_lr && fast) {
+    // Zero this CTA's slice of the next launch's t buffer (whole buffer: the
+    // next launch on this workspace may be a layer of a larger rank).
+    float* t_nxt = p.t_acc + ((gen0 + 1u) & 1u) * kTAccCap;
+    const int c0 = part(static_cast<int>(kTAccCap), b, NB), c1 = part(static_cast<int>(kTAccCap), b + 1, NB);
+    for (int c = c0 + tid; c < c1; c += kThreads) t_nxt[c] = 0.f;
+  }
+  if (gathered) {  // boundary-bin members for the resolver (order irrelevant)
+    for (int j = tid; j < p.n; j += kThreads) {
+      const uint32_t key = abs_key(ss.key(j));
+      if ((key >> 19) == bd.b12) sts2(ss.cand + 8u * atoms_add(ss.misc + 4u * M_CC, 1u), key, static_cast<uint32_t>(j));
+    }
+  }
   if (tid == 0) RSP_TRACE(3);
-  // ---- 2. this CTA's row lists: rank ranges of S and of S^c ----
-  sel_count(p.n, sr, ss);
-  sel_range_emit(p.n, sr, ss, true, static_cast<uint32_t>(wlo), static_cast<uint32_t>(whi),
-                 [&](int j, uint32_t bits, uint32_t i) { sts2(list_w + 8u * i, static_cast<uint32_t>(j), bits); });
-  sel_range_emit(p.n, sr, ss, false, static_cast<uint32_t>(ulo), static_cast<uint32_t>(uhi),
-                 [&](int j, uint32_t bits, uint32_t i) { sts2(list_u + 8u * i, static_cast<uint32_t>(j), bits); });
+  // ---- 2. this CTA's row lists: definite members now, boundary members deferred ----
+  sel_compact(ss, wc0, wc1, bd, 0, [&](int cls, uint32_t i, int j, uint32_t bits) {
+    if (cls == 0) sts2(list_w + 8u * i, static_cast<uint32_t>(j), bits);
+    else if (cls == 1) sts2(list_wb + 8u * i, static_cast<uint32_t>(j), bits);
+  });
+  if (tid == 0) RSP_TRACE(15);
+  if (has_lr) {
+    // stage 1 takes only the definitely-unselected channels; the boundary
+    // bin's unselected members enter t locally (coef_b) once the cut is known
+    sel_compact(ss, uc0, uc1, bd, 1, [&](int cls, uint32_t i, int j, uint32_t bits) {
+      if (cls == 2) sts2(list_u + 8u * i, static_cast<uint32_t>(j), bits);
+    });
+  }
   __syncthreads();
+  const int nw_def = static_cast<int>(ss.m(M_CLS + 0)), nw_bnd = static_cast<int>(ss.m(M_CLS + 1));
+  const int nu_def = has_lr ? static_cast<int>(ss.m(M_CLS + 5)) : 0;
+  // Start every definite row's DRAM -> L2 transfer now (128-byte line
+  // prefetches flattened over the block), plus the A_r rows' slices of the
+  // boundary members' B_r^T rows (needed for coef_b).
+  {
+    const int lw = (tw * 16 + 127) / 128, lu = (static_cast<int>(rowB) + 127) / 128;
+    const int tot_w = nw_def * lw, tot = tot_w + nu_def * lu;
+    for (int f = tid; f < tot; f += kThreads) {
+      if (f < tot_w) {
+        const int i = f / lw, l = f - i * lw;
+        prefetch_l2_line(Wt + static_cast<size_t>(lds(list_w + 8u * i)) * rowW + static_cast<size_t>(col0) * ES + 128 * l);
+      } else {
+        const int g = f - tot_w, i = g / lu, l = g - i * lu;
+        prefetch_l2_line(Bt + static_cast<size_t>(lds(list_u + 8u * i)) * rowB + 128 * l);
+      }
+    }
+    if (has_lr && gathered && na > 0) {
+      const int lb = (na * ES + 127) / 128 + 1;
+      for (int f = tid; f < static_cast<int>(bd.cnt) * lb; f += kThreads) {
+        const int i = f / lb, l = f - i * lb;
+        const uint32_t j = lds(ss.cand + 8u * i + 4u);
+        const uint8_t* q = Bt + static_cast<size_t>(j) * rowB + static_cast<size_t>(alo) * ES + 128 * l;
+        if (128 * l < na * ES + 128) prefetch_l2_line(q);
+      }
+    }
+  }
   if (tid == 0) RSP_TRACE(4);
 
-  if (warp < W1) {
+  // Roles: warp 0 resolves the boundary; W1 stage-1 warps (a multiple of C1);
+  // the remaining nWW warps stream W then A_r.
+  const int vb = p.r_pad * ES / 16;  // 16-B units per B_r^T row
+  const int C1 = has_lr ? (vb + 31) / 32 : 1;
+  const int C2 = (tw + 31) / 32;
+  constexpr int kWork = kWarps - 1;
+  int W1 = 0;
+  if (has_lr) {
+    const int s1 = nu_def * C1 + na, s2 = (nw_def + nw_bnd) * C2;
+    const int want = (kWork * s1 + s1 + s2 - 1) / (s1 + s2 > 0 ? s1 + s2 : 1);
+    W1 = max(1, (want + C1 - 1) / C1) * C1;
+    W1 = min(W1, ((kWork - C2) / C1) * C1);
+  }
+  const int nWW = kWork - W1;
+  constexpr int M_T = 29, M_J = 30;
+
+  if (warp == 0) {
+    // ===================== boundary resolver =====================
+    if (bnd && (nw_bnd > 0 || has_lr)) {
+      uint32_t T, J;
+      warp_resolve_cut(ss, p.n, bd, gathered, sb + L.off_wscr, T, J);
+      if (lane == 0) {
+        ss.set_m(M_T, T);
+        ss.set_m(M_J, J);
+      }
+      // keep the W-range boundary members that are in S (order preserved)
+      uint32_t keep_w = 0;
+      for (int i0 = 0; i0 < nw_bnd; i0 += 32) {
+        const int i = i0 + lane;
+        const uint2 e = i < nw_bnd ? lds2(list_wb + 8u * i) : make_uint2(0u, 0u);
+        const uint32_t key = abs_key(e.y);
+        const bool in = i < nw_bnd && (key > T || (key == T && e.x <= J));
+        const uint32_t m = __ballot_sync(0xffffffffu, in);
+        __syncwarp();
+        if (in) sts2(list_wb + 8u * (keep_w + __popc(m & lanemask_lt())), e.x, e.y);
+        keep_w += __popc(m);
+      }
+      if (lane == 0) ss.set_m(M_CLS + 1, keep_w);
+    }
+    if (tid == 0) RSP_TRACE(13);
+    named_bar_arrive(4, kThreads);  // boundary cut published
+    return;
+  }
+
+  if (warp <= W1) {
     // ===================== stage-1 warps =====================
-    const int G1 = W1 / C1, g1 = warp / C1;
-    const int v = (warp % C1) * 32 + lane;
+    const int sw = warp - 1, nst = W1 * 32, stid = tid - 32;
+    const int G1 = W1 / C1, g1 = sw / C1;
+    const int v = (sw % C1) * 32 + lane;
     const bool ok = v < vb;
     float acc[VE];
 #pragma unroll
     for (int e = 0; e < VE; ++e) acc[e] = 0.f;
-    const uint8_t* base = Bt + v * 16;
-    stream_rows<WT, U>(acc, g1, n1, G1, ok, [&](int i, bool lok, uint4& u, float& c) {
-      const uint2 e = lds2(list_u + 8u * i);
-      c = __uint_as_float(e.y);
-      u = lok ? ldg_stream(base + static_cast<size_t>(e.x) * rowB) : make_uint4(0, 0, 0, 0);
-    });
-    if (tid == 0) RSP_TRACE(5);
+    acc_add(acc, stream_list<WT, U>(list_u, g1, nu_def, G1, ok, Bt + v * 16, static_cast<uint32_t>(rowB)));
+    if (stid == 0) RSP_TRACE(5);
     if (ok) {
 #pragma unroll
       for (int e = 0; e < VE; ++e) stsf(red1 + 4u * (g1 * p.r_pad + v * VE + e), acc[e]);
     }
-    named_bar_sync(1, W1 * 32);
-    // partial t of this CTA: column b of t_part[r_pad][nb_pad]
-    for (int c = tid; c < p.r_pad; c += W1 * 32) {
+    named_bar_sync(1, nst);
+    // this CTA's stage-1 contribution: float atomics into t (fast) or
+    // column b of the partials (deterministic)
+    for (int c = stid; c < p.r_pad; c += nst) {
       float sum = 0.f;
       for (int g = 0; g < G1; ++g) sum += ldsf(red1 + 4u * (g * p.r_pad + c));
-      p.t_part[static_cast<size_t>(c) * p.nb_pad + b] = sum;
+      if (fast) {
+        if (sum != 0.f) atomicAdd(t_cur + c, sum);
+      } else {
+        p.t_part[static_cast<size_t>(c) * p.nb_pad + b] = sum;
+      }
     }
-    __threadfence();
-    named_bar_sync(1, W1 * 32);
-    if (tid == 0) {
-      gbar_arrive(p.bars, static_cast<unsigned>(NB));
+    named_bar_sync(1, nst);
+    if (stid == 0) {
+      gbar_arrive(p.bars, static_cast<unsigned>(NB), gen0);
       RSP_TRACE(6);
+    }
+    // Boundary members not in S enter t through this CTA's rank rows only (t
+    // is linear): coef_b[i] = sum of x_j * Bt[j][alo + i] over them.  Members
+    // split across the stage-1 warps, rows across lanes, fixed-order combine.
+    named_bar_sync(4, kThreads);
+    if (bnd && na > 0) {
+      const uint32_t T = ss.m(M_T), J = ss.m(M_J);
+      // channel order (not the gathered list's arrival order): deterministic sums
+      const int q0 = part(p.n, sw, W1), q1 = part(p.n, sw + 1, W1);
+      const uint8_t* brow0 = Bt + static_cast<size_t>(alo) * ES;
+      for (int i0 = 0; i0 < na; i0 += 128) {
+        float cb[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int qb = q0; qb < q1; qb += 32) {  // warp-uniform trip count
+          const int q = qb + lane;
+          const uint32_t j = static_cast<uint32_t>(q);
+          const uint32_t bits = q < q1 ? ss.key(q) : 0u;
+          const uint32_t key = abs_key(bits);
+          const bool out = q < q1 && (key >> 19) == bd.b12 && !(key > T || (key == T && j <= J));
+          uint32_t mk = __ballot_sync(0xffffffffu, out);
+          while (mk) {  // four members per round: 16 independent loads in flight
+            uint32_t jj[4];
+            float xx[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int src = mk ? __ffs(mk) - 1 : 0;
+              const bool have = mk != 0;
+              mk &= mk - 1;
+              jj[u] = __shfl_sync(0xffffffffu, j, src);
+              xx[u] = have ? __uint_as_float(__shfl_sync(0xffffffffu, bits, src)) : 0.f;
+            }
+            float w[4][4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const uint8_t* row = brow0 + static_cast<size_t>(jj[u]) * rowB;
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int i = i0 + lane + 32 * e;
+                w[u][e] = 0.f;
+                if (i < na) {
+                  if constexpr (ES == 2)
+                    w[u][e] = __bfloat162float(__ldg(reinterpret_cast<const __nv_bfloat16*>(row) + i));
+                  else
+                    w[u][e] = __ldg(reinterpret_cast<const float*>(row) + i);
+                }
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+#pragma unroll
+              for (int e = 0; e < 4; ++e) cb[e] = fmaf(xx[u], w[u][e], cb[e]);
+            }
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) stsf(red1 + 4u * (sw * 128 + lane + 32 * e), cb[e]);
+        named_bar_sync(1, nst);
+        for (int i = i0 + stid; i < min(na, i0 + 128); i += nst) {
+          float sum = 0.f;
+          for (int w = 0; w < W1; ++w) sum += ldsf(red1 + 4u * (w * 128 + i - i0));
+          stsf(coef_b + 4u * i, sum);
+        }
+        named_bar_sync(1, nst);
+      }
+    } else {
+      for (int i = stid; i < na; i += nst) stsf(coef_b + 4u * i, 0.f);
+    }
+    if (stid == 0) {
       gbar_wait(p.bars, gen0);
       RSP_TRACE(7);
     }
-    named_bar_sync(1, W1 * 32);
-    // t_c for this CTA's rank rows: 8 lanes per row sum the row's nb_pad
-    // partials (float4 loads, fixed order, then a fixed xor tree).
-    const int g8 = tid >> 3, l8 = tid & 7, ng8 = W1 * 4;
-    const int nq = p.nb_pad / 4;
-    for (int cbase = alo; cbase < ahi; cbase += ng8 * 4) {  // uniform trip count: shuffles below
-      const int c0 = cbase + g8;
-      float s4[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int rr = 0; rr < 4; ++rr) {
-        const int c = c0 + rr * ng8;
+    named_bar_sync(1, nst);
+    // t_c for this CTA's rank rows
+    if (fast) {
+      for (int i = stid; i < na; i += nst) stsf(coef_a + 4u * i, __ldcg(t_cur + alo + i) + ldsf(coef_b + 4u * i));
+    } else {
+      // 8 lanes per row sum the row's nb_pad partials (float4 loads, fixed order, fixed xor tree)
+      const int g8 = stid >> 3, l8 = stid & 7, ng8 = nst / 8;
+      const int nq = p.nb_pad / 4;
+      for (int cbase = alo; cbase < ahi; cbase += ng8) {  // uniform trip count: shuffles below
+        const int c = cbase + g8;
+        float sum = 0.f;
         if (c < ahi) {
           const float4* row = reinterpret_cast<const float4*>(p.t_part + static_cast<size_t>(c) * p.nb_pad);
           for (int q = l8; q < nq; q += 8) {
-            const float4 t = __ldcg(row + q);
-            s4[rr] += (t.x + t.y) + (t.z + t.w);
+            const float4 u = __ldcg(row + q);
+            sum += (u.x + u.y) + (u.z + u.w);
           }
         }
-      }
-#pragma unroll
-      for (int rr = 0; rr < 4; ++rr) {
-        float v8 = s4[rr];
-        v8 += __shfl_xor_sync(0xffffffffu, v8, 4);
-        v8 += __shfl_xor_sync(0xffffffffu, v8, 2);
-        v8 += __shfl_xor_sync(0xffffffffu, v8, 1);
-        const int c = c0 + rr * ng8;
-        if (l8 == 0 && c < ahi) stsf(coef_a + 4u * (c - alo), v8);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 4);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+        if (l8 == 0 && c < ahi) stsf(coef_a + 4u * (c - alo), sum + ldsf(coef_b + 4u * (c - alo)));
       }
     }
-    if (tid == 0) RSP_TRACE(8);
+    if (stid == 0) RSP_TRACE(8);
     cp_async_wait_all();
-    named_bar_arrive(3, kThreads);  // coef_a (and this thread's A_r copies) are ready
+    named_bar_arrive(3, (W1 + nWW) * 32);  // coef_a (and this thread's A_r copies) are ready
     return;
   }
 
   // ===================== W / A_r warps =====================
-  const int wr = warp - W1, G2 = nWW / C2, g2 = wr / C2;
+  const int wr = warp - 1 - W1, G2 = nWW / C2, g2 = wr / C2;
   const int v = (wr % C2) * 32 + lane;
   const bool ok = g2 < G2 && v < tw;
-  const int wt = tid - W1 * 32, nwt = nWW * 32;
+  const int wt = tid - (1 + W1) * 32, nwt = nWW * 32;
   float acc[VE];
 #pragma unroll
   for (int e = 0; e < VE; ++e) acc[e] = 0.f;
   const uint8_t* wbase = Wt + static_cast<size_t>(col0) * ES + v * 16;
-  if (g2 < G2)
-    stream_rows<WT, U>(acc, g2, nw, G2, ok, [&](int i, bool lok, uint4& u, float& c) {
-      const uint2 e = lds2(list_w + 8u * i);
-      c = __uint_as_float(e.y);
-      u = lok ? ldg_stream(wbase + static_cast<size_t>(e.x) * rowW) : make_uint4(0, 0, 0, 0);
-    });
+  acc_add(acc, stream_list<WT, U>(list_w, g2, nw_def, G2, ok, wbase, static_cast<uint32_t>(rowW)));
+  named_bar_sync(4, kThreads);
+  acc_add(acc, stream_list<WT, U>(list_wb, g2, static_cast<int>(ss.m(M_CLS + 1)), G2, ok, wbase,
+                                  static_cast<uint32_t>(rowW)));
   if (wt == 0) RSP_TRACE(9);
   if (has_lr) {
     cp_async_wait_all();
-    named_bar_sync(3, kThreads);  // stage-1 warps have published coef_a; A_r^T rows landed
+    named_bar_sync(3, (W1 + nWW) * 32);  // stage-1 warps have published coef_a; A_r^T rows landed
     if (g2 < G2) {
       if (ok) {
         for (int i = g2; i < na_s; i += G2)
           Vec<WT>::fma(acc, lds4(a_stage + (static_cast<uint32_t>(i) * tw + v) * 16u), ldsf(coef_a + 4u * i));
       }
-      const uint8_t* abase = a_tile + v * 16;
       const int first = na_s + ((g2 - na_s % G2) % G2 + G2) % G2;  // keep row i on group i % G2
-      stream_rows<WT, U>(acc, first, na, G2, ok, [&](int i, bool lok, uint4& u, float& c) {
-        c = ldsf(coef_a + 4u * i);
-        u = lok ? ldg_l2(abase + static_cast<size_t>(alo + i) * rowW) : make_uint4(0, 0, 0, 0);
-      });
+      acc_add(acc, stream_seq<WT, U>(coef_a, first, na, G2, ok,
+                                     a_tile + static_cast<size_t>(alo) * rowW + v * 16,
+                                     static_cast<uint32_t>(rowW)));
     }
   }
   if (wt == 0) RSP_TRACE(10);
@@ -380,7 +592,7 @@ cudaError_t fused_set_smem(int elem_bytes, size_t smem) {
 static int unroll_choice() {
   static int u = [] {
     const char* v = getenv("RSP_UNROLL");
-    return (v && atoi(v) == 8) ? 8 : 16;
+    return (v && atoi(v) == 16) ? 16 : 8;
   }();
   return u;
 }

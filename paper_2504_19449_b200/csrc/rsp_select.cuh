@@ -46,7 +46,7 @@ namespace rsp {
 constexpr int kHistBins = 4096;  // key >> 19
 constexpr int kCandCap = 1024;
 constexpr int kCandWords = kCandCap + 64;  // also holds the per-chunk prefix (n/32 + 1 <= 1025)
-constexpr int kMiscWords = 96;
+constexpr int kMiscWords = 192;
 
 // misc[] word slots
 enum : int {
@@ -380,6 +380,225 @@ __device__ __forceinline__ void sel_range_emit(int n, SelResult r, const SelSmem
     const uint32_t rank = in ? srank : static_cast<uint32_t>(j) - srank;
     if (j < n && in == in_s && rank >= lo && rank < hi) f(j, bits, rank - lo);
   }
+}
+
+// ===========================================================================
+// Fused-kernel selection: static channel ranges + deferred boundary.
+//
+// The fused kernel never ranks all n channels.  After the 12-bit histogram,
+// every channel is classified by its 12-bit bin c = key >> 19 against the
+// boundary bin b12 that holds the k-th largest key:
+//   c > b12  -> definitely in S;   c < b12 -> definitely in S^c;
+//   c == b12 -> boundary (resolved later by one warp: warp_resolve_cut).
+// Each CTA compacts only the channel ranges it streams, so W rows can be
+// issued right after the histogram scan.
+// ===========================================================================
+struct Boundary {
+  uint32_t b12;   // boundary bin (0xffffffff: S empty)
+  uint32_t need;  // boundary-bin members that belong to S
+  uint32_t cnt;   // boundary-bin population
+  bool all_in;    // the whole boundary bin is in S (cnt == need, or k >= n)
+};
+
+__device__ __forceinline__ Boundary sel_boundary(int n, int k, const SelSmem& s) {
+  if (k <= 0) return Boundary{0xffffffffu, 0u, 0u, false};
+  if (k >= n) return Boundary{0u, 0u, 0u, true};
+  const int tid = threadIdx.x;
+  const uint32_t kk = static_cast<uint32_t>(k);
+  const uint32_t h = s.hist + 4u * ((kHistBins - 8) - 8 * tid);
+  const uint4 lo = lds4(h), hi = lds4(h + 16u);
+  const uint32_t c[8] = {hi.w, hi.z, hi.y, hi.x, lo.w, lo.z, lo.y, lo.x};
+  uint32_t local = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) local += c[q];
+  const uint32_t above = block_excl_scan(local, s.misc + 4u * M_SCAN, nullptr);
+  if (above < kk && kk <= above + local) {
+    uint32_t acc = above;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (acc < kk && kk <= acc + c[q]) {
+        s.set_m(M_BIN, static_cast<uint32_t>(kHistBins - 1 - 8 * tid - q));
+        s.set_m(M_ABOVE, acc);
+        s.set_m(M_CNT, c[q]);
+      }
+      acc += c[q];
+    }
+  }
+  __syncthreads();
+  Boundary b;
+  b.b12 = s.m(M_BIN);
+  b.need = kk - s.m(M_ABOVE);
+  b.cnt = s.m(M_CNT);
+  b.all_in = b.cnt == b.need;
+  return b;
+}
+
+// 0: in S, 1: boundary, 2: in S^c
+__device__ __forceinline__ int sel_class(uint32_t key, const Boundary& b) {
+  const uint32_t c = key >> 19;
+  if (b.b12 == 0xffffffffu) return 2;
+  if (c > b.b12 || (c == b.b12 && b.all_in)) return 0;
+  return c == b.b12 ? 1 : 2;
+}
+
+// Deterministic compaction of channels [lo, hi) by class: f(cls, i, j, bits)
+// with i the position among that class's members of the range in ascending
+// channel order.  Class totals land in misc[M_CLS + cls].  One barrier.
+constexpr int M_CLS = 64;   // [64, 70): class totals (3 per compaction slot)
+constexpr int M_CLSW = 72;  // [72, 168): per-warp class counts (48 per slot)
+template <class F>
+__device__ __forceinline__ void sel_compact(const SelSmem& s, int lo, int hi, const Boundary& b,
+                                            int slot, F&& f) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int len = max(0, hi - lo);
+  const int chunks = (len + 31) / 32;
+  const int per = (chunks + kWarps - 1) / kWarps;
+  const int c_lo = min(chunks, warp * per), c_hi = min(chunks, (warp + 1) * per);
+  uint32_t cnt[3] = {0u, 0u, 0u};
+#pragma unroll 1
+  for (int c = c_lo; c < c_hi; ++c) {
+    const int j = lo + c * 32 + lane;
+    const int cls = j < hi ? sel_class(abs_key(s.key(min(j, hi - 1))), b) : 3;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) cnt[q] += __popc(__ballot_sync(0xffffffffu, cls == q));
+  }
+  const uint32_t base = s.misc + 4u * (M_CLSW + slot * 3 * kWarps);
+  if (lane < 3) sts(base + 4u * (3 * warp + lane), lane == 0 ? cnt[0] : (lane == 1 ? cnt[1] : cnt[2]));
+  __syncthreads();
+  uint32_t off[3];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const uint32_t wc = lane < kWarps ? lds(base + 4u * (3 * lane + q)) : 0u;
+    uint32_t inc = wc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    off[q] = __shfl_sync(0xffffffffu, inc - wc, warp);
+    if (warp == 0 && lane == kWarps - 1) s.set_m(M_CLS + 3 * slot + q, inc);
+  }
+  const uint32_t lt = lanemask_lt();
+#pragma unroll 1
+  for (int c = c_lo; c < c_hi; ++c) {
+    const int j = lo + c * 32 + lane;
+    const uint32_t bits = s.key(min(j, hi - 1));
+    const int cls = j < hi ? sel_class(abs_key(bits), b) : 3;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const uint32_t m = __ballot_sync(0xffffffffu, cls == q);
+      if (cls == q) f(q, off[q] + __popc(m & lt), j, bits);
+      off[q] += __popc(m);
+    }
+  }
+}
+
+// One warp: the exact cut (T, J) of the reference's total order (|x| desc,
+// index asc) inside the boundary bin: its need-th member.  Members are the
+// gathered (key, index) pairs at s.cand (gathered = true, cnt pairs) or, when
+// they did not fit, every channel of the bin (scanned from keys).  Warp-local
+// 8-bit radix steps on the key (then on the index for long ties) until <= 32
+// members survive; those are ranked pairwise.  `scratch` = 256 + 64 words of
+// shared memory private to the warp.  Result in lanes: (T, J).
+__device__ __noinline__ void warp_resolve_cut(const SelSmem& s, int n, const Boundary& bd, bool gathered,
+                                                 uint32_t scratch, uint32_t& T_out, uint32_t& J_out) {
+  const int lane = threadIdx.x & 31;
+  const int src_n = gathered ? static_cast<int>(bd.cnt) : n;
+  // fetch member i: (key, index, valid)
+  auto fetch = [&](int i, uint32_t& key, uint32_t& idx) -> bool {
+    if (gathered) {
+      const uint2 e = lds2(s.cand + 8u * i);
+      key = e.x;
+      idx = e.y;
+      return true;
+    }
+    key = abs_key(s.key(i));
+    idx = static_cast<uint32_t>(i);
+    return (key >> 19) == bd.b12;
+  };
+  uint32_t kpre = bd.b12 << 19, kmask = 0xfff80000u;  // key filter
+  uint32_t ipre = 0u, imask = 0u;                      // index filter (ties)
+  uint32_t need = bd.need, alive = bd.cnt;
+  const uint32_t whist = scratch, wbuf = scratch + 4u * 256;
+  // key digits 18..11, 10..3, 2..0, then (ascending) index digits 15..8, 7..0
+#pragma unroll 1
+  for (int step = 0; step < 5 && alive > 32u; ++step) {
+    const bool on_key = step < 3;
+    const int shift = step == 0 ? 11 : step == 1 ? 3 : step == 2 ? 0 : step == 3 ? 8 : 0;
+    const int nb = step == 2 ? 8 : 256;
+    const uint32_t dmask = static_cast<uint32_t>(nb - 1);
+    for (int i = lane; i < 256; i += 32) sts(whist + 4u * i, 0u);
+    __syncwarp();
+#pragma unroll 1
+    for (int i0 = 0; i0 < src_n; i0 += 32) {
+      const int i = i0 + lane;
+      uint32_t key = 0, idx = 0;
+      const bool ok = i < src_n && fetch(i, key, idx) && (key & kmask) == kpre && (idx & imask) == ipre;
+      if (ok) reds_add(whist + 4u * ((on_key ? key : idx) >> shift & dmask), 1u);
+    }
+    __syncwarp();
+    // keys: descending bins (largest first); indices: ascending (lowest first)
+    const int per = (nb + 31) / 32;
+    uint32_t c[8], local = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int pos = lane * per + q;
+      const int bin = on_key ? nb - 1 - pos : pos;
+      c[q] = (q < per && pos < nb) ? lds(whist + 4u * bin) : 0u;
+      local += c[q];
+    }
+    uint32_t inc = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    uint32_t acc = inc - local, my_bin = 0, my_above = 0, my_cnt = 0;
+    bool found = false;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int pos = lane * per + q;
+      if (!found && acc < need && need <= acc + c[q]) {
+        found = true;
+        my_bin = static_cast<uint32_t>(on_key ? nb - 1 - pos : pos);
+        my_above = acc;
+        my_cnt = c[q];
+      }
+      acc += c[q];
+    }
+    const int src = __ffs(__ballot_sync(0xffffffffu, found)) - 1;
+    const uint32_t bin = __shfl_sync(0xffffffffu, my_bin, src);
+    need -= __shfl_sync(0xffffffffu, my_above, src);
+    alive = __shfl_sync(0xffffffffu, my_cnt, src);
+    if (on_key) {
+      kpre |= bin << shift;
+      kmask |= dmask << shift;
+    } else {
+      ipre |= bin << shift;
+      imask |= dmask << shift;
+    }
+  }
+  // <= 32 survivors: compact into lanes, rank in the total order
+  uint32_t have = 0;
+#pragma unroll 1
+  for (int i0 = 0; i0 < src_n; i0 += 32) {
+    const int i = i0 + lane;
+    uint32_t key = 0, idx = 0;
+    const bool ok = i < src_n && fetch(i, key, idx) && (key & kmask) == kpre && (idx & imask) == ipre;
+    const uint32_t bal = __ballot_sync(0xffffffffu, ok);
+    if (ok) sts2(wbuf + 8u * (have + __popc(bal & lanemask_lt())), key, idx);
+    have += __popc(bal);
+  }
+  __syncwarp();
+  const uint2 me = lane < static_cast<int>(have) ? lds2(wbuf + 8u * lane) : make_uint2(0u, 0xffffffffu);
+  uint32_t rank = 0;
+  for (int q = 0; q < static_cast<int>(have); ++q) {
+    const uint32_t ok = __shfl_sync(0xffffffffu, me.x, q), oi = __shfl_sync(0xffffffffu, me.y, q);
+    rank += (ok > me.x) || (ok == me.x && oi < me.y);
+  }
+  const int who = __ffs(__ballot_sync(0xffffffffu, lane < static_cast<int>(have) && rank == need - 1)) - 1;
+  T_out = __shfl_sync(0xffffffffu, me.x, who);
+  J_out = __shfl_sync(0xffffffffu, me.y, who);
 }
 
 }  // namespace rsp

@@ -18,10 +18,10 @@ import paper_2504_19449_b200 as rsp  # noqa: E402
 from paper_2504_19449_b200 import _lib as L  # noqa: E402
 from paper_2504_19449_b200 import workloads as wl  # noqa: E402
 
-EV = {1: "after_griddep", 2: "x_loaded", 3: "selected", 4: "lists_built", 5: "prod_S1_issued",
-      6: "prod_W_issued", 7: "prod_A_issued", 8: "cons_S1_done", 15: "cons_first_W_stage",
-      9: "cons_W_done", 10: "cons_grid_wait_done", 11: "cons_A_done", 12: "ypart_written",
-      13: "tile_barrier_done", 14: "end"}
+EV = {1: "after_griddep", 2: "x_loaded+hist", 14: "boundary_bin", 3: "gathered", 15: "W_list",
+      4: "lists+prefetch",
+      13: "resolver_done", 5: "S1_rows_done", 6: "grid_arrived", 7: "grid_wait_done", 8: "coefs_done",
+      9: "W_rows_done", 10: "A_rows_done", 11: "y_written", 12: "end"}
 SHAPES = {"q": (4096, 4096), "gate": (11008, 4096), "down": (4096, 11008)}
 
 
