@@ -269,20 +269,11 @@ def run_ours(args):
         st = rsp.Stack(layers, xs, ys)
         launch = lambda: st.launch(stream)  # noqa: E731
     else:
-        import torch.distributed as dist
-        ylocs = [torch.empty(mloc[i], dtype=torch.float32, device=dev) for i in range(len(layers))]
-        wss = [l.workspace() for l in layers]
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.stream(stream):
-            for i, l in enumerate(layers):  # warm NCCL before capture
-                l.forward(xs[i], out=ylocs[i], workspace=wss[i], stream=stream)
-                dist.all_gather_into_tensor(ys[i], ylocs[i])
-            torch.cuda.synchronize()
-            with torch.cuda.graph(g, stream=stream):
-                for i, l in enumerate(layers):
-                    l.forward(xs[i], out=ylocs[i], workspace=wss[i], stream=stream)
-                    dist.all_gather_into_tensor(ys[i], ylocs[i])
-        launch = lambda: g.replay()  # noqa: E731
+        # row-sharded linears, each followed by one in-place NCCL all-gather
+        # of y (paper_2504_19449_b200/sharding.py), captured as one graph
+        from paper_2504_19449_b200.sharding import ShardedStack
+        st = ShardedStack(layers, xs, ys, stream=stream)
+        launch = st.launch
 
     def barrier():
         if world > 1:

@@ -175,6 +175,39 @@ rsp_status rsp_linear_io_cost(const rsp_linear* h, rsp_io_report* out);
  * checker can run on exactly the values the kernels read.  Synchronous. */
 rsp_status rsp_linear_export(const rsp_linear* h, int which, double* out_host);
 
+/* -- RSPL decomposed-layer files ------------------------------------------------ */
+/* The reference's on-disk DecomposedLayer (write_decomposed_layer /
+ * read_decomposed_layer, layer.hpp:93-95, layer.cpp:243-301): magic "RSPL",
+ * u8 version 1, u32 m_in, m_out, rank, kept width ceil(s*m_in), then f32
+ * w_cols (column-major, data[j*m_out+i] = W(i,j)), f32 a_r (m_out x r),
+ * f32 b_r (r x m_in), u32 selected components[r], f64 keep_fraction, f64 rank.
+ * Little-endian.  Malformed files fail with RSP_E_IO and the reference's
+ * io_error message (bad magic, unsupported version, truncated, inconsistent
+ * rank fields). */
+typedef struct rsp_rspl_header {
+  uint32_t m_in, m_out, rank, kept_width;
+  double keep_fraction;
+} rsp_rspl_header;
+
+/* Host-only parse (no device).  Any array pointer may be NULL (skipped);
+ * w_cols holds m_in*m_out, a_r m_out*rank, b_r rank*m_in floats, comps rank. */
+rsp_status rsp_rspl_read(const char* path, rsp_rspl_header* header, float* w_cols, float* a_r,
+                         float* b_r, uint32_t* comps);
+
+/* read_decomposed_layer + upload: a device-resident operator from an RSPL
+ * file.  `opts` (may be NULL) supplies weight_dtype, device, shard_rank,
+ * shard_count, flags and k_override; its shape, plan and pointer fields are
+ * ignored (they come from the file). */
+rsp_status rsp_linear_load_rspl(const char* path, const rsp_linear_desc* opts, rsp_linear** out);
+
+/* write_decomposed_layer of the values the device holds (bf16 handles write
+ * their bf16 values widened to f32).  Unsharded handles only. */
+rsp_status rsp_linear_save_rspl(const rsp_linear* h, const char* path);
+
+/* The layer's selected SVD components (DecomposedLayer::selected_components):
+ * from the RSPL file, else 0..rank-1.  comps holds rank entries. */
+rsp_status rsp_linear_components(const rsp_linear* h, uint32_t* comps);
+
 /* -- selector ---------------------------------------------------------------- */
 /* Replaces top_k_by_magnitude(span<const double> x, size_t k) (matrix.hpp:63,
  * matrix.cpp:100-117): indices of the k largest |x|, ties to the lower index,

@@ -249,6 +249,10 @@ class RefOracle(_Lib):
                                         ct.c_uint64, ct.POINTER(ct.c_double),
                                         ct.POINTER(ct.c_double), _u64p, _u64p]
         L.rspr_bench_matvec.restype = ct.c_int
+        L.rspr_write_layer.argtypes = [ct.c_void_p, _i64p, ct.c_char_p]
+        L.rspr_write_layer.restype = ct.c_int
+        L.rspr_read_layer.argtypes = [ct.c_char_p, _u64p, _dp, _dp, _dp, _i64p, _dp]
+        L.rspr_read_layer.restype = ct.c_int
 
     class Layer:
         """An owned reference DecomposedLayer."""
@@ -311,6 +315,30 @@ class RefOracle(_Lib):
                                                comps.ctypes.data_as(_i64p)), "decompose")
         return (a[: m * rank].reshape(m, rank).copy(), b[: rank * n].reshape(rank, n).copy(),
                 comps[:rank].copy())
+
+    def write_layer(self, path: str, w_cols, a_r, b_r, keep_fraction: float, comps=None) -> None:
+        """write_decomposed_layer (layer.cpp:243-267) of the layer built from these arrays."""
+        L = self.layer(w_cols, a_r, b_r, keep_fraction)
+        cp = None
+        if comps is not None:
+            comps = np.ascontiguousarray(np.asarray(comps, dtype=np.int64))
+            cp = comps.ctypes.data_as(_i64p)
+        _raise(self.lib.rspr_write_layer(L.h, cp, path.encode()), "write_decomposed_layer")
+
+    def read_layer(self, path: str):
+        """read_decomposed_layer (layer.cpp:269-301) -> dict of arrays (float64)."""
+        dims = (ct.c_uint64 * 3)()
+        _raise(self.lib.rspr_read_layer(path.encode(), dims, None, None, None, None, None),
+               "read_decomposed_layer")
+        n, m, r = int(dims[0]), int(dims[1]), int(dims[2])
+        w = np.empty(max(n * m, 1)); a = np.empty(max(m * r, 1)); b = np.empty(max(r * n, 1))
+        comps = np.empty(max(r, 1), dtype=np.int64)
+        plan = np.empty(2)
+        _raise(self.lib.rspr_read_layer(path.encode(), dims, _d(w), _d(a), _d(b),
+                                        comps.ctypes.data_as(_i64p), _d(plan)), "read_decomposed_layer")
+        return {"m_in": n, "m_out": m, "rank": r, "w_cols": w[: n * m].reshape(n, m).copy(),
+                "a_r": a[: m * r].reshape(m, r).copy(), "b_r": b[: r * n].reshape(r, n).copy(),
+                "comps": comps[:r].copy(), "keep_fraction": float(plan[0])}
 
     def bench_matvec(self, m_in: int, m_out: int, s: float, reps: int, seed: int = 42):
         dn, gn = ct.c_double(), ct.c_double()

@@ -220,4 +220,36 @@ int rspr_bench_matvec(size_t m_in, size_t m_out, double s, size_t reps, uint64_t
   })
 }
 
+// layer.cpp:243-267: write a DecomposedLayer (from rspr_layer_create, with
+// the given selected components) to an RSPL file.
+int rspr_write_layer(void* h, const int64_t* comps, const char* path) {
+  GUARD({
+    auto* L = static_cast<DecomposedLayer*>(h);
+    if (comps)
+      for (size_t c = 0; c < L->plan.rank; ++c) L->selected_components[c] = static_cast<size_t>(comps[c]);
+    write_decomposed_layer(*L, path);
+  })
+}
+
+// layer.cpp:269-301: read an RSPL file.  dims = {m_in, m_out, rank};
+// w_cols / a_r / b_r / comps may be null (dims only); plan = {s, r}.
+int rspr_read_layer(const char* path, uint64_t* dims, double* w_cols, double* a_r, double* b_r,
+                    int64_t* comps, double* plan) {
+  GUARD({
+    const DecomposedLayer L = read_decomposed_layer(path);
+    dims[0] = L.m_in;
+    dims[1] = L.m_out;
+    dims[2] = L.plan.rank;
+    if (w_cols) std::memcpy(w_cols, L.w_cols.data.data(), L.w_cols.data.size() * sizeof(double));
+    if (a_r) std::memcpy(a_r, L.a_r.data(), L.m_out * L.plan.rank * sizeof(double));
+    if (b_r) std::memcpy(b_r, L.b_r.data(), L.plan.rank * L.m_in * sizeof(double));
+    if (comps)
+      for (size_t c = 0; c < L.plan.rank; ++c) comps[c] = static_cast<int64_t>(L.selected_components[c]);
+    if (plan) {
+      plan[0] = L.plan.keep_fraction;
+      plan[1] = static_cast<double>(L.plan.rank);
+    }
+  })
+}
+
 }  // extern "C"

@@ -24,6 +24,7 @@ EXPORTS = [
     "rsp_linear_selected", "rsp_linear_io_cost", "rsp_linear_export",
     "rsp_top_k_by_magnitude", "rsp_threshold_sparsify", "rsp_stack_create",
     "rsp_stack_launch", "rsp_stack_destroy", "rsp_device_sm_count", "rsp_debug_forward_trace",
+    "rsp_rspl_read", "rsp_linear_load_rspl", "rsp_linear_save_rspl", "rsp_linear_components",
 ]
 
 
@@ -57,6 +58,11 @@ class IoReport(ct.Structure):
         ("relative_cost", ct.c_double), ("kernel_weight_bytes", ct.c_uint64),
         ("kernel_total_bytes", ct.c_uint64), ("dense_weight_bytes", ct.c_uint64),
     ]
+
+
+class RsplHeader(ct.Structure):
+    _fields_ = [("m_in", ct.c_uint32), ("m_out", ct.c_uint32), ("rank", ct.c_uint32),
+                ("kept_width", ct.c_uint32), ("keep_fraction", ct.c_double)]
 
 
 class RspError(RuntimeError):
@@ -125,6 +131,10 @@ def lib() -> ct.CDLL:
         "rsp_stack_destroy": (None, [vp]),
         "rsp_device_sm_count": (ct.c_int, [ct.c_int]),
         "rsp_debug_forward_trace": (ct.c_int, [vp, vp, ct.c_int, vp, vp, ct.c_size_t, vp, ct.c_int, vp]),
+        "rsp_rspl_read": (ct.c_int, [ct.c_char_p, ct.POINTER(RsplHeader), vp, vp, vp, vp]),
+        "rsp_linear_load_rspl": (ct.c_int, [ct.c_char_p, ct.POINTER(LinearDesc), ct.POINTER(vp)]),
+        "rsp_linear_save_rspl": (ct.c_int, [vp, ct.c_char_p]),
+        "rsp_linear_components": (ct.c_int, [vp, ct.POINTER(u32)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

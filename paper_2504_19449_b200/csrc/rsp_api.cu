@@ -14,6 +14,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <fstream>
+#include <iterator>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -121,6 +123,7 @@ struct rsp_linear {
   void* x_pin = nullptr;
   float* y_pin = nullptr;
   uint32_t host_batch = 0;
+  std::vector<uint32_t> comps;  // DecomposedLayer::selected_components
 };
 
 struct rsp_stack {
@@ -133,49 +136,51 @@ struct rsp_stack {
 namespace {
 
 // Decompose one forward over the GPU: col_tiles column tiles x k_splits
-// K-splits, one CTA per SM.  A column tile is a whole number of 16-byte units
-// of a row; tiles of ~512 B per row (one warp-wide 16-byte load) keep the
-// split-K fan-in small (~9) so the last-CTA reduction of y is cheap.
+// channel splits, at most one CTA per SM (a second slot per SM is left for
+// the next linear's CTAs under PDL).  A column tile is C2 whole 512-byte warp
+// columns of a row (C2 in {1,2,4,8,16}); per-CTA time ~ k*C2/(16*k_splits),
+// and the split-K combine costs k_splits*m float reductions, so the cheapest
+// C2/k_splits wins with k_splits <= 32.
 rsp_status make_plan(const rsp_linear& L, const DevProps& dp, LaunchPlan* out) {
   LaunchPlan p;
   const uint32_t n = L.m_in;
-  const int vrow = static_cast<int>(L.m_pad * L.es / 16);   // 16-B units per W^T row
-  const int vb = static_cast<int>(L.r_pad * L.es / 16);     // 16-B units per B_r^T row
-  const int c1 = L.rank ? (vb + 31) / 32 : 0;               // warps per B_r^T row
-  if (c1 > 8 || L.r_pad > rsp::kTAccCap)
-    return fail(RSP_E_UNSUPPORTED, "rank %u too large (B_r^T rows limited to 4 KB)", L.rank);
-  const int max_tiles = env_int("RSP_MAX_TILES", 16);
-  int nt = std::max(1, std::min(vrow / 32, max_tiles));
-  nt = std::max(nt, (vrow + 255) / 256);                    // <= 8 warps per tile row
-  nt = std::min(nt, std::min(vrow, dp.sms));
-  int ks = std::max(1, dp.sms / nt);
+  const int vrow = static_cast<int>(L.m_pad * L.es / 16);  // 16-B units per W^T row
+  const int wcols = (vrow + 31) / 32;                       // 512-B warp columns per row
+  if (L.r_pad > rsp::kTAccCap)
+    return fail(RSP_E_UNSUPPORTED, "rank %u too large (r_pad <= %u)", L.rank, rsp::kTAccCap);
+  const int sms = std::max(1, dp.sms);
+  const int ks_cap = std::max(1, env_int("RSP_MAX_KSPLITS", 32));
+  int best_nt = 1, best_ks = 1;
+  double best = 1e30;
+  for (int c2 = 1; c2 <= 16; c2 *= 2) {
+    const int nt = (wcols + c2 - 1) / c2;
+    if (nt > sms) continue;
+    const int ks = std::min(sms / nt, ks_cap);
+    const double cost = static_cast<double>(c2) / ks;
+    if (cost < best * 0.99 || (cost <= best * 1.01 && ks <= 24)) {
+      best = std::min(best, cost);
+      best_nt = nt;
+      best_ks = ks;
+    }
+  }
+  int nt = best_nt, ks = best_ks;
   // Small layers: keep >= ~32 KB of streamed bytes per CTA.
   const double bytes = static_cast<double>(L.k + L.rank) * vrow * 16.0 +
-                       static_cast<double>(n - L.k) * vb * 16.0;
+                       static_cast<double>(n - std::min(n, L.k)) * (L.r_pad * L.es);
   const int want = std::max(1, static_cast<int>(std::ceil(bytes / 32768.0)));
   ks = std::min(ks, std::max(1, (want + nt - 1) / nt));
   ks = std::min(ks, static_cast<int>(std::max(1u, n)));
+  if (const int force = env_int("RSP_KSPLITS", 0)) ks = std::max(1, std::min(force, sms / nt));
   p.col_tiles = nt;
   p.k_splits = ks;
   p.grid = nt * ks;
   p.nb_pad = static_cast<int>(round_up(static_cast<uint32_t>(p.grid), 4u));
-  p.cap_w = static_cast<int>((n + ks - 1) / ks) + 1;  // W channel range of one CTA
+  p.cap_w = static_cast<int>((n + ks - 1) / ks) + 1;          // W channel range of one CTA
   p.cap_u = static_cast<int>((n + p.grid - 1) / p.grid) + 1;  // stage-1 channel range of one CTA
-  p.cap_a = static_cast<int>((L.rank + ks - 1) / ks) + 4;
-  p.a_smem_bytes = 0;
-  const size_t base = rsp::fused_smem_bytes(p, static_cast<int>(n));
-  if (base > static_cast<size_t>(dp.smem_optin))
-    return fail(RSP_E_UNSUPPORTED, "fused kernel needs %zu B shared memory (> %d)", base,
-                dp.smem_optin);
-  if (L.rank > 0 && env_int("RSP_A_SMEM", 1)) {
-    // Stage this CTA's A_r^T rows in shared memory when they fit (they do not
-    // depend on x, so the copy is issued before the kernel waits for x).
-    const int tw_max = (vrow + nt - 1) / nt;
-    const size_t want_a = static_cast<size_t>(p.cap_a) * tw_max * 16;
-    const size_t room = static_cast<size_t>(dp.smem_optin) - base - 256;
-    p.a_smem_bytes = static_cast<int>(std::min(want_a, room) / 16 * 16);
-  }
-  p.smem = rsp::fused_smem_bytes(p, static_cast<int>(n));
+  p.cap_a = static_cast<int>((L.rank + ks - 1) / ks) + 1;     // A_r^T rows of one CTA
+  p.smem = rsp::fused_smem_bytes(p, static_cast<int>(n), false);  // fp32 x: the larger footprint
+  if (p.smem > static_cast<size_t>(dp.smem_optin))
+    return fail(RSP_E_UNSUPPORTED, "fused kernel needs %zu B shared memory (> %d)", p.smem, dp.smem_optin);
   // Workspace: the barrier words and the double-buffered stage-1 sums sit at
   // fixed offsets, so layers of any shape may share one workspace (the t
   // buffers carry state from one launch to the next); per-launch scratch follows.
@@ -212,10 +217,8 @@ FusedParams fused_params(const rsp_linear* h, const void* x, rsp_dtype xdt, floa
   p.cap_w = h->plan.cap_w;
   p.cap_u = h->plan.cap_u;
   p.cap_a = h->plan.cap_a;
-  p.a_smem_bytes = h->plan.a_smem_bytes;
   p.nb_pad = h->plan.nb_pad;
   p.deterministic = h->deterministic ? 1 : 0;
-  p.x_bf16 = xdt == RSP_BF16 ? 1 : 0;
   p.dense = dense ? 1 : 0;
   return p;
 }
@@ -301,8 +304,76 @@ rsp_status launch_forward(const rsp_linear* h, const void* x, rsp_dtype xdt, flo
                 h->plan.ws_bytes);
   FusedParams p = fused_params(h, x, xdt, y, ws, dense);
   p.trace = trace;
-  cudaError_t e = rsp::launch_fused(p, h->es, h->plan.grid, h->plan.smem, stream, h->pdl);
+  cudaError_t e = rsp::launch_fused(p, h->es, xdt == RSP_BF16, h->plan.grid, h->plan.smem, stream, h->pdl);
   if (e != cudaSuccess) return fail(RSP_E_CUDA, "fused forward launch: %s", cudaGetErrorString(e));
+  return RSP_OK;
+}
+
+// Device operand [rows][ld] (first `cols` valid) -> host float, element (i, j)
+// stored at out[j * rows + i] (the reference's row-major transpose).
+rsp_status device_to_host_t(const rsp_linear* h, const void* src, size_t rows, size_t cols, size_t ld,
+                            std::vector<float>* out) {
+  out->assign(rows * cols, 0.f);
+  if (rows * cols == 0) return RSP_OK;
+  std::vector<uint8_t> buf(rows * ld * h->es);
+  RSP_CUDA(cudaMemcpy(buf.data(), src, buf.size(), cudaMemcpyDeviceToHost));
+  for (size_t i = 0; i < rows; ++i)
+    for (size_t j = 0; j < cols; ++j) {
+      const size_t idx = i * ld + j;
+      float f;
+      if (h->es == 4) {
+        std::memcpy(&f, buf.data() + idx * 4, 4);
+      } else {
+        uint16_t b;
+        std::memcpy(&b, buf.data() + idx * 2, 2);
+        const uint32_t u = static_cast<uint32_t>(b) << 16;
+        std::memcpy(&f, &u, 4);
+      }
+      (*out)[j * rows + i] = f;
+    }
+  return RSP_OK;
+}
+
+// RSPL parse (layer.cpp:269-301) over an in-memory copy of the file.
+struct RsplReader {
+  const std::string& path;
+  const std::vector<char>& buf;
+  size_t pos = 0;
+  bool take(void* dst, size_t bytes) {
+    if (buf.size() - pos < bytes) return false;
+    if (dst) std::memcpy(dst, buf.data() + pos, bytes);
+    pos += bytes;
+    return true;
+  }
+};
+
+rsp_status rspl_parse(const char* path, rsp_rspl_header* hdr, float* w, float* a, float* b, uint32_t* comps) {
+  if (!path || !hdr) return fail(RSP_E_USAGE, "null path or header");
+  const std::string p(path);
+  std::ifstream in(p, std::ios::binary);
+  if (!in) return fail(RSP_E_IO, "cannot open layer file: %s", path);
+  const std::vector<char> buf((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  RsplReader r{p, buf};
+  char magic[4];
+  if (!r.take(magic, 4) || std::memcmp(magic, "RSPL", 4) != 0)
+    return fail(RSP_E_IO, "bad magic in %s (expected RSPL)", path);
+  uint8_t version = 0;
+  if (!r.take(&version, 1)) return fail(RSP_E_IO, "truncated file: %s", path);
+  if (version != 1) return fail(RSP_E_IO, "unsupported RSPL version %u in %s", version, path);
+  uint32_t dims[4];
+  if (!r.take(dims, sizeof(dims))) return fail(RSP_E_IO, "truncated file: %s", path);
+  const uint64_t n = dims[0], m = dims[1], rk = dims[2];
+  if (!r.take(w, 4 * n * m) || !r.take(a, 4 * m * rk) || !r.take(b, 4 * rk * n) ||
+      !r.take(comps, 4 * rk))
+    return fail(RSP_E_IO, "truncated file: %s", path);
+  double plan[2];
+  if (!r.take(plan, sizeof(plan))) return fail(RSP_E_IO, "truncated file: %s", path);
+  if (static_cast<uint64_t>(plan[1]) != rk) return fail(RSP_E_IO, "inconsistent rank fields in %s", path);
+  hdr->m_in = dims[0];
+  hdr->m_out = dims[1];
+  hdr->rank = dims[2];
+  hdr->kept_width = dims[3];
+  hdr->keep_fraction = plan[0];
   return RSP_OK;
 }
 
@@ -419,11 +490,13 @@ rsp_status rsp_linear_create(const rsp_linear_desc* d, rsp_linear** out) {
   }
   // The attribute is per kernel, not per launch: raise it to the opt-in
   // maximum once so every handle's plan fits regardless of creation order.
-  e = rsp::fused_set_smem(h->es, static_cast<size_t>(dp.smem_optin));
+  e = rsp::fused_set_smem(static_cast<size_t>(dp.smem_optin));
   if (e != cudaSuccess) {
     free_linear(h);
     return fail(RSP_E_CUDA, "cudaFuncSetAttribute(smem=%zu): %s", h->plan.smem, cudaGetErrorString(e));
   }
+  h->comps.resize(h->rank);
+  for (uint32_t c = 0; c < h->rank; ++c) h->comps[c] = c;
   *out = h;
   return RSP_OK;
 }
@@ -558,6 +631,75 @@ rsp_status rsp_gather_matvec(const rsp_linear* h, const void* x, rsp_dtype xdt, 
   RSP_CUDA(cudaStreamSynchronize(s));  // k32 must outlive the async copy
   if (e != cudaSuccess) return fail(RSP_E_CUDA, "gather launch: %s", cudaGetErrorString(e));
   if (touched_bytes) *touched_bytes += static_cast<uint64_t>(nkept) * h->m_out * 4u;  // layer.cpp:91
+  return RSP_OK;
+}
+
+rsp_status rsp_rspl_read(const char* path, rsp_rspl_header* hdr, float* w_cols, float* a_r, float* b_r,
+                         uint32_t* comps) {
+  return rspl_parse(path, hdr, w_cols, a_r, b_r, comps);
+}
+
+rsp_status rsp_linear_load_rspl(const char* path, const rsp_linear_desc* opts, rsp_linear** out) {
+  if (!out) return fail(RSP_E_USAGE, "null output");
+  *out = nullptr;
+  rsp_rspl_header hd;
+  if (rsp_status st = rspl_parse(path, &hd, nullptr, nullptr, nullptr, nullptr)) return st;
+  std::vector<float> w(static_cast<size_t>(hd.m_in) * hd.m_out), a(static_cast<size_t>(hd.m_out) * hd.rank),
+      b(static_cast<size_t>(hd.rank) * hd.m_in);
+  std::vector<uint32_t> comps(hd.rank);
+  if (rsp_status st = rspl_parse(path, &hd, w.data(), a.data(), b.data(), comps.data())) return st;
+  rsp_linear_desc d = {};
+  if (opts) d = *opts;
+  else d.weight_dtype = RSP_F32;
+  if (!opts) d.k_override = -1;
+  d.m_in = hd.m_in;
+  d.m_out = hd.m_out;
+  d.rank = hd.rank;
+  d.keep_fraction = hd.keep_fraction;
+  d.src_dtype = RSP_F32;
+  d.src_memory = RSP_MEM_HOST;
+  d.w_layout = RSP_W_COL_MAJOR;
+  d.w = w.data();
+  d.a_r = hd.rank ? a.data() : nullptr;
+  d.b_r = hd.rank ? b.data() : nullptr;
+  if (rsp_status st = rsp_linear_create(&d, out)) return st;
+  (*out)->comps = comps;
+  return RSP_OK;
+}
+
+rsp_status rsp_linear_save_rspl(const rsp_linear* h, const char* path) {
+  if (!h || !path) return fail(RSP_E_USAGE, "null handle or path");
+  if (h->m != h->m_out) return fail(RSP_E_USAGE, "save_rspl: handle is a row shard (%u of %u rows)", h->m, h->m_out);
+  DeviceGuard g(h->device);
+  std::vector<float> w, a, b;
+  // Wt[n][m_pad] -> w_cols data[j*m+i]: row j of Wt is column j of W
+  if (rsp_status st = device_to_host_t(h, h->Wt, h->m_in, h->m, h->m_pad, &w)) return st;
+  std::vector<float> wc(w.size());
+  for (size_t j = 0; j < h->m_in; ++j)
+    for (size_t i = 0; i < h->m; ++i) wc[j * h->m + i] = w[i * h->m_in + j];
+  if (rsp_status st = device_to_host_t(h, h->At, h->rank, h->m, h->m_pad, &a)) return st;  // -> m x r
+  if (rsp_status st = device_to_host_t(h, h->Bt, h->m_in, h->rank, h->r_pad, &b)) return st;  // -> r x n
+  std::ofstream f(path, std::ios::binary);
+  if (!f) return fail(RSP_E_IO, "cannot open layer file for writing: %s", path);
+  const uint8_t version = 1;
+  const uint32_t dims[4] = {h->m_in, h->m_out, h->rank,
+                            static_cast<uint32_t>(std::ceil(h->keep_fraction * static_cast<double>(h->m_in)))};
+  const double plan[2] = {h->keep_fraction, static_cast<double>(h->rank)};
+  f.write("RSPL", 4);
+  f.write(reinterpret_cast<const char*>(&version), 1);
+  f.write(reinterpret_cast<const char*>(dims), sizeof(dims));
+  f.write(reinterpret_cast<const char*>(wc.data()), static_cast<std::streamsize>(wc.size() * 4));
+  f.write(reinterpret_cast<const char*>(a.data()), static_cast<std::streamsize>(a.size() * 4));
+  f.write(reinterpret_cast<const char*>(b.data()), static_cast<std::streamsize>(b.size() * 4));
+  f.write(reinterpret_cast<const char*>(h->comps.data()), static_cast<std::streamsize>(h->comps.size() * 4));
+  f.write(reinterpret_cast<const char*>(plan), sizeof(plan));
+  if (!f) return fail(RSP_E_IO, "write failed: %s", path);
+  return RSP_OK;
+}
+
+rsp_status rsp_linear_components(const rsp_linear* h, uint32_t* comps) {
+  if (!h || (h->rank && !comps)) return fail(RSP_E_USAGE, "null handle or buffer");
+  std::copy(h->comps.begin(), h->comps.end(), comps);
   return RSP_OK;
 }
 

@@ -300,4 +300,36 @@ struct Vec<float> {
   }
 };
 
+
+// ---------------------------------------------------------------------------
+// v3 streaming helpers
+// ---------------------------------------------------------------------------
+// L2 prefetch that survives the streaming traffic: operands that do not
+// depend on x (A_r^T, B_r^T rows) are pulled into L2 while the previous
+// linear still runs (under PDL) and read back from L2 later.
+__device__ __forceinline__ void prefetch_l2_keep(const void* p) {
+  asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
+}
+
+// Streamed-once weights: no L1 allocation, first in line for L2 eviction.
+__device__ __forceinline__ uint4 ldg_stream_ef(const void* p, uint64_t pol) {
+  uint4 u;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w)
+               : "l"(p), "l"(pol));
+  return u;
+}
+
+// Vector float reduction into global memory (sm_90+): no return value,
+// performed at L2.  p must be 16-byte aligned.
+__device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+__device__ __forceinline__ void red_add_f32(float* p, float a) {
+  asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(a) : "memory");
+}
+
+__device__ __forceinline__ float ldcg_f32(const float* p) { return __ldcg(p); }
+
 }  // namespace rsp

@@ -19,40 +19,38 @@ struct FusedParams {
   const void* Bt;  // [n][r_pad]  B_r^T (row j = column j of b_r)
   const void* x;   // [n] fp32 or bf16
   float* y;        // [m] fp32
-  float* t_part;   // [r_pad][nb_pad] stage-1 partial sums (column b = CTA b; deterministic mode)
-  float* t_acc;    // [2][kTAccCap] stage-1 sums by float atomics (fast mode; buffer = barrier gen & 1)
-  float* y_part;   // [k_splits][m_pad] split-K partial sums
+  float* t_acc;    // [2][kTAccCap] stage-1 sums (fast mode; buffer = barrier generation & 1)
+  float* t_part;   // [r_pad][nb_pad] stage-1 partial sums, column b = CTA b (deterministic mode)
+  float* y_part;   // [k_splits][m_pad] split-K partial sums (deterministic mode)
   unsigned* bars;  // [2] grid barrier {count, gen} + [col_tiles] tile tickets
   int n, m, m_pad, r, r_pad, k;
   int col_tiles, k_splits;
-  int cap_w, cap_u, cap_a;  // per-CTA list capacities
-  int a_smem_bytes;         // shared-memory staging for this CTA's A_r^T rows
-  int nb_pad;               // row stride of t_part ([r_pad][nb_pad], grid rounded up to 4)
-  int deterministic;        // 1: fixed-order split-K combine (bit-reproducible y)
-  int x_bf16;
-  int dense;  // 1: all n channels through W, no selection, no low-rank term
-  int pdl;    // 1: launched with programmatic dependent launch
-  long long* trace;  // debug: [grid][16] phase timestamps (null in production)
+  int cap_w, cap_u, cap_a;  // per-CTA list capacities (W rows, stage-1 rows, A rows)
+  int nb_pad;               // row stride of t_part (grid rounded up to 4)
+  int deterministic;        // 1: fixed-order combines (bit-reproducible y)
+  int dense;                // 1: all n channels through W, no selection, no low-rank term
+  int pdl;                  // 1: launched with programmatic dependent launch
+  long long* trace;         // debug: [grid][16] phase timestamps (null in production)
 };
 
 struct LaunchPlan {
   int col_tiles = 1, k_splits = 1, grid = 1;
   int cap_w = 1, cap_u = 1, cap_a = 1;
-  int a_smem_bytes = 0, nb_pad = 4;
+  int nb_pad = 4;
   size_t smem = 0;
-  size_t ws_bytes = 0;  // workspace: barriers + t_part + y_part
-  size_t ws_t_off = 0, ws_acc_off = 0, ws_y_off = 0;
+  size_t ws_bytes = 0;  // workspace: barriers + t buffers + partials
+  size_t ws_acc_off = 0, ws_t_off = 0, ws_y_off = 0;
 };
 
 // Shared-memory bytes the fused kernel needs for a plan.
-size_t fused_smem_bytes(const LaunchPlan& p, int n);
+size_t fused_smem_bytes(const LaunchPlan& p, int n, bool x_bf16);
 
-cudaError_t fused_set_smem(int elem_bytes, size_t smem);
-cudaError_t launch_fused(const FusedParams& p, int elem_bytes, int grid, size_t smem,
+cudaError_t fused_set_smem(size_t smem);
+cudaError_t launch_fused(const FusedParams& p, int elem_bytes, bool x_bf16, int grid, size_t smem,
                          cudaStream_t stream, bool pdl);
 
 // Stand-alone selector: one CTA.  Any of kept/rest/sparse may be null.
-size_t select_smem_bytes(int n);
+size_t select_smem_bytes(int n, bool x_bf16);
 cudaError_t launch_select(const void* x, bool x_bf16, int n, int k, int32_t* kept, int32_t* rest,
                           float* sparse_x, cudaStream_t stream);
 

@@ -146,16 +146,49 @@ class DecomposedLayer:
         if torch is not None and wmem == L.RSP_MEM_DEVICE:
             torch.cuda.synchronize(device)
         check(L.lib().rsp_linear_create(ct.byref(d), ct.byref(h)), "rsp_linear_create")
+        self._adopt(h, device, weight_dtype)
+
+    def _adopt(self, h, device: int, weight_dtype: str) -> None:
         self._h = h
         self.device = device
         self.weight_dtype = weight_dtype
-        self.m_in, self.m_out = m_in, m_out
         info = L.LinearInfo()
         check(L.lib().rsp_linear_info_get(self._h, ct.byref(info)))
         self.info = {f: getattr(info, f) for f, _ in L.LinearInfo._fields_}
+        self.m_in, self.m_out = info.m_in, info.m_out
         self.k = info.k
         self.row_begin, self.row_end = info.row_begin, info.row_end
         self._ws = None
+
+    # -- RSPL files (layer.cpp:243-301) ---------------------------------------
+    @classmethod
+    def load_rspl(cls, path: str, *, weight_dtype: str = "f32", k: Optional[int] = None,
+                  device: int = 0, shard_rank: int = 0, shard_count: int = 1,
+                  deterministic: bool = False) -> "DecomposedLayer":
+        """read_decomposed_layer (layer.hpp:95) straight into HBM."""
+        hdr = read_rspl_header(path)
+        d = L.LinearDesc()
+        d.k_override = -1 if k is None else int(k)
+        d.weight_dtype = {"bf16": L.RSP_BF16, "f32": L.RSP_F32, "fp32": L.RSP_F32}[weight_dtype]
+        d.device, d.shard_rank, d.shard_count = device, shard_rank, shard_count
+        d.flags = L.RSP_FLAG_DETERMINISTIC if deterministic else 0
+        h = ct.c_void_p()
+        check(L.lib().rsp_linear_load_rspl(path.encode(), ct.byref(d), ct.byref(h)), "rsp_linear_load_rspl")
+        self = cls.__new__(cls)
+        self.plan = SparsityPlan(hdr["keep_fraction"], hdr["rank"])
+        self._adopt(h, device, weight_dtype)
+        return self
+
+    def save_rspl(self, path: str) -> None:
+        """write_decomposed_layer (layer.hpp:93) of the device-resident values."""
+        check(L.lib().rsp_linear_save_rspl(self._h, path.encode()), "rsp_linear_save_rspl")
+
+    @property
+    def selected_components(self) -> List[int]:
+        r = int(self.plan.rank)
+        buf = (ct.c_uint32 * max(r, 1))()
+        check(L.lib().rsp_linear_components(self._h, buf), "rsp_linear_components")
+        return list(buf)[:r]
 
     # -- plumbing ------------------------------------------------------------
     @property
@@ -258,6 +291,37 @@ class DecomposedLayer:
                 check(L.lib().rsp_linear_export(self._h, which, a.ctypes.data_as(ct.POINTER(ct.c_double))))
             outs.append(a)
         return tuple(outs)
+
+
+def read_rspl_header(path: str) -> dict:
+    """RSPL header fields (host-only parse; RSP_E_IO -> IoError like io_error)."""
+    h = L.RsplHeader()
+    check(L.lib().rsp_rspl_read(path.encode(), ct.byref(h), None, None, None, None), "rsp_rspl_read")
+    return {f: getattr(h, f) for f, _ in L.RsplHeader._fields_}
+
+
+def read_rspl(path: str) -> dict:
+    """Host-only read of a whole RSPL file (read_decomposed_layer's fields as
+    float32 arrays: w_cols (m_in, m_out), a_r (m_out, r), b_r (r, m_in), comps)."""
+    hdr = read_rspl_header(path)
+    n, m, r = hdr["m_in"], hdr["m_out"], hdr["rank"]
+    w = np.empty((n, m), np.float32)
+    a = np.empty((m, r), np.float32)
+    b = np.empty((r, n), np.float32)
+    c = np.empty(max(r, 1), np.uint32)
+    check(L.lib().rsp_rspl_read(path.encode(), ct.byref(L.RsplHeader()), w.ctypes.data, a.ctypes.data,
+                                b.ctypes.data, c.ctypes.data), "rsp_rspl_read")
+    return dict(hdr, w_cols=w, a_r=a, b_r=b, comps=c[:r])
+
+
+def read_decomposed_layer(path: str, **kw) -> DecomposedLayer:
+    """rsparse::read_decomposed_layer (layer.hpp:95), device-resident."""
+    return DecomposedLayer.load_rspl(path, **kw)
+
+
+def write_decomposed_layer(layer: DecomposedLayer, path: str) -> None:
+    """rsparse::write_decomposed_layer (layer.hpp:93)."""
+    layer.save_rspl(path)
 
 
 def forward(layer: DecomposedLayer, x, **kw):

@@ -18,10 +18,8 @@ import paper_2504_19449_b200 as rsp  # noqa: E402
 from paper_2504_19449_b200 import _lib as L  # noqa: E402
 from paper_2504_19449_b200 import workloads as wl  # noqa: E402
 
-EV = {1: "after_griddep", 2: "x_loaded+hist", 14: "boundary_bin", 3: "gathered", 15: "W_list",
-      4: "lists+prefetch",
-      13: "resolver_done", 5: "S1_rows_done", 6: "grid_arrived", 7: "grid_wait_done", 8: "coefs_done",
-      9: "W_rows_done", 10: "A_rows_done", 11: "y_written", 12: "end"}
+EV = {1: "after_griddep", 2: "x_loaded+hist", 3: "cut", 4: "lists", 5: "stage1+arrive",
+      6: "W_rows_done", 7: "barrier_waited", 8: "A_rows_done", 9: "end"}
 SHAPES = {"q": (4096, 4096), "gate": (11008, 4096), "down": (4096, 11008)}
 
 
