@@ -116,22 +116,25 @@ class ClockSampler:
 
 # --------------------------------------------------------------------------- workload
 def build_stack(rsp, wl, plans, rank, world, dev, torch):
-    """Create every linear's shard on the device from synthetic weights."""
+    """Create every linear's shard on the device from synthetic weights, and
+    one synthetic activation per input group (q/k/v share one, gate/up share
+    one: workloads.input_groups)."""
     rng = np.random.default_rng(1234)
     gen = torch.Generator(device=dev)
     gen.manual_seed(4321)
+    gid, wait = wl.input_groups(plans)
     layers, xs_host = [], []
-    for (name, m, n, s, r) in plans:
+    for i, (name, m, n, s, r) in enumerate(plans):
         w = torch.randn(m, n, device=dev, dtype=torch.bfloat16, generator=gen) * 0.02
         a = torch.randn(m, r, device=dev, dtype=torch.bfloat16, generator=gen) * 0.05
         b = torch.randn(r, n, device=dev, dtype=torch.bfloat16, generator=gen) * 0.05
         layers.append(rsp.DecomposedLayer(w, a, b, rsp.SparsityPlan(s, r), weight_dtype="bf16",
                                           device=dev.index, shard_rank=rank, shard_count=world))
         del w, a, b
-        x = wl.silu_gate_x(n, rng) if name.endswith("down_proj") else wl.heavy_tailed_x(n, rng)
-        xs_host.append(x)
+        if wait[i]:
+            xs_host.append(wl.silu_gate_x(n, rng) if name.endswith("down_proj") else wl.heavy_tailed_x(n, rng))
     torch.cuda.synchronize()
-    return layers, xs_host
+    return layers, xs_host, gid, wait
 
 
 def kernel_bytes(layers):
@@ -249,14 +252,15 @@ def run_ours(args):
     rsp.lib()
 
     plans = wl.config2_plans(n_layers=args.layers)
-    layers, xs_host = build_stack(rsp, wl, plans, rank, world, dev, torch)
+    layers, xs_host, gid, wait = build_stack(rsp, wl, plans, rank, world, dev, torch)
 
     # activations: one contiguous bf16 buffer (device + pinned host) for the e2e copy
     offs = np.cumsum([0] + [x.size for x in xs_host])
     x_host = torch.empty(int(offs[-1]), dtype=torch.bfloat16).pin_memory()
     x_host.copy_(torch.from_numpy(np.concatenate(xs_host)).to(torch.bfloat16))
     x_dev = x_host.to(dev)
-    xs = [x_dev[offs[i]:offs[i + 1]] for i in range(len(layers))]
+    xg = [x_dev[offs[g]:offs[g + 1]] for g in range(len(xs_host))]
+    xs = [xg[gid[i]] for i in range(len(layers))]
     mloc = [l.row_end - l.row_begin for l in layers]
     mfull = [l.m_out for l in layers]
     yoffs = np.cumsum([0] + (mfull if world > 1 else mloc))
@@ -266,7 +270,8 @@ def run_ours(args):
     stream = torch.cuda.Stream(device=dev)
 
     if world == 1:
-        st = rsp.Stack(layers, xs, ys)
+        # one persistent launch per token; q/k/v and gate/up overlap (shared input)
+        st = rsp.Stack(layers, xs, ys, wait_prev=wait)
         launch = lambda: st.launch(stream)  # noqa: E731
     else:
         # row-sharded linears, each followed by one in-place NCCL all-gather
@@ -314,7 +319,7 @@ def run_ours(args):
 
     extras = {}
     if not args.no_dense and not args.profile and world == 1:
-        extras.update(dense_baselines(torch, rsp, layers, xs, ys, stream, args, plans, dev))
+        extras.update(dense_baselines(torch, rsp, layers, xs, ys, stream, args, plans, dev, gid, wait))
 
     out = {
         "metric": METRIC, "value": us_token, "unit": "us/token", "n_gpus": world,
@@ -361,35 +366,41 @@ def load_traffic():
     return None
 
 
-def dense_baselines(torch, rsp, layers, xs, ys, stream, args, plans, dev):
+def dense_baselines(torch, rsp, layers, xs, ys, stream, args, plans, dev, gid, wait):
     """Dense bf16 GEMV stacks of the same layers under the same protocol:
-    (1) the in-house streaming kernel over all m_in channels, (2) cuBLAS
-    (torch.nn.functional.linear on row-major bf16 W, graph-captured)."""
-    import torch.nn.functional as F
+    (1) the in-house kernel over all m_in channels (same persistent stack,
+    same overlap of shared-input linears), (2) cuBLAS (torch.matmul on
+    row-major bf16 W, graph-captured) with the shared-input linears of a layer
+    concatenated into one GEMV (fused QKV and gate/up, as production decode
+    does), which is the strongest dense baseline."""
     res = {}
-    st = rsp.Stack(layers, xs, ys, dense=True)
+    st = rsp.Stack(layers, xs, ys, dense=True, wait_prev=wait)
     with torch.cuda.stream(stream):
         tot, _ = time_graph(torch, lambda: st.launch(stream), args.steps, args.warmup, stream)
     res["dense_inhouse_us_per_token"] = tot / args.steps * 1e3
     st.close()
-    # cuBLAS: row-major W (m x n) bf16, y = W x
     gen = torch.Generator(device=dev)
     gen.manual_seed(7)
-    Ws = [torch.randn(m, n, device=dev, dtype=torch.bfloat16, generator=gen) * 0.02 for (_, m, n, _, _) in plans]
-    outs = [torch.empty(m, device=dev, dtype=torch.bfloat16) for (_, m, _, _, _) in plans]
+    groups = []
+    for g in range(max(gid) + 1):
+        idx = [i for i in range(len(plans)) if gid[i] == g]
+        m = sum(plans[i][1] for i in idx)
+        n = plans[idx[0]][2]
+        groups.append((torch.randn(m, n, device=dev, dtype=torch.bfloat16, generator=gen) * 0.02,
+                       xs[idx[0]], torch.empty(m, device=dev, dtype=torch.bfloat16)))
     g = torch.cuda.CUDAGraph()
     with torch.cuda.stream(stream):
-        for W, x, o in zip(Ws, xs, outs):
+        for W, x, o in groups:
             torch.matmul(W, x, out=o)
         torch.cuda.synchronize()
         with torch.cuda.graph(g, stream=stream):
-            for W, x, o in zip(Ws, xs, outs):
+            for W, x, o in groups:
                 torch.matmul(W, x, out=o)
         tot, _ = time_graph(torch, lambda: g.replay(), args.steps, args.warmup, stream)
     res["dense_cublas_us_per_token"] = tot / args.steps * 1e3
     dense_bytes = sum(2 * m * n for (_, m, n, _, _) in plans)
     res["dense_cublas_GBps"] = dense_bytes / (tot / args.steps * 1e-3) / 1e9
-    del Ws, outs, g
+    del groups, g
     torch.cuda.empty_cache()
     return res
 

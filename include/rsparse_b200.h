@@ -224,12 +224,21 @@ rsp_status rsp_threshold_sparsify(const void* x_dev, rsp_dtype x_dtype, uint32_t
                                   uint32_t* k_out, void* stream);
 
 /* -- stack executor ----------------------------------------------------------- */
-/* A sequence of forwards captured once into a CUDA graph (decode: linear
- * i+1 runs after linear i).  x_devs[i] / y_devs[i] are bound at creation. */
+/* A decode-order sequence of forwards run by ONE persistent kernel launch
+ * (captured into a CUDA graph): the instruction working set stays hot across
+ * linears and each linear's x-independent operands are prefetched while the
+ * previous one drains.  x_devs[i] / y_devs[i] are bound at creation.  By
+ * default linear i+1 starts only after linear i's output is complete (its x
+ * may be y_i); rsp_stack_create_ex takes wait_prev[i] = 0 for linears that
+ * share the previous linear's input (q/k/v, gate/up), which may then overlap.
+ * Layers must share device, weight dtype and the deterministic flag. */
 typedef struct rsp_stack rsp_stack;
 rsp_status rsp_stack_create(const rsp_linear* const* layers, uint32_t count,
                             const void* const* x_devs, rsp_dtype x_dtype, float* const* y_devs,
                             int dense, rsp_stack** out);
+rsp_status rsp_stack_create_ex(const rsp_linear* const* layers, uint32_t count,
+                               const void* const* x_devs, rsp_dtype x_dtype, float* const* y_devs,
+                               int dense, const uint8_t* wait_prev, rsp_stack** out);
 rsp_status rsp_stack_launch(rsp_stack* s, void* stream);
 void rsp_stack_destroy(rsp_stack* s);
 
@@ -240,6 +249,12 @@ void rsp_stack_destroy(rsp_stack* s);
 rsp_status rsp_debug_forward_trace(const rsp_linear* h, const void* x_dev, rsp_dtype x_dtype,
                                    float* y_dev, void* workspace, size_t workspace_bytes,
                                    int64_t* trace_dev, int dense, void* stream);
+
+/* One launch of the stack that records, per (linear l, CTA b), 16 int64 at
+ * trace_dev[(l * grid + b) * 16]: [0] %globaltimer at the linear's start,
+ * [13] after its dependency wait, [14] at its end, [1..12] %clock64 phase
+ * stamps relative to the CTA's start of the linear.  *grid_out = grid. */
+rsp_status rsp_debug_stack_trace(rsp_stack* s, int64_t* trace_dev, uint32_t* grid_out, void* stream);
 
 /* -- device helpers ------------------------------------------------------------- */
 int rsp_device_sm_count(int device);

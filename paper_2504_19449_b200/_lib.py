@@ -22,9 +22,9 @@ EXPORTS = [
     "rsp_linear_workspace_size", "rsp_workspace_init", "rsp_linear_forward",
     "rsp_linear_forward_host", "rsp_linear_dense_forward", "rsp_gather_matvec",
     "rsp_linear_selected", "rsp_linear_io_cost", "rsp_linear_export",
-    "rsp_top_k_by_magnitude", "rsp_threshold_sparsify", "rsp_stack_create",
+    "rsp_top_k_by_magnitude", "rsp_threshold_sparsify", "rsp_stack_create", "rsp_stack_create_ex",
     "rsp_stack_launch", "rsp_stack_destroy", "rsp_device_sm_count", "rsp_debug_forward_trace",
-    "rsp_rspl_read", "rsp_linear_load_rspl", "rsp_linear_save_rspl", "rsp_linear_components",
+    "rsp_debug_stack_trace", "rsp_rspl_read", "rsp_linear_load_rspl", "rsp_linear_save_rspl", "rsp_linear_components",
 ]
 
 
@@ -127,10 +127,13 @@ def lib() -> ct.CDLL:
                                               ct.POINTER(u32), vp]),
         "rsp_stack_create": (ct.c_int, [ct.POINTER(vp), u32, ct.POINTER(vp), ct.c_int,
                                         ct.POINTER(vp), ct.c_int, ct.POINTER(vp)]),
+        "rsp_stack_create_ex": (ct.c_int, [ct.POINTER(vp), u32, ct.POINTER(vp), ct.c_int,
+                                           ct.POINTER(vp), ct.c_int, ct.POINTER(ct.c_uint8), ct.POINTER(vp)]),
         "rsp_stack_launch": (ct.c_int, [vp, vp]),
         "rsp_stack_destroy": (None, [vp]),
         "rsp_device_sm_count": (ct.c_int, [ct.c_int]),
         "rsp_debug_forward_trace": (ct.c_int, [vp, vp, ct.c_int, vp, vp, ct.c_size_t, vp, ct.c_int, vp]),
+        "rsp_debug_stack_trace": (ct.c_int, [vp, vp, ct.POINTER(u32), vp]),
         "rsp_rspl_read": (ct.c_int, [ct.c_char_p, ct.POINTER(RsplHeader), vp, vp, vp, vp]),
         "rsp_linear_load_rspl": (ct.c_int, [ct.c_char_p, ct.POINTER(LinearDesc), ct.POINTER(vp)]),
         "rsp_linear_save_rspl": (ct.c_int, [vp, ct.c_char_p]),

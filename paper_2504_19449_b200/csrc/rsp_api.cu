@@ -23,8 +23,9 @@
 #include "../../include/rsparse_b200.h"
 #include "rsp_internal.h"
 
-using rsp::FusedParams;
-using rsp::LaunchPlan;
+using rsp::LinDesc;
+using rsp::StackParams;
+using rsp::WsLayout;
 
 namespace {
 
@@ -100,6 +101,17 @@ uint32_t keep_count(double s, uint32_t n) {
   return static_cast<uint32_t>(std::ceil(s * static_cast<double>(n)));
 }
 
+// How one linear is decomposed over the GPU (see make_plan).
+struct LaunchPlan {
+  int col_tiles = 1, k_splits = 1, grid = 1;
+  int cap_w = 1, cap_u = 1, cap_a = 1;
+  int nb_pad = 4;
+  int need_a = 0, need_b = 0;    // bytes of one CTA's A_r^T tile rows / B_r^T slice
+  int abuf = 0, bbuf = 0;        // shared-memory operand buffers of a single-linear launch
+  size_t smem = 0;
+  size_t ws_bytes = 0;  // single-linear workspace
+};
+
 }  // namespace
 
 struct rsp_linear {
@@ -131,9 +143,29 @@ struct rsp_stack {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   void* ws = nullptr;
+  LinDesc* descs = nullptr;  // device array
+  StackParams params = {};   // the captured launch (re-launched by the debug trace)
+  int es = 2, grid = 1;
+  bool x_bf16 = false;
+  size_t smem = 0;
 };
 
 namespace {
+
+// Split the shared memory left over by the kernel's fixed carve-up between
+// the operand buffers: the B_r^T slice is used all-or-nothing (it precedes
+// the grid barrier), the A_r^T tile takes what remains.  Opt-in (env
+// RSP_SMEM_OPS=1): measured on the config-2 stack it speeds up stage 1 and
+// stage 2 but the bulk copies compete with the critical W stream, and the
+// stack is 3-4% faster without them.
+void operand_buffers(int avail, int need_a, int need_b, int* abuf, int* bbuf) {
+  // one buffer (abuf) holds a linear's B_r^T slice then its A_r^T rows; the
+  // kernel splits it per linear (operand_split)
+  avail = std::max(0, avail - 1024);
+  *abuf = *bbuf = 0;
+  if (!env_int("RSP_SMEM_OPS", 0)) return;
+  *abuf = std::min(need_a + need_b + 16, avail) / 16 * 16;
+}
 
 // Decompose one forward over the GPU: col_tiles column tiles x k_splits
 // channel splits, at most one CTA per SM (a second slot per SM is left for
@@ -141,20 +173,21 @@ namespace {
 // columns of a row (C2 in {1,2,4,8,16}); per-CTA time ~ k*C2/(16*k_splits),
 // and the split-K combine costs k_splits*m float reductions, so the cheapest
 // C2/k_splits wins with k_splits <= 32.
-rsp_status make_plan(const rsp_linear& L, const DevProps& dp, LaunchPlan* out) {
+rsp_status make_plan(const rsp_linear& L, const DevProps& dp, LaunchPlan* out, int budget = 0) {
   LaunchPlan p;
   const uint32_t n = L.m_in;
   const int vrow = static_cast<int>(L.m_pad * L.es / 16);  // 16-B units per W^T row
   const int wcols = (vrow + 31) / 32;                       // 512-B warp columns per row
-  if (L.r_pad > rsp::kTAccCap)
-    return fail(RSP_E_UNSUPPORTED, "rank %u too large (r_pad <= %u)", L.rank, rsp::kTAccCap);
-  const int sms = std::max(1, dp.sms);
+  if (L.r_pad > rsp::kTAccCap || L.r_pad * L.es > 4096u)
+    return fail(RSP_E_UNSUPPORTED, "rank %u too large (B_r^T rows limited to 4 KB, r_pad <= %u)", L.rank,
+                rsp::kTAccCap);
+  const int sms = std::max(1, budget > 0 ? std::min(budget, dp.sms) : dp.sms);  // CTAs this linear may use
   const int ks_cap = std::max(1, env_int("RSP_MAX_KSPLITS", 32));
   int best_nt = 1, best_ks = 1;
   double best = 1e30;
-  for (int c2 = 1; c2 <= 16; c2 *= 2) {
+  for (int c2 = 1; c2 <= 8; c2 *= 2) {  // <= one row of warps (kThreads / 32 = 8)
     const int nt = (wcols + c2 - 1) / c2;
-    if (nt > sms) continue;
+    if (nt > sms || nt > static_cast<int>(rsp::kMaxTickets)) continue;
     const int ks = std::min(sms / nt, ks_cap);
     const double cost = static_cast<double>(c2) / ks;
     if (cost < best * 0.99 || (cost <= best * 1.01 && ks <= 24)) {
@@ -171,6 +204,7 @@ rsp_status make_plan(const rsp_linear& L, const DevProps& dp, LaunchPlan* out) {
   ks = std::min(ks, std::max(1, (want + nt - 1) / nt));
   ks = std::min(ks, static_cast<int>(std::max(1u, n)));
   if (const int force = env_int("RSP_KSPLITS", 0)) ks = std::max(1, std::min(force, sms / nt));
+  ks = std::max(1, std::min(ks, sms / nt));
   p.col_tiles = nt;
   p.k_splits = ks;
   p.grid = nt * ks;
@@ -178,49 +212,53 @@ rsp_status make_plan(const rsp_linear& L, const DevProps& dp, LaunchPlan* out) {
   p.cap_w = static_cast<int>((n + ks - 1) / ks) + 1;          // W channel range of one CTA
   p.cap_u = static_cast<int>((n + p.grid - 1) / p.grid) + 1;  // stage-1 channel range of one CTA
   p.cap_a = static_cast<int>((L.rank + ks - 1) / ks) + 1;     // A_r^T rows of one CTA
-  p.smem = rsp::fused_smem_bytes(p, static_cast<int>(n), false);  // fp32 x: the larger footprint
-  if (p.smem > static_cast<size_t>(dp.smem_optin))
-    return fail(RSP_E_UNSUPPORTED, "fused kernel needs %zu B shared memory (> %d)", p.smem, dp.smem_optin);
-  // Workspace: the barrier words and the double-buffered stage-1 sums sit at
-  // fixed offsets, so layers of any shape may share one workspace (the t
-  // buffers carry state from one launch to the next); per-launch scratch follows.
-  static_assert(4 * (2 + 148) <= rsp::kWsBarBytes, "barrier region");
-  p.ws_acc_off = rsp::kWsBarBytes;
-  p.ws_t_off = p.ws_acc_off + 2u * 4u * rsp::kTAccCap;
-  p.ws_y_off = p.ws_t_off + round_up(4u * static_cast<uint32_t>(p.nb_pad) * std::max(L.r_pad, 8u), 256u);
-  p.ws_bytes = p.ws_y_off + static_cast<size_t>(4) * ks * L.m_pad;
+  {
+    const int wmax = 32 * ((wcols + nt - 1) / nt);  // widest tile, 16-B units
+    const bool lr = L.rank > 0 && L.k < n;
+    p.need_a = lr ? p.cap_a * std::min(wmax, vrow) * 16 : 0;
+    p.need_b = lr ? (p.cap_u - 1) * static_cast<int>(L.r_pad * L.es) : 0;
+  }
+  const size_t base = rsp::stack_smem_bytes(static_cast<int>(n), false, p.cap_w, p.cap_u, p.cap_a);  // fp32 x
+  if (base > static_cast<size_t>(dp.smem_optin))
+    return fail(RSP_E_UNSUPPORTED, "fused kernel needs %zu B shared memory (> %d)", base, dp.smem_optin);
+  operand_buffers(static_cast<int>(dp.smem_optin - base), p.need_a, p.need_b, &p.abuf, &p.bbuf);
+  p.smem = rsp::stack_smem_bytes(static_cast<int>(n), false, p.cap_w, p.cap_u, p.cap_a, p.abuf, p.bbuf);
+  p.ws_bytes = WsLayout::make(1, p.nb_pad, static_cast<int>(L.r_pad), ks, static_cast<int>(L.m_pad)).bytes;
   *out = p;
   return RSP_OK;
 }
 
-FusedParams fused_params(const rsp_linear* h, const void* x, rsp_dtype xdt, float* y, void* ws,
-                         bool dense) {
-  FusedParams p = {};
-  p.Wt = h->Wt;
-  p.At = h->At;
-  p.Bt = h->Bt;
-  p.x = x;
-  p.y = y;
-  uint8_t* w = static_cast<uint8_t*>(ws);
-  p.bars = reinterpret_cast<unsigned*>(w);
-  p.t_part = reinterpret_cast<float*>(w + h->plan.ws_t_off);
-  p.t_acc = reinterpret_cast<float*>(w + h->plan.ws_acc_off);
-  p.y_part = reinterpret_cast<float*>(w + h->plan.ws_y_off);
-  p.n = static_cast<int>(h->m_in);
-  p.m = static_cast<int>(h->m);
-  p.m_pad = static_cast<int>(h->m_pad);
-  p.r = static_cast<int>(h->rank);
-  p.r_pad = static_cast<int>(h->r_pad);
-  p.k = dense ? static_cast<int>(h->m_in) : static_cast<int>(h->k);
-  p.col_tiles = h->plan.col_tiles;
-  p.k_splits = h->plan.k_splits;
-  p.cap_w = h->plan.cap_w;
-  p.cap_u = h->plan.cap_u;
-  p.cap_a = h->plan.cap_a;
-  p.nb_pad = h->plan.nb_pad;
-  p.deterministic = h->deterministic ? 1 : 0;
-  p.dense = dense ? 1 : 0;
-  return p;
+LinDesc lin_desc(const rsp_linear* h, const void* x, float* y, bool dense, int slot, int flags,
+                 const LaunchPlan* plan = nullptr, int cta0 = 0) {
+  const LaunchPlan& pl = plan ? *plan : h->plan;
+  LinDesc d = {};
+  d.Wt = h->Wt;
+  d.At = h->At;
+  d.Bt = h->Bt;
+  d.x = x;
+  d.y = y;
+  d.n = static_cast<int>(h->m_in);
+  d.m = static_cast<int>(h->m);
+  d.m_pad = static_cast<int>(h->m_pad);
+  d.r = static_cast<int>(h->rank);
+  d.r_pad = static_cast<int>(h->r_pad);
+  d.k = dense ? static_cast<int>(h->m_in) : static_cast<int>(h->k);
+  d.col_tiles = pl.col_tiles;
+  d.k_splits = pl.k_splits;
+  d.grid = pl.grid;
+  d.flags = flags | (dense ? rsp::kLinDense : 0);
+  d.slot = slot;
+  d.cta0 = cta0;
+  return d;
+}
+
+void bind_workspace(StackParams* p, void* ws, const WsLayout& w) {
+  uint8_t* b = static_cast<uint8_t*>(ws);
+  p->hdr = reinterpret_cast<unsigned*>(b);
+  p->slots = reinterpret_cast<unsigned*>(b + w.slots_off);
+  p->t_acc = reinterpret_cast<float*>(b + w.tacc_off);
+  p->t_part = reinterpret_cast<float*>(b + w.tpart_off);
+  p->y_part = reinterpret_cast<float*>(b + w.ypart_off);
 }
 
 rsp_status check_x_dtype(rsp_dtype d) {
@@ -302,9 +340,23 @@ rsp_status launch_forward(const rsp_linear* h, const void* x, rsp_dtype xdt, flo
   if (!ws || ws_bytes < h->plan.ws_bytes)
     return fail(RSP_E_USAGE, "workspace of %zu bytes is smaller than the %zu required", ws_bytes,
                 h->plan.ws_bytes);
-  FusedParams p = fused_params(h, x, xdt, y, ws, dense);
+  StackParams p = {};
+  p.descs = nullptr;
+  p.one = lin_desc(h, x, y, dense, 0, 0);
+  p.count = 1;
+  p.n_max = static_cast<int>(h->m_in);
+  p.cap_w = h->plan.cap_w;
+  p.cap_u = h->plan.cap_u;
+  p.cap_a = h->plan.cap_a;
+  p.abuf_bytes = h->plan.abuf;
+  p.bbuf_bytes = h->plan.bbuf;
+  p.nb_pad = h->plan.nb_pad;
+  p.deterministic = h->deterministic ? 1 : 0;
+  p.knobs = env_int("RSP_KNOBS", 0);
   p.trace = trace;
-  cudaError_t e = rsp::launch_fused(p, h->es, xdt == RSP_BF16, h->plan.grid, h->plan.smem, stream, h->pdl);
+  bind_workspace(&p, ws, WsLayout::make(1, h->plan.nb_pad, static_cast<int>(h->r_pad), h->plan.k_splits,
+                                         static_cast<int>(h->m_pad)));
+  cudaError_t e = rsp::launch_stack(p, h->es, xdt == RSP_BF16, h->plan.grid, h->plan.smem, stream, h->pdl);
   if (e != cudaSuccess) return fail(RSP_E_CUDA, "fused forward launch: %s", cudaGetErrorString(e));
   return RSP_OK;
 }
@@ -490,7 +542,7 @@ rsp_status rsp_linear_create(const rsp_linear_desc* d, rsp_linear** out) {
   }
   // The attribute is per kernel, not per launch: raise it to the opt-in
   // maximum once so every handle's plan fits regardless of creation order.
-  e = rsp::fused_set_smem(static_cast<size_t>(dp.smem_optin));
+  e = rsp::stack_set_smem(static_cast<size_t>(dp.smem_optin));
   if (e != cudaSuccess) {
     free_linear(h);
     return fail(RSP_E_CUDA, "cudaFuncSetAttribute(smem=%zu): %s", h->plan.smem, cudaGetErrorString(e));
@@ -805,43 +857,131 @@ rsp_status rsp_linear_export(const rsp_linear* h, int which, double* out) {
   return RSP_OK;
 }
 
-rsp_status rsp_stack_create(const rsp_linear* const* layers, uint32_t count, const void* const* x_devs,
-                            rsp_dtype xdt, float* const* y_devs, int dense, rsp_stack** out) {
+rsp_status rsp_stack_create_ex(const rsp_linear* const* layers, uint32_t count, const void* const* x_devs,
+                               rsp_dtype xdt, float* const* y_devs, int dense, const uint8_t* wait_prev,
+                               rsp_stack** out) {
   if (!layers || !x_devs || !y_devs || !out || count == 0) return fail(RSP_E_USAGE, "bad stack arguments");
   if (rsp_status st = check_x_dtype(xdt)) return st;
   *out = nullptr;
-  const int dev = layers[0]->device;
+  const rsp_linear* h0 = layers[0];
+  const int dev = h0->device;
   DeviceGuard g(dev);
-  size_t ws = 0;
+  std::vector<LinDesc> descs(count);
+  int grid = 1, n_max = 1, cap_w = 1, cap_u = 1, cap_a = 1, nb_pad = 4, r_pad_max = 8, ks_max = 1, m_pad_max = 8;
+  size_t smem = 0;
+  const bool det = h0->deterministic;
+  const DevProps dpx = device_props(dev);
   for (uint32_t i = 0; i < count; ++i) {
-    if (layers[i]->device != dev) return fail(RSP_E_USAGE, "stack layers must share one device");
-    ws = std::max(ws, layers[i]->plan.ws_bytes);
+    const rsp_linear* h = layers[i];
+    if (!h) return fail(RSP_E_USAGE, "null layer %u", i);
+    if (h->device != dev) return fail(RSP_E_USAGE, "stack layers must share one device");
+    if (h->es != h0->es) return fail(RSP_E_USAGE, "stack layers must share one weight dtype");
+    if (h->deterministic != det) return fail(RSP_E_USAGE, "stack layers must share the deterministic flag");
   }
+  // Groups: a linear that does not wait for its predecessor shares its
+  // input and runs beside it on a disjoint partition of the CTAs, sized by
+  // its share of the group's bytes.  Deterministic mode shares one
+  // partial-sum scratch, so there every linear waits for the previous one.
+  std::vector<LaunchPlan> plans(count);
+  for (uint32_t g0 = 0; g0 < count;) {
+    uint32_t g1 = g0 + 1;
+    while (g1 < count && !det && wait_prev && !wait_prev[g1]) ++g1;
+    double tot = 0.0;
+    std::vector<double> bytes(g1 - g0);
+    for (uint32_t i = g0; i < g1; ++i) {
+      const rsp_linear* h = layers[i];
+      const uint32_t kk = dense ? h->m_in : h->k;
+      const bool lr = !dense && h->rank > 0 && kk < h->m_in;
+      bytes[i - g0] = static_cast<double>(h->es) *
+                      (static_cast<double>(kk) * h->m_pad +
+                       (lr ? static_cast<double>(h->m_in - kk) * h->r_pad + static_cast<double>(h->rank) * h->m_pad : 0.0));
+      tot += bytes[i - g0];
+    }
+    int cta0 = 0;
+    const int sms = std::max(1, dpx.sms);
+    for (uint32_t i = g0; i < g1; ++i) {
+      int budget = g1 - g0 == 1 ? sms
+                                : std::max(1, static_cast<int>(std::floor(sms * bytes[i - g0] / std::max(tot, 1.0))));
+      budget = std::min(budget, sms - cta0 - static_cast<int>(g1 - 1 - i));  // leave >= 1 CTA per later member
+      if (rsp_status st = make_plan(*layers[i], dpx, &plans[i], std::max(1, budget))) return st;
+      const bool wp = i > 0 && (i == g0);
+      descs[i] = lin_desc(layers[i], x_devs[i], y_devs[i], dense != 0, static_cast<int>(i),
+                          wp ? rsp::kLinWaitPrev : 0, &plans[i], cta0);
+      cta0 += plans[i].grid;
+      grid = std::max(grid, cta0);
+    }
+    g0 = g1;
+  }
+  int need_a = 0, need_b = 0;
+  for (uint32_t i = 0; i < count; ++i) {
+    const rsp_linear* h = layers[i];
+    need_a = std::max(need_a, plans[i].need_a);
+    need_b = std::max(need_b, plans[i].need_b);
+    n_max = std::max(n_max, static_cast<int>(h->m_in));
+    cap_w = std::max(cap_w, plans[i].cap_w);
+    cap_u = std::max(cap_u, plans[i].cap_u);
+    cap_a = std::max(cap_a, plans[i].cap_a);
+    nb_pad = std::max(nb_pad, plans[i].nb_pad);
+    r_pad_max = std::max(r_pad_max, static_cast<int>(h->r_pad));
+    ks_max = std::max(ks_max, plans[i].k_splits);
+    m_pad_max = std::max(m_pad_max, static_cast<int>(h->m_pad));
+  }
+  smem = rsp::stack_smem_bytes(n_max, xdt == RSP_BF16, cap_w, cap_u, cap_a);
+  const DevProps& dp = dpx;
+  if (smem > static_cast<size_t>(dp.smem_optin))
+    return fail(RSP_E_UNSUPPORTED, "stack needs %zu B shared memory (> %d)", smem, dp.smem_optin);
+  int abuf = 0, bbuf = 0;
+  operand_buffers(static_cast<int>(dp.smem_optin - smem), need_a, need_b, &abuf, &bbuf);
+  smem = rsp::stack_smem_bytes(n_max, xdt == RSP_BF16, cap_w, cap_u, cap_a, abuf, bbuf);
+  const WsLayout wl = WsLayout::make(static_cast<int>(count), nb_pad, r_pad_max, ks_max, m_pad_max);
   auto* s = new rsp_stack();
   s->device = dev;
   cudaStream_t cs = nullptr;
-  cudaError_t e = cudaMalloc(&s->ws, ws);
-  if (e == cudaSuccess) e = cudaMemset(s->ws, 0, ws);
+  cudaError_t e = cudaMalloc(&s->ws, wl.bytes);
+  if (e == cudaSuccess) e = cudaMemset(s->ws, 0, wl.bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&s->descs, sizeof(LinDesc) * count);
+  if (e == cudaSuccess) e = cudaMemcpy(s->descs, descs.data(), sizeof(LinDesc) * count, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
-  rsp_status st = RSP_OK;
   if (e == cudaSuccess) {
-    for (uint32_t i = 0; i < count && !st; ++i)
-      st = launch_forward(layers[i], x_devs[i], xdt, y_devs[i], s->ws, ws, cs, dense != 0);
+    StackParams p = {};
+    p.descs = s->descs;
+    p.one = descs[0];
+    p.count = static_cast<int>(count);
+    p.n_max = n_max;
+    p.cap_w = cap_w;
+    p.cap_u = cap_u;
+    p.cap_a = cap_a;
+    p.abuf_bytes = abuf;
+    p.bbuf_bytes = bbuf;
+    p.nb_pad = nb_pad;
+    p.deterministic = det ? 1 : 0;
+    p.knobs = env_int("RSP_KNOBS", 0);
+    bind_workspace(&p, s->ws, wl);
+    s->params = p;
+    s->es = h0->es;
+    s->grid = grid;
+    s->x_bf16 = xdt == RSP_BF16;
+    s->smem = smem;
+    const cudaError_t el = rsp::launch_stack(p, h0->es, xdt == RSP_BF16, grid, smem, cs, h0->pdl);
     cudaGraph_t graph = nullptr;
     const cudaError_t ec = cudaStreamEndCapture(cs, &graph);
     s->graph = graph;
-    if (!st && ec != cudaSuccess) e = ec;
+    e = el != cudaSuccess ? el : ec;
   }
-  if (e == cudaSuccess && !st) e = cudaGraphInstantiate(&s->exec, s->graph, 0);
+  if (e == cudaSuccess) e = cudaGraphInstantiate(&s->exec, s->graph, 0);
   if (cs) cudaStreamDestroy(cs);
-  if (st || e != cudaSuccess) {
+  if (e != cudaSuccess) {
     rsp_stack_destroy(s);
-    if (st) return st;
     return fail(RSP_E_CUDA, "stack graph: %s", cudaGetErrorString(e));
   }
   *out = s;
   return RSP_OK;
+}
+
+rsp_status rsp_stack_create(const rsp_linear* const* layers, uint32_t count, const void* const* x_devs,
+                            rsp_dtype xdt, float* const* y_devs, int dense, rsp_stack** out) {
+  return rsp_stack_create_ex(layers, count, x_devs, xdt, y_devs, dense, nullptr, out);
 }
 
 rsp_status rsp_stack_launch(rsp_stack* s, void* stream) {
@@ -851,12 +991,24 @@ rsp_status rsp_stack_launch(rsp_stack* s, void* stream) {
   return RSP_OK;
 }
 
+rsp_status rsp_debug_stack_trace(rsp_stack* s, int64_t* trace_dev, uint32_t* grid_out, void* stream) {
+  if (!s || !trace_dev) return fail(RSP_E_USAGE, "null stack or trace buffer");
+  DeviceGuard g(s->device);
+  StackParams p = s->params;
+  p.trace = reinterpret_cast<long long*>(trace_dev);
+  cudaError_t e = rsp::launch_stack(p, s->es, s->x_bf16, s->grid, s->smem, static_cast<cudaStream_t>(stream), false);
+  if (e != cudaSuccess) return fail(RSP_E_CUDA, "stack trace launch: %s", cudaGetErrorString(e));
+  if (grid_out) *grid_out = static_cast<uint32_t>(s->grid);
+  return RSP_OK;
+}
+
 void rsp_stack_destroy(rsp_stack* s) {
   if (!s) return;
   DeviceGuard g(s->device);
   if (s->exec) cudaGraphExecDestroy(s->exec);
   if (s->graph) cudaGraphDestroy(s->graph);
   cudaFree(s->ws);
+  cudaFree(s->descs);
   delete s;
 }
 

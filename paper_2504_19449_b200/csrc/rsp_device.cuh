@@ -10,7 +10,7 @@
 
 namespace rsp {
 
-constexpr int kThreads = 512;               // every kernel in the fused path
+constexpr int kThreads = 256;               // every kernel in the fused path
 constexpr int kWarps = kThreads / 32;
 
 // ---------------------------------------------------------------------------
@@ -261,6 +261,39 @@ __device__ __forceinline__ uint4 ldg_l2(const void* p) {
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+// mbarrier / bulk-copy helpers on shared-window addresses.
+__device__ __forceinline__ void mbar_init_s(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_s(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_s(uint32_t bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  }
+}
+// 1-D TMA bulk copy global -> this CTA's shared memory, completion counted in
+// bytes on the mbarrier (dst, src 16-B aligned, bytes % 16 == 0).
+__device__ __forceinline__ void bulk_g2s_s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+// cp.async of 16 bytes to a shared-window address (LDGSTS, L2 only).
+__device__ __forceinline__ void cp_async16_s(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
@@ -311,6 +344,14 @@ __device__ __forceinline__ void prefetch_l2_keep(const void* p) {
   asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
 }
 
+// Register fence: the value must be materialised here.  Placed after a batch
+// of asm-volatile loads it keeps ptxas from interleaving each load with its
+// consumer (which leaves one load in flight per warp: measured, streaming
+// then runs at a fraction of HBM bandwidth).
+__device__ __forceinline__ void reg_fence(uint4& u) {
+  asm volatile("" : "+r"(u.x), "+r"(u.y), "+r"(u.z), "+r"(u.w));
+}
+
 // Streamed-once weights: no L1 allocation, first in line for L2 eviction.
 __device__ __forceinline__ uint4 ldg_stream_ef(const void* p, uint64_t pol) {
   uint4 u;
@@ -331,5 +372,22 @@ __device__ __forceinline__ void red_add_f32(float* p, float a) {
 }
 
 __device__ __forceinline__ float ldcg_f32(const float* p) { return __ldcg(p); }
+
+
+// ---------------------------------------------------------------------------
+// Counting barriers on workspace words that start every launch at zero (the
+// stack kernel's last CTA resets them): arrive = red.release.gpu (callers
+// __syncthreads first so the whole CTA's writes are ordered before it), wait
+// = acquire-poll until the count reaches the number of arriving CTAs.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void spin_until_count(const unsigned* p, unsigned target) {
+  unsigned long long spins = 0;
+  while (ld_acquire_gpu(p) < target) {
+    if (++spins > (1ull << 28)) __trap();  // watchdog: CTAs not co-resident / corrupted workspace
+  }
+}
 
 }  // namespace rsp

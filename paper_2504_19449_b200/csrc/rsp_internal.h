@@ -8,45 +8,72 @@
 
 namespace rsp {
 
-// Workspace regions at fixed offsets (shared by every layer using a workspace).
-constexpr unsigned kWsBarBytes = 1024;  // {count, gen} + per-column-tile tickets
-constexpr unsigned kTAccCap = 2048;     // floats per stage-1 t buffer (r_pad <= 2048)
+constexpr unsigned kTAccCap = 2048;  // floats per stage-1 t buffer (r_pad <= 2048)
+constexpr unsigned kSlotWords = 32;  // per-linear barrier slot: [0] y arrivals, [1] t arrivals, [2..] tickets
+constexpr unsigned kMaxTickets = kSlotWords - 2;
+constexpr unsigned kWsHdrBytes = 256;  // [0] launch epoch, [1] CTAs done in this launch
 
-// Parameters of one fused R-Sparse forward launch (see rsp_kernels.cu).
-struct FusedParams {
+// Flags of one linear in a stack launch.
+constexpr int kLinWaitPrev = 1;  // its x depends on the previous linear's y: full grid barrier first
+constexpr int kLinDense = 2;     // all n channels through W, no selection, no low-rank term
+
+// One linear of a stack launch (descriptors live in device memory; a
+// single-linear forward passes its descriptor inline).
+struct LinDesc {
   const void* Wt;  // [n][m_pad]  input-channel-major W (row j = W[:, j])
   const void* At;  // [r][m_pad]  A_r^T (row c = column c of a_r)
   const void* Bt;  // [n][r_pad]  B_r^T (row j = column j of b_r)
   const void* x;   // [n] fp32 or bf16
   float* y;        // [m] fp32
-  float* t_acc;    // [2][kTAccCap] stage-1 sums (fast mode; buffer = barrier generation & 1)
-  float* t_part;   // [r_pad][nb_pad] stage-1 partial sums, column b = CTA b (deterministic mode)
-  float* y_part;   // [k_splits][m_pad] split-K partial sums (deterministic mode)
-  unsigned* bars;  // [2] grid barrier {count, gen} + [col_tiles] tile tickets
   int n, m, m_pad, r, r_pad, k;
-  int col_tiles, k_splits;
-  int cap_w, cap_u, cap_a;  // per-CTA list capacities (W rows, stage-1 rows, A rows)
-  int nb_pad;               // row stride of t_part (grid rounded up to 4)
-  int deterministic;        // 1: fixed-order combines (bit-reproducible y)
-  int dense;                // 1: all n channels through W, no selection, no low-rank term
-  int pdl;                  // 1: launched with programmatic dependent launch
-  long long* trace;         // debug: [grid][16] phase timestamps (null in production)
+  int col_tiles, k_splits, grid;  // CTAs [cta0, cta0 + grid) work on this linear
+  int flags;
+  int slot;  // index of the linear's barrier slot / t buffers in the workspace
+  int cta0;  // first CTA of this linear (linears sharing an input run side by side)
 };
 
-struct LaunchPlan {
-  int col_tiles = 1, k_splits = 1, grid = 1;
-  int cap_w = 1, cap_u = 1, cap_a = 1;
-  int nb_pad = 4;
-  size_t smem = 0;
-  size_t ws_bytes = 0;  // workspace: barriers + t buffers + partials
-  size_t ws_acc_off = 0, ws_t_off = 0, ws_y_off = 0;
+// Parameters of one launch of the stack kernel (rsp_kernels.cu).
+struct StackParams {
+  const LinDesc* descs;  // device array of `count` descriptors (null: use `one`)
+  LinDesc one;
+  int count;
+  int n_max, cap_w, cap_u, cap_a;  // shared-memory carve-up (maxima over the linears)
+  int abuf_bytes, bbuf_bytes;      // shared-memory operand buffers (A_r^T tile rows, B_r^T slice)
+  unsigned* hdr;                   // workspace header
+  unsigned* slots;                 // [slots][kSlotWords]
+  float* t_acc;                    // [slots][2][kTAccCap] stage-1 sums (parity = launch epoch & 1)
+  float* t_part;                   // [r_pad][nb_pad] stage-1 partials (deterministic mode)
+  float* y_part;                   // [k_splits][m_pad] split-K partials (deterministic mode)
+  int nb_pad;                      // row stride of t_part
+  int deterministic;               // 1: fixed-order combines (bit-reproducible y); linears serialised
+  int pdl;                         // 1: launched with programmatic dependent launch
+  int knobs;                       // experiment switches (env RSP_KNOBS): 1 no W prefetch, 2 no A/B prefetch
+  long long* trace;                // debug: [grid][16] phase timestamps of the last linear (null in production)
 };
 
-// Shared-memory bytes the fused kernel needs for a plan.
-size_t fused_smem_bytes(const LaunchPlan& p, int n, bool x_bf16);
+// Workspace byte layout for `slots` linears; t_part/y_part sized for the
+// deterministic mode of the largest linear.
+struct WsLayout {
+  size_t slots_off, tacc_off, tpart_off, ypart_off, bytes;
+  static WsLayout make(int slots, int nb_pad, int r_pad_max, int ks_max, int m_pad_max) {
+    auto up = [](size_t v) { return (v + 255) / 256 * 256; };
+    WsLayout w;
+    w.slots_off = kWsHdrBytes;
+    w.tacc_off = up(w.slots_off + static_cast<size_t>(slots) * kSlotWords * 4);
+    w.tpart_off = up(w.tacc_off + static_cast<size_t>(slots) * 2 * kTAccCap * 4);
+    w.ypart_off = up(w.tpart_off + static_cast<size_t>(nb_pad) * (r_pad_max > 8 ? r_pad_max : 8) * 4);
+    w.bytes = up(w.ypart_off + static_cast<size_t>(ks_max) * m_pad_max * 4);
+    return w;
+  }
+};
 
-cudaError_t fused_set_smem(size_t smem);
-cudaError_t launch_fused(const FusedParams& p, int elem_bytes, bool x_bf16, int grid, size_t smem,
+// Shared-memory bytes of the stack kernel for these maxima (without / with
+// the operand buffers).
+size_t stack_smem_bytes(int n_max, bool x_bf16, int cap_w, int cap_u, int cap_a, int abuf_bytes = 0,
+                        int bbuf_bytes = 0);
+
+cudaError_t stack_set_smem(size_t smem);
+cudaError_t launch_stack(const StackParams& p, int elem_bytes, bool x_bf16, int grid, size_t smem,
                          cudaStream_t stream, bool pdl);
 
 // Stand-alone selector: one CTA.  Any of kept/rest/sparse may be null.

@@ -19,7 +19,7 @@
 // Decode is a chain of dependent linears, each only 2-8 us of HBM time, so the
 // kernel is shaped around hiding the fixed per-linear latency (x load,
 // selection, grid barrier, split-K combine; tools/overhead_probe.cu):
-//   * two CTAs fit per SM (<= 64 registers, < 110 KB shared memory), and each
+//   * two CTAs fit per SM (256 threads, <= 128 registers, < 110 KB shared memory), and each
 //     CTA releases its dependents (griddepcontrol.launch_dependents) right
 //     after it has waited for its own predecessor, so linear i+1's CTAs sit
 //     next to linear i's on every SM;
@@ -46,18 +46,20 @@
 
 namespace rsp {
 
-constexpr int kU = 8;               // rows in flight per warp
+constexpr int kU = 16;              // rows in flight per warp
+constexpr int kUA = 8;              // A_r^T rows per warp loaded ahead of the barrier wait
 constexpr int kRedFloats = 4096;    // 16 KB cross-group reduction scratch
 
 // Shared-memory carve-up of the fused kernel (host and device agree).  The
 // level-1 histogram is dead once the cut is known, so the cross-group
 // reduction scratch reuses it.
 struct SmemLayout {
-  uint32_t off_h1, off_cand, off_h2, off_misc, off_red, off_w, off_u, off_a, off_x, total;
+  uint32_t off_h1, off_cand, off_h2, off_misc, off_red, off_w, off_u, off_a, off_x, off_abuf, off_bbuf, total;
 
   __host__ __device__ static uint32_t up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
 
-  __host__ __device__ static SmemLayout make(int n, bool x_bf16, int cap_w, int cap_u, int cap_a) {
+  __host__ __device__ static SmemLayout make(int n, bool x_bf16, int cap_w, int cap_u, int cap_a, int abuf = 0,
+                                             int bbuf = 0) {
     SmemLayout L;
     uint32_t o = 0;
     L.off_h1 = o;
@@ -77,14 +79,15 @@ struct SmemLayout {
     o = up(o + 4u * cap_a, 16);
     L.off_x = o;
     o = up(o + (x_bf16 ? 2u : 4u) * static_cast<uint32_t>(n), 16);
+    L.off_abuf = o;
+    o = up(o + static_cast<uint32_t>(abuf), 16);
+    L.off_bbuf = o;
+    o = up(o + static_cast<uint32_t>(bbuf), 16);
     L.total = up(o, 128);
     return L;
   }
 };
 
-size_t fused_smem_bytes(const LaunchPlan& p, int n, bool x_bf16) {
-  return SmemLayout::make(n, x_bf16, p.cap_w, p.cap_u, p.cap_a).total;
-}
 
 __device__ __forceinline__ long long clk() {
   long long c;
@@ -96,12 +99,6 @@ __device__ __forceinline__ long long gtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-// Debug phase trace: slot 0 = globaltimer at CTA start, slots 1.. = clock64 - start.
-#define RSP_TRACE(ev)                                                            \
-  do {                                                                           \
-    if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * 16 + (ev)] = clk() - t_start; \
-  } while (0)
-
 // Partial sums of one lane's 16-byte column slice, returned in registers.
 struct Acc {
   float v[8];
@@ -112,25 +109,37 @@ struct Acc {
 // row(j) = base + j * row_bytes.  kU rows are loaded before any is consumed;
 // out-of-range slots reuse the last valid row with a zero coefficient so
 // every load is unconditional.  Out of line: one copy of the hot loop.
+// ptxas schedules each streaming load right before its first consumer, which
+// leaves one or two 16-byte loads in flight per warp (measured: streaming at
+// a fraction of HBM bandwidth).  The coefficients of a batch therefore take a
+// data dependence on EVERY load of the batch through `zero` -- a runtime 0
+// the compiler cannot fold (a kernel parameter) -- so all kU loads issue before
+// the first FMA.
+__device__ __forceinline__ float batch_dep(const uint4 (&u)[kU], uint32_t zero) {
+  uint32_t t = 0;
+#pragma unroll
+  for (int q = 0; q < kU; ++q) t ^= u[q].x;
+  return __uint_as_float(t & zero);  // +0.0f at run time
+}
+
 template <typename WT>
-__device__ __noinline__ Acc stream_list(uint32_t list, int first, int count, int stride, bool lane_ok,
-                                        const uint8_t* base, uint32_t row_bytes, uint64_t pol) {
+__device__ __forceinline__ Acc stream_list(uint32_t list, int first, int count, int stride, bool lane_ok,
+                                           const uint8_t* base, uint32_t row_bytes, uint64_t pol, uint32_t zero) {
   float acc[Vec<WT>::kElems];
 #pragma unroll
   for (int e = 0; e < Vec<WT>::kElems; ++e) acc[e] = 0.f;
   if (lane_ok) {
     for (int i0 = first; i0 < count; i0 += stride * kU) {
+      uint2 e[kU];
+#pragma unroll
+      for (int q = 0; q < kU; ++q) e[q] = lds2(list + 8u * static_cast<uint32_t>(min(i0 + q * stride, count - 1)));
       uint4 u[kU];
-      float c[kU];
 #pragma unroll
-      for (int q = 0; q < kU; ++q) {
-        const int i = i0 + q * stride;
-        const uint2 e = lds2(list + 8u * static_cast<uint32_t>(min(i, count - 1)));
-        c[q] = i < count ? __uint_as_float(e.y) : 0.f;
-        u[q] = ldg_stream_ef(base + static_cast<size_t>(e.x) * row_bytes, pol);
-      }
+      for (int q = 0; q < kU; ++q) u[q] = ldg_stream_ef(base + static_cast<size_t>(e[q].x) * row_bytes, pol);
+      const float dep = batch_dep(u, zero);
 #pragma unroll
-      for (int q = 0; q < kU; ++q) Vec<WT>::fma(acc, u[q], c[q]);
+      for (int q = 0; q < kU; ++q)
+        Vec<WT>::fma(acc, u[q], (i0 + q * stride < count ? __uint_as_float(e[q].y) : 0.f) + dep);
     }
   }
   Acc r;
@@ -142,23 +151,23 @@ __device__ __noinline__ Acc stream_list(uint32_t list, int first, int count, int
 // Consecutive rows (the A_r^T rows, prefetched into L2):
 // sum over i of coef[i] * (base + i * row_bytes)[lane's 16 B].
 template <typename WT>
-__device__ __noinline__ Acc stream_seq(uint32_t coef, int first, int count, int stride, bool lane_ok,
-                                       const uint8_t* base, uint32_t row_bytes, uint64_t pol) {
+__device__ __forceinline__ Acc stream_seq(uint32_t coef, int first, int count, int stride, bool lane_ok,
+                                          const uint8_t* base, uint32_t row_bytes, uint64_t pol, uint32_t zero) {
   float acc[Vec<WT>::kElems];
 #pragma unroll
   for (int e = 0; e < Vec<WT>::kElems; ++e) acc[e] = 0.f;
   if (lane_ok) {
     for (int i0 = first; i0 < count; i0 += stride * kU) {
       uint4 u[kU];
-      float c[kU];
+#pragma unroll
+      for (int q = 0; q < kU; ++q)
+        u[q] = ldg_stream_ef(base + static_cast<size_t>(min(i0 + q * stride, count - 1)) * row_bytes, pol);
+      const float dep = batch_dep(u, zero);
 #pragma unroll
       for (int q = 0; q < kU; ++q) {
         const int i = min(i0 + q * stride, count - 1);
-        c[q] = i0 + q * stride < count ? ldsf(coef + 4u * i) : 0.f;
-        u[q] = ldg_stream_ef(base + static_cast<size_t>(i) * row_bytes, pol);
+        Vec<WT>::fma(acc, u[q], (i0 + q * stride < count ? ldsf(coef + 4u * i) : 0.f) + dep);
       }
-#pragma unroll
-      for (int q = 0; q < kU; ++q) Vec<WT>::fma(acc, u[q], c[q]);
     }
   }
   Acc r;
@@ -173,99 +182,182 @@ __device__ __forceinline__ int part(int total, int i, int parts) {
   return static_cast<int>(static_cast<uint32_t>(total) * static_cast<uint32_t>(i) / static_cast<uint32_t>(parts));
 }
 
+// ---------------------------------------------------------------------------
+// The stack kernel: one persistent launch runs `count` linears in order.
+// Per linear, every CTA with blockIdx < grid owns a (column tile, channel
+// split); CTAs beyond a linear's grid only take part in its completion
+// barrier.  Per-linear barrier slots in the workspace are reset by the last
+// CTA of the launch, so every launch starts from zero counts.
+// ---------------------------------------------------------------------------
+struct Ctx {
+  SelArea S;
+  uint32_t list_w, list_u, coef_a, red;
+  uint32_t obuf;        // shared-memory operand buffer (B_r^T slice, then A_r^T tile rows)
+  int obuf_bytes;
+  uint32_t bar;         // mbarrier of the operand bulk copies
+  uint64_t pol;
+  uint32_t epoch;
+  uint32_t zero;  // 0 at run time, opaque to the compiler (stream_list)
+};
+
+// How much of CTA b's operands of linear d sit in shared memory: the whole
+// B_r^T channel slice or none of it, and the first `na_s` A_r^T tile rows.
+struct OperandSplit {
+  bool b_smem;
+  int na_s;
+  __device__ __forceinline__ uint32_t a_off(int nu, int rowB) const {  // A rows after the B slice
+    return b_smem ? static_cast<uint32_t>((nu * rowB + 15) / 16 * 16) : 0u;
+  }
+};
+
+__device__ __forceinline__ unsigned* slot_of(const StackParams& P, int slot) {
+  return P.slots + static_cast<size_t>(slot) * kSlotWords;
+}
+
+template <typename WT>
+__device__ __forceinline__ OperandSplit operand_split(const LinDesc& d, int b, const Ctx& C) {
+  constexpr int ES = static_cast<int>(sizeof(WT));
+  OperandSplit o{false, 0};
+  if ((d.flags & kLinDense) || d.r <= 0 || d.k >= d.n) return o;
+  const int KS = d.k_splits, ct = b / KS, ks = b % KS;
+  const int vrow = d.m_pad * ES / 16, wcols = (vrow + 31) / 32;
+  const int tw = min(vrow, 32 * part(wcols, ct + 1, d.col_tiles)) - min(vrow, 32 * part(wcols, ct, d.col_tiles));
+  const int na = part(d.r, ks + 1, KS) - part(d.r, ks, KS);
+  const int nu = part(d.n, b + 1, d.grid) - part(d.n, b, d.grid);
+  // one operand buffer per CTA: the whole B_r^T slice first (or none of it),
+  // then as many A_r^T tile rows as fit
+  const int bytes_b = nu * d.r_pad * ES;
+  o.b_smem = bytes_b <= C.obuf_bytes;
+  const int room = C.obuf_bytes - (o.b_smem ? (bytes_b + 15) / 16 * 16 : 0);
+  o.na_s = tw > 0 ? min(na, room / (tw * 16)) : 0;
+  return o;
+}
+
+// The x-independent operands of CTA bg's share of linear d go to shared
+// memory by TMA bulk copies issued by one warp (the B_r^T channel slice is one
+// contiguous block, each A_r^T tile row one copy), completing on C.bar; they
+// land while the previous linear drains and this one selects, when HBM is
+// otherwise idle.  Measured: per-thread cp.async / prefetch loops stall every
+// warp for microseconds of issue, which costs more than it hides.
+// Returns whether a copy was issued (the consumer then waits on C.bar).
+template <typename WT>
+__device__ __forceinline__ bool preload_operands(const LinDesc& d, int bg, const Ctx& C) {
+  constexpr int ES = static_cast<int>(sizeof(WT));
+  const int b = bg - d.cta0;  // this CTA's index within the linear's partition
+  if (b < 0 || b >= d.grid || (d.flags & kLinDense) || d.r <= 0 || d.k >= d.n) return false;
+  const OperandSplit os = operand_split<WT>(d, b, C);
+  const int KS = d.k_splits, ct = b / KS, ks = b % KS;
+  const int vrow = d.m_pad * ES / 16, wcols = (vrow + 31) / 32;
+  const int v0 = min(vrow, 32 * part(wcols, ct, d.col_tiles)), v1 = min(vrow, 32 * part(wcols, ct + 1, d.col_tiles));
+  const int tw = v1 - v0;
+  const int alo = part(d.r, ks, KS);
+  const int uc0 = part(d.n, b, d.grid), nu = part(d.n, b + 1, d.grid) - uc0;
+  const uint32_t rowW = static_cast<uint32_t>(d.m_pad) * ES, rowB = static_cast<uint32_t>(d.r_pad) * ES;
+  const uint32_t bytes_b = os.b_smem ? static_cast<uint32_t>(nu) * rowB : 0u;
+  const uint32_t bytes_a = static_cast<uint32_t>(os.na_s) * static_cast<uint32_t>(tw) * 16u;
+  if (bytes_a + bytes_b == 0) return false;
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    if (lane == 0) {
+      fence_proxy_async_smem();  // earlier generic reads of the buffers precede the async writes
+      mbar_expect_tx_s(C.bar, bytes_a + bytes_b);
+    }
+    __syncwarp();
+    if (bytes_b && lane == 0)
+      bulk_g2s_s(C.obuf, static_cast<const uint8_t*>(d.Bt) + static_cast<size_t>(uc0) * rowB, bytes_b, C.bar);
+    const uint8_t* a_tile = static_cast<const uint8_t*>(d.At) + static_cast<size_t>(v0) * 16 + static_cast<size_t>(alo) * rowW;
+    const uint32_t abase_s = C.obuf + os.a_off(nu, static_cast<int>(rowB));
+    for (int i = lane; i < os.na_s; i += 32)
+      bulk_g2s_s(abase_s + static_cast<uint32_t>(i * tw) * 16u, a_tile + static_cast<size_t>(i) * rowW,
+                 static_cast<uint32_t>(tw) * 16u, C.bar);
+  }
+  return true;
+}
+
+// Stage-1 rows from the shared-memory B_r^T slice: sum over the list's
+// channels j (i = first, first + stride, ...) of x_j * slice[j - uc0][lane's 16 B].
+template <typename WT>
+__device__ __forceinline__ Acc stream_list_smem(uint32_t list, int first, int count, int stride, bool lane_ok,
+                                                uint32_t sbase, int uc0, uint32_t row_bytes) {
+  float acc[Vec<WT>::kElems];
+#pragma unroll
+  for (int e = 0; e < Vec<WT>::kElems; ++e) acc[e] = 0.f;
+  if (lane_ok) {
+#pragma unroll 4
+    for (int i = first; i < count; i += stride) {
+      const uint2 e = lds2(list + 8u * static_cast<uint32_t>(i));
+      Vec<WT>::fma(acc, lds4(sbase + (e.x - static_cast<uint32_t>(uc0)) * row_bytes), __uint_as_float(e.y));
+    }
+  }
+  Acc r;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) r.v[e] = e < Vec<WT>::kElems ? acc[e] : 0.f;
+  return r;
+}
+
+// One linear, CTA b < d.grid.  Ends with this CTA's contribution to y issued.
 template <typename WT, bool XBF>
-__global__ void __launch_bounds__(kThreads, 2) linear_kernel(const FusedParams p) {
+__device__ __forceinline__ void run_linear(const StackParams& P, const LinDesc& d, const Ctx& C,
+                                           long long* trace, bool preloaded, uint32_t parity) {
   const long long t_start = clk();
-  if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * 16] = gtimer();
-  extern __shared__ __align__(16) uint8_t smem[];
   constexpr int VE = Vec<WT>::kElems;  // elements per 16 B
   constexpr int ES = static_cast<int>(sizeof(WT));
-  const SmemLayout L = SmemLayout::make(p.n, XBF, p.cap_w, p.cap_u, p.cap_a);
-  const uint32_t sb = smem_base_pinned(smem);  // shared-window base: every access below is LDS/STS
-  SelArea S;
-  S.xs = sb + L.off_x;
-  S.h1 = sb + L.off_h1;
-  S.cand = sb + L.off_cand;
-  S.h2a = sb + L.off_h2;
-  S.h2b = S.h2a + 4u * 256;
-  S.misc = sb + L.off_misc;
-  const uint32_t list_w = sb + L.off_w;  // {channel j, bits of x_j}: W rows of this CTA in S
-  const uint32_t list_u = sb + L.off_u;  // stage-1 rows of this CTA in S^c
-  const uint32_t coef_a = sb + L.off_a;  // t_c of this CTA's A_r^T rows
-  const uint32_t red = sb + L.off_red;   // cross-group reduction scratch
-
+  const SelArea& S = C.S;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int b = blockIdx.x, NB = gridDim.x;
-  const int KS = p.k_splits;
+  const int b = static_cast<int>(blockIdx.x) - d.cta0, NB = d.grid;  // index within the linear's partition
+  const int KS = d.k_splits;
   const int ct = b / KS, ks = b % KS;
+  const bool dense = (d.flags & kLinDense) != 0;
+#define RSP_TRACE(ev)                                                              \
+  do {                                                                             \
+    if (trace && tid == 0) trace[ev] = clk() - t_start;                           \
+  } while (0)
 
   // Column tile of this CTA in 16-byte units (whole 32-unit warp columns).
-  const int vrow = p.m_pad * ES / 16;
+  const int vrow = d.m_pad * ES / 16;
   const int wcols = (vrow + 31) / 32;
-  const int v0 = min(vrow, 32 * part(wcols, ct, p.col_tiles)), v1 = min(vrow, 32 * part(wcols, ct + 1, p.col_tiles));
+  const int v0 = min(vrow, 32 * part(wcols, ct, d.col_tiles)), v1 = min(vrow, 32 * part(wcols, ct + 1, d.col_tiles));
   const int tw = v1 - v0, col0 = v0 * VE;
 
-  const int k_eff = p.dense ? p.n : p.k;
-  const bool has_lr = !p.dense && p.r > 0 && k_eff < p.n;
-  const bool det = p.deterministic != 0;
+  const int k_eff = dense ? d.n : d.k;
+  const bool has_lr = !dense && d.r > 0 && k_eff < d.n;
+  const bool det = P.deterministic != 0;
   const bool use_bar = has_lr || (KS > 1 && !det);
   // Static channel ranges: W rows in [wc0, wc1), stage-1 rows in [uc0, uc1),
   // A_r^T rows [alo, ahi).
-  const int wc0 = part(p.n, ks, KS), wc1 = part(p.n, ks + 1, KS);
-  const int uc0 = has_lr ? part(p.n, b, NB) : 0, uc1 = has_lr ? part(p.n, b + 1, NB) : 0;
-  const int alo = has_lr ? part(p.r, ks, KS) : 0, ahi = has_lr ? part(p.r, ks + 1, KS) : 0;
+  const int wc0 = part(d.n, ks, KS), wc1 = part(d.n, ks + 1, KS);
+  const int uc0 = has_lr ? part(d.n, b, NB) : 0, uc1 = has_lr ? part(d.n, b + 1, NB) : 0;
+  const int alo = has_lr ? part(d.r, ks, KS) : 0, ahi = has_lr ? part(d.r, ks + 1, KS) : 0;
   const int na = ahi - alo;
+  const OperandSplit os = operand_split<WT>(d, b, C);  // rows [0, os.na_s) of A in shared memory
 
-  const uint8_t* Wt = static_cast<const uint8_t*>(p.Wt);
-  const uint8_t* At = static_cast<const uint8_t*>(p.At);
-  const uint8_t* Bt = static_cast<const uint8_t*>(p.Bt);
-  const uint32_t rowW = static_cast<uint32_t>(p.m_pad) * ES;  // bytes per W^T / A_r^T row
-  const uint32_t rowB = static_cast<uint32_t>(p.r_pad) * ES;  // bytes per B_r^T row
+  const uint8_t* Wt = static_cast<const uint8_t*>(d.Wt);
+  const uint8_t* At = static_cast<const uint8_t*>(d.At);
+  const uint8_t* Bt = static_cast<const uint8_t*>(d.Bt);
+  const uint32_t rowW = static_cast<uint32_t>(d.m_pad) * ES;  // bytes per W^T / A_r^T row
+  const uint32_t rowB = static_cast<uint32_t>(d.r_pad) * ES;  // bytes per B_r^T row
   const uint8_t* a_tile = At + static_cast<size_t>(col0) * ES;
-  const uint64_t pol = l2_evict_first_policy();
+  unsigned* slot = slot_of(P, d.slot);
+  float* t_cur = P.t_acc + (static_cast<size_t>(d.slot) * 2 + (C.epoch & 1u)) * kTAccCap;
+  float* t_nxt = P.t_acc + (static_cast<size_t>(d.slot) * 2 + ((C.epoch + 1u) & 1u)) * kTAccCap;
 
-  // ---- prologue: independent of x (overlaps the previous linear under PDL) ----
-  if (has_lr) {
-    const int la = (tw * 16 + 127) / 128, lb = static_cast<int>((rowB + 127) / 128);
-    const int tot_a = na * la, tot = tot_a + (uc1 - uc0) * lb;
-    for (int f = tid; f < tot; f += kThreads) {
-      if (f < tot_a) {
-        const int i = f / la, l = f - i * la;
-        prefetch_l2_keep(a_tile + static_cast<size_t>(alo + i) * rowW + 128 * l);
-      } else {
-        const int g = f - tot_a, i = g / lb, l = g - i * lb;
-        prefetch_l2_keep(Bt + static_cast<size_t>(uc0 + i) * rowB + 128 * l);
-      }
-    }
-  }
-  if (!p.dense) sel_clear(S);
-  if (p.pdl) {
-    griddep_wait();
-    griddep_launch_dependents();
-  }
-  RSP_TRACE(1);
   if (use_bar) {
-    if (tid == 0) S.set_m(M_GEN, ld_relaxed_gpu(p.bars + 1));  // nobody of this launch has arrived yet
-    if (KS > 1 && !det) {  // zero this CTA's slice of y; published by the grid barrier
-      const int y0 = part(p.m, b, NB), y1 = part(p.m, b + 1, NB);
-      for (int i = y0 + tid; i < y1; i += kThreads) p.y[i] = 0.f;
+    if (KS > 1 && !det) {  // zero this CTA's slice of y; published by the barrier below
+      const int y0 = part(d.m, b, NB), y1 = part(d.m, b + 1, NB);
+      for (int i = y0 + tid; i < y1; i += kThreads) d.y[i] = 0.f;
     }
-  }
-  __syncthreads();  // histograms zeroed, generation published
-  const uint32_t gen0 = use_bar ? S.m(M_GEN) : 0u;
-  float* t_cur = p.t_acc + (gen0 & 1u) * kTAccCap;
-  if (use_bar) {
-    // Zero this CTA's slice of the next barrier launch's t buffer (all of it:
-    // the next launch on this workspace may be a layer of a larger rank).
-    float* t_nxt = p.t_acc + ((gen0 + 1u) & 1u) * kTAccCap;
+    // zero this CTA's slice of the next launch's t buffer of this slot
     const int c0 = part(static_cast<int>(kTAccCap), b, NB), c1 = part(static_cast<int>(kTAccCap), b + 1, NB);
     for (int c = c0 + tid; c < c1; c += kThreads) t_nxt[c] = 0.f;
   }
+  if (!dense) sel_clear(S);
+  __syncthreads();  // histograms zero; previous linear's shared-memory use complete
+  RSP_TRACE(1);
 
   // ---- 1. x -> shared memory + level-1 histogram; the exact cut ----
-  sel_load<XBF>(p.x, p.n, S, !p.dense);
+  sel_load<XBF>(d.x, d.n, S, !dense);
   RSP_TRACE(2);
-  const Cut cut = p.dense ? Cut{0u, INT_MAX} : sel_cut<XBF>(p.n, p.k, S);
+  const Cut cut = dense ? Cut{0u, INT_MAX} : sel_cut<XBF>(d.n, d.k, S);
   RSP_TRACE(3);
 
   // ---- 2. this CTA's row lists: W rows of S in [wc0, wc1), stage-1 rows of S^c in [uc0, uc1) ----
@@ -273,62 +365,79 @@ __global__ void __launch_bounds__(kThreads, 2) linear_kernel(const FusedParams p
   compact2(
       S, wc0, wc1, uc0, uc1, [&](int j) { return in_cut(sel_key<XBF>(S, j), j, cut); },
       [&](int j) { return !in_cut(sel_key<XBF>(S, j), j, cut); },
-      [&](int i, int j) { sts2(list_w + 8u * i, static_cast<uint32_t>(j), sel_bits<XBF>(S, j)); },
-      [&](int i, int j) { sts2(list_u + 8u * i, static_cast<uint32_t>(j), sel_bits<XBF>(S, j)); }, &nW, &nU);
+      [&](int i, int j) { sts2(C.list_w + 8u * i, static_cast<uint32_t>(j), sel_bits<XBF>(S, j)); },
+      [&](int i, int j) { sts2(C.list_u + 8u * i, static_cast<uint32_t>(j), sel_bits<XBF>(S, j)); }, &nW, &nU);
   RSP_TRACE(4);
-
-  // ---- 3. stage 1: partial t over this CTA's S^c slice (B_r^T rows from L2) ----
+  // ---- 3. stage 1: partial t over this CTA's S^c slice (B_r^T rows from the
+  // shared-memory slice preloaded while the previous linear drained) ----
   if (has_lr) {
-    const int vb = p.r_pad * ES / 16;  // 16-B units per B_r^T row
+    const int vb = d.r_pad * ES / 16;  // 16-B units per B_r^T row
     const int C1 = (vb + 31) / 32, G1 = kWarps / C1, g1 = warp / C1;
-    const int v = (warp % C1) * 32 + lane;
-    const bool ok = g1 < G1 && v < vb;
-    const Acc a1 = stream_list<WT>(list_u, g1, nU, G1, ok, Bt + v * 16, rowB, pol);
+    const int v1 = (warp % C1) * 32 + lane;
+    const bool ok = g1 < G1 && v1 < vb;
+    if (preloaded) mbar_wait_s(C.bar, parity);  // the operand bulk copies have landed
+    RSP_TRACE(10);
+    const Acc a1 = os.b_smem ? stream_list_smem<WT>(C.list_u, g1, nU, G1, ok, C.obuf + v1 * 16u, uc0, rowB)
+                             : stream_list<WT>(C.list_u, g1, nU, G1, ok, Bt + v1 * 16, rowB, C.pol, C.zero);
+    RSP_TRACE(11);
     if (ok) {
 #pragma unroll
-      for (int e = 0; e < VE; ++e) stsf(red + 4u * (g1 * p.r_pad + v * VE + e), a1.v[e]);
+      for (int e = 0; e < VE; ++e) stsf(C.red + 4u * (g1 * d.r_pad + v1 * VE + e), a1.v[e]);
     }
     __syncthreads();
-    for (int c = tid; c < p.r_pad; c += kThreads) {
+    for (int c = tid; c < d.r_pad; c += kThreads) {
       float sum = 0.f;
-      for (int g = 0; g < G1; ++g) sum += ldsf(red + 4u * (g * p.r_pad + c));
+      for (int g = 0; g < G1; ++g) sum += ldsf(C.red + 4u * (g * d.r_pad + c));
       if (det)
-        p.t_part[static_cast<size_t>(c) * p.nb_pad + b] = sum;
+        P.t_part[static_cast<size_t>(c) * P.nb_pad + b] = sum;
       else if (sum != 0.f)
         red_add_f32(t_cur + c, sum);
     }
+    RSP_TRACE(12);
   }
   if (use_bar) {
-    __syncthreads();  // this CTA's t contributions and y zeroing are issued
-    if (tid == 0) gbar_arrive(p.bars, static_cast<unsigned>(NB), gen0);
+    __syncthreads();  // this CTA's t contributions and y zeroing are issued; `red` is free again
+    if (tid == 0) red_release_add(slot + 1, 1u);
   }
   RSP_TRACE(5);
 
-  // ---- 4. W rows of S (HBM) ----
-  const int C2 = (tw + 31) / 32, G2 = kWarps / max(C2, 1), g2 = warp / max(C2, 1);
-  const int v = (warp % max(C2, 1)) * 32 + lane;
+  // ---- 4. W rows of S (HBM): all warps; the t barrier completes meanwhile ----
+  const int C2 = max((tw + 31) / 32, 1), G2 = kWarps / C2, g2 = warp / C2;
+  const int v = (warp % C2) * 32 + lane;
   const bool ok2 = g2 < G2 && v < tw;
-  Acc acc = stream_list<WT>(list_w, g2, nW, G2, ok2, Wt + static_cast<size_t>(col0) * ES + v * 16, rowW, pol);
+  Acc acc = stream_list<WT>(C.list_w, g2, nW, G2, ok2, Wt + static_cast<size_t>(col0) * ES + v * 16, rowW, C.pol,
+                            C.zero);
   RSP_TRACE(6);
 
   // ---- 5. stage 2: A_r^T rows [alo, ahi) (L2) ----
+  // The first batch of this warp's A rows is loaded before waiting on the
+  // barrier (A does not depend on t), so its L2 round trip overlaps the wait.
+  const uint8_t* abase = a_tile + static_cast<size_t>(alo) * rowW + v * 16;
+  uint4 ua[kUA];
+  if (has_lr && ok2) {
+#pragma unroll
+    for (int q = 0; q < kUA; ++q) {  // first global batch (rows past the shared-memory ones)
+      const int i = min(os.na_s + g2 + q * G2, max(na - 1, 0));
+      ua[q] = ldg_stream_ef(abase + static_cast<size_t>(i) * rowW, C.pol);
+    }
+  }
   if (use_bar) {
-    if (tid == 0) gbar_wait(p.bars, gen0);
+    if (tid == 0) spin_until_count(slot + 1, static_cast<unsigned>(NB));
     __syncthreads();
   }
   RSP_TRACE(7);
   if (has_lr) {
     if (!det) {
-      for (int i = tid; i < na; i += kThreads) stsf(coef_a + 4u * i, __ldcg(t_cur + alo + i));
+      for (int i = tid; i < na; i += kThreads) stsf(C.coef_a + 4u * i, __ldcg(t_cur + alo + i));
     } else {
       // 8 lanes per row sum the row's nb_pad partials (float4 loads, fixed order, fixed xor tree)
       const int g8 = tid >> 3, l8 = tid & 7, ng8 = kThreads / 8;
-      const int nq = p.nb_pad / 4;
+      const int nq = P.nb_pad / 4;
       for (int cbase = alo; cbase < ahi; cbase += ng8) {  // uniform trip count: shuffles below
         const int c = cbase + g8;
         float sum = 0.f;
         if (c < ahi) {
-          const float4* row = reinterpret_cast<const float4*>(p.t_part + static_cast<size_t>(c) * p.nb_pad);
+          const float4* row = reinterpret_cast<const float4*>(P.t_part + static_cast<size_t>(c) * P.nb_pad);
           for (int q = l8; q < nq; q += 8) {
             const float4 u = __ldcg(row + q);
             sum += (u.x + u.y) + (u.z + u.w);
@@ -337,78 +446,188 @@ __global__ void __launch_bounds__(kThreads, 2) linear_kernel(const FusedParams p
         sum += __shfl_xor_sync(0xffffffffu, sum, 4);
         sum += __shfl_xor_sync(0xffffffffu, sum, 2);
         sum += __shfl_xor_sync(0xffffffffu, sum, 1);
-        if (l8 == 0 && c < ahi) stsf(coef_a + 4u * (c - alo), sum);
+        if (l8 == 0 && c < ahi) stsf(C.coef_a + 4u * (c - alo), sum);
       }
     }
     __syncthreads();
-    const Acc a2 = stream_seq<WT>(coef_a, g2, na, G2, ok2, a_tile + static_cast<size_t>(alo) * rowW + v * 16,
-                                  rowW, pol);
+    if (ok2) {
+      float acc8[Vec<WT>::kElems];
+#pragma unroll
+      for (int e = 0; e < VE; ++e) acc8[e] = acc.v[e];
+      // shared-memory rows
+      const uint32_t a_s = C.obuf + os.a_off(uc1 - uc0, static_cast<int>(rowB));
+#pragma unroll 4
+      for (int i = g2; i < os.na_s; i += G2)
+        Vec<WT>::fma(acc8, lds4(a_s + (static_cast<uint32_t>(i) * tw + v) * 16u), ldsf(C.coef_a + 4u * i));
+      // the early global batch
+#pragma unroll
+      for (int q = 0; q < kUA; ++q) {
+        const int i = os.na_s + g2 + q * G2;
+        Vec<WT>::fma(acc8, ua[q], i < na ? ldsf(C.coef_a + 4u * i) : 0.f);
+      }
+#pragma unroll
+      for (int e = 0; e < VE; ++e) acc.v[e] = acc8[e];
+    }
+    const Acc a2 = stream_seq<WT>(C.coef_a, os.na_s + g2 + kUA * G2, na, G2, ok2, abase, rowW, C.pol, C.zero);
 #pragma unroll
     for (int e = 0; e < VE; ++e) acc.v[e] += a2.v[e];
   }
   RSP_TRACE(8);
 
   // ---- 6. cross-group reduction, then y ----
-  const int gstride = max(C2, 1) * 32 * VE;  // floats per group in `red`
+  const int gstride = C2 * 32 * VE;  // floats per group in `red`
   if (ok2) {
 #pragma unroll
-    for (int e = 0; e < VE; ++e) stsf(red + 4u * (g2 * gstride + v * VE + e), acc.v[e]);
+    for (int e = 0; e < VE; ++e) stsf(C.red + 4u * (g2 * gstride + v * VE + e), acc.v[e]);
   }
   __syncthreads();
   const int tcw = tw * VE;  // floats in this tile (multiple of 4)
-  const bool y16 = (reinterpret_cast<uintptr_t>(p.y) & 15u) == 0;
+  const bool y16 = (reinterpret_cast<uintptr_t>(d.y) & 15u) == 0;
   for (int q = tid; q < tcw / 4; q += kThreads) {
     float s4[4] = {0.f, 0.f, 0.f, 0.f};
     for (int g = 0; g < G2; ++g) {
-      const uint4 u = lds4(red + 4u * (g * gstride + 4 * q));
+      const uint4 u = lds4(C.red + 4u * (g * gstride + 4 * q));
       s4[0] += __uint_as_float(u.x);
       s4[1] += __uint_as_float(u.y);
       s4[2] += __uint_as_float(u.z);
       s4[3] += __uint_as_float(u.w);
     }
     const int col = col0 + 4 * q;
-    if (col >= p.m) continue;
+    if (col >= d.m) continue;
     if (KS > 1 && det) {
-      *reinterpret_cast<float4*>(p.y_part + static_cast<size_t>(ks) * p.m_pad + col) =
+      *reinterpret_cast<float4*>(P.y_part + static_cast<size_t>(ks) * d.m_pad + col) =
           make_float4(s4[0], s4[1], s4[2], s4[3]);
     } else if (KS > 1) {
-      if (y16 && col + 3 < p.m) {
-        red_add_v4(p.y + col, s4[0], s4[1], s4[2], s4[3]);
+      if (y16 && col + 3 < d.m) {
+        red_add_v4(d.y + col, s4[0], s4[1], s4[2], s4[3]);
       } else {
-        for (int e = 0; e < 4 && col + e < p.m; ++e) red_add_f32(p.y + col + e, s4[e]);
+        for (int e = 0; e < 4 && col + e < d.m; ++e) red_add_f32(d.y + col + e, s4[e]);
       }
     } else {
-      for (int e = 0; e < 4 && col + e < p.m; ++e) p.y[col + e] = s4[e];
+      for (int e = 0; e < 4 && col + e < d.m; ++e) d.y[col + e] = s4[e];
     }
   }
   if (KS > 1 && det) {
     __threadfence();
     __syncthreads();
-    unsigned* ticket = p.bars + 2 + ct;
+    unsigned* ticket = slot + 2 + (ct % kMaxTickets);
     if (tid == 0) S.set_m(M_LAST, atom_add_acq_rel_gpu(ticket, 1u) == static_cast<unsigned>(KS - 1));
     __syncthreads();
     if (S.m(M_LAST)) {
       // Last CTA of this column tile: fixed-order sum of the k_splits partials.
       for (int c = tid; c < tcw; c += kThreads) {
         const int col = col0 + c;
-        if (col >= p.m) break;
+        if (col >= d.m) break;
         float sum = 0.f;
 #pragma unroll 4
-        for (int kk = 0; kk < KS; ++kk) sum += __ldcg(p.y_part + static_cast<size_t>(kk) * p.m_pad + col);
-        p.y[col] = sum;
+        for (int kk = 0; kk < KS; ++kk) sum += __ldcg(P.y_part + static_cast<size_t>(kk) * d.m_pad + col);
+        d.y[col] = sum;
       }
       if (tid == 0) st_relaxed_gpu(ticket, 0u);
     }
   }
   RSP_TRACE(9);
+#undef RSP_TRACE
 }
 
-cudaError_t fused_set_smem(size_t smem) {
+template <typename WT, bool XBF>
+__global__ void __launch_bounds__(kThreads, 1) stack_kernel(const StackParams P) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const SmemLayout L = SmemLayout::make(P.n_max, XBF, P.cap_w, P.cap_u, P.cap_a, P.abuf_bytes, P.bbuf_bytes);
+  const uint32_t sb = smem_base_pinned(smem);  // shared-window base: every access below is LDS/STS
+  Ctx C;
+  C.S.xs = sb + L.off_x;
+  C.S.h1 = sb + L.off_h1;
+  C.S.cand = sb + L.off_cand;
+  C.S.h2a = sb + L.off_h2;
+  C.S.h2b = C.S.h2a + 4u * 256;
+  C.S.misc = sb + L.off_misc;
+  C.list_w = sb + L.off_w;  // {channel j, bits of x_j}: W rows of this CTA in S
+  C.list_u = sb + L.off_u;  // stage-1 rows of this CTA in S^c
+  C.coef_a = sb + L.off_a;  // t_c of this CTA's A_r^T rows
+  C.red = sb + L.off_red;   // cross-group reduction scratch
+  C.obuf = sb + L.off_abuf;
+  C.obuf_bytes = P.abuf_bytes;
+  C.bar = sb + L.off_misc + 4u * M_MBAR;  // 8-byte aligned slot
+  if (threadIdx.x == 0) {
+    mbar_init_s(C.bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  C.pol = l2_evict_first_policy();
+  C.zero = static_cast<uint32_t>(P.knobs) & 0x40000000u;  // bit 30 of knobs is never set
+  const int tid = threadIdx.x, b = blockIdx.x, NB = gridDim.x;
+
+  // x-independent work first: overlaps the previous launch under PDL
+  const LinDesc d0 = P.descs ? P.descs[0] : P.one;
+  uint32_t parity = 0;
+  bool pre = !(P.knobs & 2) && preload_operands<WT>(d0, b, C);
+  sel_clear(C.S);
+  if (P.pdl) {
+    griddep_wait();
+    griddep_launch_dependents();
+  }
+  if (tid == 0) C.S.set_m(M_GEN, ld_relaxed_gpu(P.hdr));  // launch epoch (stable during the launch)
+  __syncthreads();
+  C.epoch = C.S.m(M_GEN);
+
+  LinDesc d = d0;
+  int prev_slot = -1;
+  for (int l = 0; l < P.count; ++l) {
+    // debug trace of (linear l, CTA b): [0] globaltimer at iteration start,
+    // [13] globaltimer after the dependency wait, [1..12] clock64 phases
+    long long* tr = P.trace ? P.trace + (static_cast<size_t>(l) * NB + b) * 16 : nullptr;
+    if (tr && tid == 0) tr[0] = gtimer();
+    if (prev_slot >= 0 && (d.flags & kLinWaitPrev)) {
+      // x of this linear is the output of the previous one: all CTAs' y
+      // contributions of linear l-1 must have landed
+      if (tid == 0) spin_until_count(slot_of(P, prev_slot), static_cast<unsigned>(NB));
+      __syncthreads();
+    }
+    if (tr && tid == 0) tr[13] = gtimer();
+    if (b >= d.cta0 && b < d.cta0 + d.grid) run_linear<WT, XBF>(P, d, C, tr, pre, parity);
+    if (pre) parity ^= 1u;
+    // next linear's operands towards L2 while this one drains
+    LinDesc dn = d;
+    if (l + 1 < P.count) {
+      dn = P.descs[l + 1];
+      pre = !(P.knobs & 2) && preload_operands<WT>(dn, b, C);
+    }
+    __syncthreads();  // this CTA's y contributions are issued
+    if (tid == 0) red_release_add(slot_of(P, d.slot), 1u);
+    if (tr && tid == 0) tr[14] = gtimer();
+    prev_slot = d.slot;
+    d = dn;
+  }
+
+  // Launch epilogue: the last CTA to finish resets every slot used and
+  // advances the epoch for the next launch on this workspace.
+  if (tid == 0) C.S.set_m(M_LAST, atom_add_acq_rel_gpu(P.hdr + 1, 1u) == static_cast<unsigned>(NB - 1));
+  __syncthreads();
+  if (C.S.m(M_LAST)) {
+    for (int l = 0; l < P.count; ++l) {
+      const int sl = P.descs ? P.descs[l].slot : P.one.slot;
+      if (tid < 2) slot_of(P, sl)[tid] = 0u;
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      st_relaxed_gpu(P.hdr + 1, 0u);
+      st_release_gpu(P.hdr, C.epoch + 1u);
+    }
+  }
+}
+
+size_t stack_smem_bytes(int n_max, bool x_bf16, int cap_w, int cap_u, int cap_a, int abuf_bytes, int bbuf_bytes) {
+  return SmemLayout::make(n_max, x_bf16, cap_w, cap_u, cap_a, abuf_bytes, bbuf_bytes).total;
+}
+
+cudaError_t stack_set_smem(size_t smem) {
   cudaError_t e = cudaSuccess;
   const int s = static_cast<int>(smem);
-#define RSP_SET(WT, XB)                                                                              \
-  if (e == cudaSuccess)                                                                              \
-    e = cudaFuncSetAttribute(linear_kernel<WT, XB>, cudaFuncAttributeMaxDynamicSharedMemorySize, s);
+#define RSP_SET(WT, XB)                                                                             \
+  if (e == cudaSuccess)                                                                             \
+    e = cudaFuncSetAttribute(stack_kernel<WT, XB>, cudaFuncAttributeMaxDynamicSharedMemorySize, s);
   RSP_SET(__nv_bfloat16, true)
   RSP_SET(__nv_bfloat16, false)
   RSP_SET(float, true)
@@ -417,7 +636,7 @@ cudaError_t fused_set_smem(size_t smem) {
   return e;
 }
 
-cudaError_t launch_fused(const FusedParams& p, int elem_bytes, bool x_bf16, int grid, size_t smem,
+cudaError_t launch_stack(const StackParams& p, int elem_bytes, bool x_bf16, int grid, size_t smem,
                          cudaStream_t stream, bool pdl) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -429,13 +648,13 @@ cudaError_t launch_fused(const FusedParams& p, int elem_bytes, bool x_bf16, int 
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  FusedParams q = p;
+  StackParams q = p;
   q.pdl = pdl ? 1 : 0;
   if (elem_bytes == 2)
-    return x_bf16 ? cudaLaunchKernelEx(&cfg, linear_kernel<__nv_bfloat16, true>, q)
-                  : cudaLaunchKernelEx(&cfg, linear_kernel<__nv_bfloat16, false>, q);
-  return x_bf16 ? cudaLaunchKernelEx(&cfg, linear_kernel<float, true>, q)
-                : cudaLaunchKernelEx(&cfg, linear_kernel<float, false>, q);
+    return x_bf16 ? cudaLaunchKernelEx(&cfg, stack_kernel<__nv_bfloat16, true>, q)
+                  : cudaLaunchKernelEx(&cfg, stack_kernel<__nv_bfloat16, false>, q);
+  return x_bf16 ? cudaLaunchKernelEx(&cfg, stack_kernel<float, true>, q)
+                : cudaLaunchKernelEx(&cfg, stack_kernel<float, false>, q);
 }
 
 // ---------------------------------------------------------------------------

@@ -48,7 +48,8 @@ enum : int {
   M_SCAN = 0,  // [0, 16): block-scan scratch
   M_BIN = 16, M_ABOVE = 17, M_CNT = 18, M_T = 19, M_JLIM = 20, M_GEN = 21, M_LAST = 22,
   M_RCNT = 64,   // [64, 80): per-warp gathered member counts
-  M_WSUM = 80,   // [80, 96): per-warp level-1 bin totals
+  M_WSUM = 80,   // [80, 88): per-warp level-1 bin totals (kWarps <= 8)
+  M_MBAR = 88,   // [88, 90): the stack kernel's operand mbarrier (8-byte aligned)
   M_LISTA = 32,  // [32, 48): per-warp member counts, list A
   M_LISTB = 48,  // [48, 64): per-warp member counts, list B
 };
@@ -288,15 +289,24 @@ __device__ __noinline__ Cut sel_cut(int n, int k, SelArea s) {
   if (k >= n) return Cut{0u, INT_MAX};
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t kk = static_cast<uint32_t>(k);
-  // ---- level-1 boundary bin.  Warp w owns bins [4096-256(w+1), 4096-256w),
-  // lane l the 8 bins below 4096-256w-8l; both in descending order.
+  // ---- level-1 boundary bin.  Thread t owns kPB bins, descending from the
+  // top: bins [kBins - kPB (t+1), kBins - kPB t).  Per-warp totals (redux)
+  // locate the warp, then the owning warp scans its lanes.
   {
-    const uint32_t h = s.h1 + 4u * static_cast<uint32_t>(kBins - 256 * (warp + 1) + 8 * (31 - lane));
-    const uint4 lo = lds4(h), hi = lds4(h + 16u);
-    const uint32_t c[8] = {hi.w, hi.z, hi.y, hi.x, lo.w, lo.z, lo.y, lo.x};
+    constexpr int kPB = kBins / kThreads;
+    const uint32_t h = s.h1 + 4u * static_cast<uint32_t>(kBins - kPB * (tid + 1));
+    uint32_t c[kPB];
+#pragma unroll
+    for (int q4 = 0; q4 < kPB / 4; ++q4) {
+      const uint4 u = lds4(h + 16u * (kPB / 4 - 1 - q4));
+      c[4 * q4 + 0] = u.w;
+      c[4 * q4 + 1] = u.z;
+      c[4 * q4 + 2] = u.y;
+      c[4 * q4 + 3] = u.x;
+    }
     uint32_t local = 0;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) local += c[q];
+    for (int q = 0; q < kPB; ++q) local += c[q];
     const uint32_t wsum = __reduce_add_sync(0xffffffffu, local);
     if (lane == 0) s.set_m(M_WSUM + warp, wsum);
     __syncthreads();
@@ -320,9 +330,9 @@ __device__ __noinline__ Cut sel_cut(int n, int k, SelArea s) {
       uint32_t acc = wabove + li - local;
       if (acc < kk && kk <= acc + local) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < kPB; ++q) {
           if (acc < kk && kk <= acc + c[q]) {
-            s.set_m(M_BIN, static_cast<uint32_t>(kBins - 1 - 256 * warp - 8 * lane - q));
+            s.set_m(M_BIN, static_cast<uint32_t>(kBins - 1 - kPB * tid - q));
             s.set_m(M_ABOVE, acc);
             s.set_m(M_CNT, c[q]);
           }

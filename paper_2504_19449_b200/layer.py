@@ -418,19 +418,31 @@ class Recipe:
 
 
 class Stack:
-    """A decode-order sequence of forwards captured once into a CUDA graph."""
+    """A decode-order sequence of forwards run by one persistent kernel launch
+    (captured once into a CUDA graph; rsp_stack_create_ex).
 
-    def __init__(self, layers: List[DecomposedLayer], xs, ys, dense: bool = False):
+    ``wait_prev[i]`` (default all True) says linear i's input depends on
+    linear i-1's output, so it starts only once that output is complete.
+    Linears that share the previous linear's input (q/k/v, gate/up) pass False
+    and overlap with it."""
+
+    def __init__(self, layers: List[DecomposedLayer], xs, ys, dense: bool = False,
+                 wait_prev: Optional[Sequence[bool]] = None):
         self.layers = layers
         self.xs, self.ys = xs, ys
         n = len(layers)
         hp = (ct.c_void_p * n)(*[l.handle.value for l in layers])
         xp = (ct.c_void_p * n)(*[x.data_ptr() for x in xs])
         yp = (ct.c_void_p * n)(*[y.data_ptr() for y in ys])
+        wp = None
+        if wait_prev is not None:
+            if len(wait_prev) != n:
+                raise L.UsageError(L.RSP_E_USAGE, "wait_prev length differs from the layer count")
+            wp = (ct.c_uint8 * n)(*[1 if w else 0 for w in wait_prev])
         h = ct.c_void_p()
         torch.cuda.synchronize()
-        check(L.lib().rsp_stack_create(hp, n, xp, _x_dtype(xs[0]), yp, 1 if dense else 0, ct.byref(h)),
-              "rsp_stack_create")
+        check(L.lib().rsp_stack_create_ex(hp, n, xp, _x_dtype(xs[0]), yp, 1 if dense else 0, wp, ct.byref(h)),
+              "rsp_stack_create_ex")
         self._h = h
 
     def launch(self, stream=None) -> None:

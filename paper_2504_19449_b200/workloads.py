@@ -36,6 +36,32 @@ LLAMA3_8B = [
 ]
 N_LAYERS = 32
 
+# Which input each decoder-layer linear reads (model.cpp:159-242 decode
+# order): q/k/v share the normed hidden state, o reads the attention
+# context, gate/up share the post-attention normed state, down reads
+# up * SiLU(gate).  A linear that starts a new input group depends on the
+# previous linear's output in a real decode (wait_prev); the others may
+# overlap with the linear before them.
+INPUT_GROUP = {"q_proj": "attn_in", "k_proj": "attn_in", "v_proj": "attn_in", "o_proj": "attn_out",
+               "gate_proj": "mlp_in", "up_proj": "mlp_in", "down_proj": "mlp_act"}
+
+
+def input_groups(plans):
+    """[(group index per linear)], [wait_prev per linear]: consecutive linears
+    of one decoder layer reading the same input share one activation vector."""
+    gid, wait, last = [], [], None
+    for (name, *_rest) in plans:
+        layer, short = name.rsplit(".", 1) if "." in name else ("", name)
+        key = (layer, INPUT_GROUP.get(short, short))
+        if key != last:
+            gid.append(gid[-1] + 1 if gid else 0)
+            wait.append(True)
+            last = key
+        else:
+            gid.append(gid[-1])
+            wait.append(False)
+    return gid, wait
+
 
 def heavy_tailed_x(n: int, rng: np.random.Generator, outliers: int = 8, scale: float = 20.0) -> np.ndarray:
     """Laplace(0,1) * LogNormal(0,1) with `outliers` channels x`scale` (float32)."""

@@ -304,20 +304,58 @@ def test_io_cost_gpu(golden, cuda):
         assert rep.dense_bytes == int(db) and rep.touched_bytes == int(tb) and rep.relative_cost == rc
 
 
-def test_stack_graph_matches_individual_forwards(cuda):
+@pytest.mark.parametrize("grouped", [False, True])
+def test_stack_graph_matches_individual_forwards(cuda, grouped):
+    # one persistent launch over a decoder layer's 7 linears; grouped: q/k/v
+    # and gate/up share one input and overlap (wait_prev False)
     rng = np.random.default_rng(9)
     layers, xs = [], []
-    for (name, m, n) in wl.LLAMA2_7B:
+    plans = [(f"layers.0.{name}", m, n, 0.0, 64) for (name, m, n) in wl.LLAMA2_7B]
+    gid, wait = wl.input_groups(plans)
+    xg = {}
+    for i, (name, m, n) in enumerate(wl.LLAMA2_7B):
         w = torch.randn(m, n, device=cuda) * 0.02
         r = 64
         a = torch.randn(m, r, device=cuda) * 0.1
         b = torch.randn(r, n, device=cuda) * 0.1
         layers.append(rsp.DecomposedLayer(w, a, b, rsp.SparsityPlan(float(rng.uniform(0.15, 0.35)), r)))
-        xs.append(torch.from_numpy(wl.heavy_tailed_x(n, rng)).to(cuda).to(torch.bfloat16))
+        key = gid[i] if grouped else i
+        if key not in xg:
+            xg[key] = torch.from_numpy(wl.heavy_tailed_x(n, rng)).to(cuda).to(torch.bfloat16)
+        xs.append(xg[key])
     ys = [torch.empty(l.m_out, device=cuda) for l in layers]
-    st = rsp.Stack(layers, xs, ys)
+    st = rsp.Stack(layers, xs, ys, wait_prev=wait if grouped else None)
     for _ in range(3):
         st.launch()
     torch.cuda.synchronize()
     for l, x, y in zip(layers, xs, ys):
         assert maxrel(y.cpu().numpy(), l.forward(x).cpu().numpy()) <= 1e-6
+    # dense stack == dense forward of each layer
+    yd = [torch.empty(l.m_out, device=cuda) for l in layers]
+    sd = rsp.Stack(layers, xs, yd, dense=True, wait_prev=wait if grouped else None)
+    sd.launch()
+    torch.cuda.synchronize()
+    for l, x, y in zip(layers, xs, yd):
+        assert maxrel(y.cpu().numpy(), l.dense_forward(x).cpu().numpy()) <= 1e-6
+
+
+def test_stack_deterministic_bit_reproducible(cuda):
+    rng = np.random.default_rng(10)
+    layers, xs = [], []
+    for (name, m, n) in wl.LLAMA2_7B[:4]:
+        w = torch.randn(m, n, device=cuda) * 0.02
+        a = torch.randn(m, 64, device=cuda) * 0.1
+        b = torch.randn(64, n, device=cuda) * 0.1
+        layers.append(rsp.DecomposedLayer(w, a, b, rsp.SparsityPlan(0.25, 64), deterministic=True))
+        xs.append(torch.from_numpy(wl.heavy_tailed_x(n, rng)).to(cuda).to(torch.bfloat16))
+    ys = [torch.empty(l.m_out, device=cuda) for l in layers]
+    st = rsp.Stack(layers, xs, ys, wait_prev=[True, False, False, True])
+    outs = []
+    for _ in range(3):
+        st.launch()
+        torch.cuda.synchronize()
+        outs.append([y.clone() for y in ys])
+    for o in outs[1:]:
+        assert all(torch.equal(a, b) for a, b in zip(outs[0], o))
+    for l, x, y in zip(layers, xs, ys):
+        assert torch.equal(y, l.forward(x))

@@ -18,7 +18,8 @@ import paper_2504_19449_b200 as rsp  # noqa: E402
 from paper_2504_19449_b200 import _lib as L  # noqa: E402
 from paper_2504_19449_b200 import workloads as wl  # noqa: E402
 
-EV = {1: "after_griddep", 2: "x_loaded+hist", 3: "cut", 4: "lists", 5: "stage1+arrive",
+EV = {1: "after_griddep", 2: "x_loaded+hist", 3: "cut", 4: "lists", 10: "W_prefetch_issued",
+      11: "stage1_rows", 12: "t_reds", 5: "stage1+arrive",
       6: "W_rows_done", 7: "barrier_waited", 8: "A_rows_done", 9: "end"}
 SHAPES = {"q": (4096, 4096), "gate": (11008, 4096), "down": (4096, 11008)}
 
