@@ -9,10 +9,14 @@ per-linear (s, r) from Recipe::plan_for with rho ~ U(0.3, 0.7), C = 0.5
 weights (no checkpoints offline); heavy-tailed synthetic activations
 (Laplace x LogNormal, 8 outliers x20; SiLU(g)*u for down_proj).
 
-One step = one decode token through all 224 linears in order (CUDA graph of
-224 fused kernels).  The resident operands (~16 GB) dwarf the 126 MB L2, so
-no flush is needed between steps.  N > 1: every linear is row-sharded over
-the ranks and followed by one NCCL all-gather of y.
+One step = one decode token through all 224 linears in decode order: ONE
+persistent stack-kernel launch (CUDA graph) with a grid barrier wherever a
+linear's input is the previous output; q/k/v (and gate/up), which read the
+same activation in a Llama decoder layer, run side by side on disjoint CTA
+partitions (workloads.input_groups).  The resident operands (~16 GB) dwarf
+the 126 MB L2, so no flush is needed between steps.  N > 1: every linear is
+row-sharded over the ranks and followed by one NCCL all-gather of y
+(SURVEY §8(e)).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 """
@@ -327,7 +331,8 @@ def run_ours(args):
         "higher_is_better": False, "scaling": "weak" if world == 1 else "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": "config2: 32-layer Llama-2-7B-shaped R-Sparse linear stack, batch 1, "
-                               "50% model-level sparsity (rho~U(0.3,0.7), C=0.5), bf16 W/x, fp32 accum",
+                               "50% model-level sparsity (rho~U(0.3,0.7), C=0.5), bf16 W/x, fp32 accum; "
+                               "q/k/v and gate/up share one input (decoder-layer dataflow)",
                    "global_batch": 1, "layers": args.layers, "linears": len(layers),
                    "parallelism": f"row-shard{world}" + ("+allgather" if world > 1 else ""),
                    "l2": "no flush: 16 GB resident operands >> 126 MB L2",
@@ -335,10 +340,10 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": load_traffic(),
                      "peak_kind": peak_kind, "algorithmic_bytes_per_step": bytes_step,
-                     "kernel": "fused_forward_kernel<bf16> (224 launches/step)"},
+                     "kernel": "stack_kernel<bf16,bf16> (1 persistent launch/step, 224 linears)"},
         "e2e": {"value": e2e_ms * 1e3, "unit": "us/token", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
-        "gpu_launches": args.steps * len(layers),
+        "gpu_launches": args.steps * (1 if world == 1 else len(layers)),
         "clocks": clocks.summary(),
     }
     out.update(extras)
