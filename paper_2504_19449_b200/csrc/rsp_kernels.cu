@@ -295,6 +295,30 @@ __device__ __forceinline__ Acc stream_list_smem(uint32_t list, int first, int co
   return r;
 }
 
+// x-independent per-linear setup of CTA bg, done in the previous linear's
+// tail (off the critical path): zero its slice of y (split-K reductions land
+// there after the t barrier, which orders them after this) and of the next
+// launch's t buffer, and the selection histograms.
+template <typename WT>
+__device__ __forceinline__ void prep_linear(const StackParams& P, const LinDesc& d, int bg, const Ctx& C) {
+  const int b = bg - d.cta0, NB = d.grid, tid = threadIdx.x;
+  if (b < 0 || b >= NB) return;
+  const bool dense = (d.flags & kLinDense) != 0;
+  const bool has_lr = !dense && d.r > 0 && d.k < d.n;
+  const bool det = P.deterministic != 0;
+  const int KS = d.k_splits;
+  if (has_lr || (KS > 1 && !det)) {
+    if (KS > 1 && !det) {
+      const int y0 = part(d.m, b, NB), y1 = part(d.m, b + 1, NB);
+      for (int i = y0 + tid; i < y1; i += kThreads) d.y[i] = 0.f;
+    }
+    float* t_nxt = P.t_acc + (static_cast<size_t>(d.slot) * 2 + ((C.epoch + 1u) & 1u)) * kTAccCap;
+    const int c0 = part(static_cast<int>(kTAccCap), b, NB), c1 = part(static_cast<int>(kTAccCap), b + 1, NB);
+    for (int c = c0 + tid; c < c1; c += kThreads) t_nxt[c] = 0.f;
+  }
+  if (!dense) sel_clear(C.S);
+}
+
 // One linear, CTA b < d.grid.  Ends with this CTA's contribution to y issued.
 template <typename WT, bool XBF>
 __device__ __forceinline__ void run_linear(const StackParams& P, const LinDesc& d, const Ctx& C,
@@ -323,9 +347,8 @@ __device__ __forceinline__ void run_linear(const StackParams& P, const LinDesc& 
   const bool has_lr = !dense && d.r > 0 && k_eff < d.n;
   const bool det = P.deterministic != 0;
   const bool use_bar = has_lr || (KS > 1 && !det);
-  // Static channel ranges: W rows in [wc0, wc1), stage-1 rows in [uc0, uc1),
-  // A_r^T rows [alo, ahi).
-  const int wc0 = part(d.n, ks, KS), wc1 = part(d.n, ks + 1, KS);
+  // Static ranges: stage-1 rows in channel slice [uc0, uc1), A_r^T rows
+  // [alo, ahi); W rows are split by rank in S below.
   const int uc0 = has_lr ? part(d.n, b, NB) : 0, uc1 = has_lr ? part(d.n, b + 1, NB) : 0;
   const int alo = has_lr ? part(d.r, ks, KS) : 0, ahi = has_lr ? part(d.r, ks + 1, KS) : 0;
   const int na = ahi - alo;
@@ -339,19 +362,8 @@ __device__ __forceinline__ void run_linear(const StackParams& P, const LinDesc& 
   const uint8_t* a_tile = At + static_cast<size_t>(col0) * ES;
   unsigned* slot = slot_of(P, d.slot);
   float* t_cur = P.t_acc + (static_cast<size_t>(d.slot) * 2 + (C.epoch & 1u)) * kTAccCap;
-  float* t_nxt = P.t_acc + (static_cast<size_t>(d.slot) * 2 + ((C.epoch + 1u) & 1u)) * kTAccCap;
 
-  if (use_bar) {
-    if (KS > 1 && !det) {  // zero this CTA's slice of y; published by the barrier below
-      const int y0 = part(d.m, b, NB), y1 = part(d.m, b + 1, NB);
-      for (int i = y0 + tid; i < y1; i += kThreads) d.y[i] = 0.f;
-    }
-    // zero this CTA's slice of the next launch's t buffer of this slot
-    const int c0 = part(static_cast<int>(kTAccCap), b, NB), c1 = part(static_cast<int>(kTAccCap), b + 1, NB);
-    for (int c = c0 + tid; c < c1; c += kThreads) t_nxt[c] = 0.f;
-  }
-  if (!dense) sel_clear(S);
-  __syncthreads();  // histograms zero; previous linear's shared-memory use complete
+  __syncthreads();  // prep_linear's zeroing (histograms, y slice) is complete
   RSP_TRACE(1);
 
   // ---- 1. x -> shared memory + level-1 histogram; the exact cut ----
@@ -361,12 +373,17 @@ __device__ __forceinline__ void run_linear(const StackParams& P, const LinDesc& 
   RSP_TRACE(3);
 
   // ---- 2. this CTA's row lists: W rows of S in [wc0, wc1), stage-1 rows of S^c in [uc0, uc1) ----
+  // (measured: splitting S by global rank balances the W rows exactly but the
+  // extra pass over all n costs more than the imbalance)
   int nW = 0, nU = 0;
-  compact2(
-      S, wc0, wc1, uc0, uc1, [&](int j) { return in_cut(sel_key<XBF>(S, j), j, cut); },
-      [&](int j) { return !in_cut(sel_key<XBF>(S, j), j, cut); },
-      [&](int i, int j) { sts2(C.list_w + 8u * i, static_cast<uint32_t>(j), sel_bits<XBF>(S, j)); },
-      [&](int i, int j) { sts2(C.list_u + 8u * i, static_cast<uint32_t>(j), sel_bits<XBF>(S, j)); }, &nW, &nU);
+  {
+    const int wc0 = part(d.n, ks, KS), wc1 = part(d.n, ks + 1, KS);
+    compact2(
+        S, wc0, wc1, uc0, uc1, [&](int j) { return in_cut(sel_key<XBF>(S, j), j, cut); },
+        [&](int j) { return !in_cut(sel_key<XBF>(S, j), j, cut); },
+        [&](int i, int j) { sts2(C.list_w + 8u * i, static_cast<uint32_t>(j), sel_bits<XBF>(S, j)); },
+        [&](int i, int j) { sts2(C.list_u + 8u * i, static_cast<uint32_t>(j), sel_bits<XBF>(S, j)); }, &nW, &nU);
+  }
   RSP_TRACE(4);
   // ---- 3. stage 1: partial t over this CTA's S^c slice (B_r^T rows from the
   // shared-memory slice preloaded while the previous linear drained) ----
@@ -396,8 +413,8 @@ __device__ __forceinline__ void run_linear(const StackParams& P, const LinDesc& 
     RSP_TRACE(12);
   }
   if (use_bar) {
-    __syncthreads();  // this CTA's t contributions and y zeroing are issued; `red` is free again
-    if (tid == 0) red_release_add(slot + 1, 1u);
+    if (has_lr) __syncthreads();  // this CTA's t contributions are issued; `red` is free again
+    if (tid == 0) red_release_add(slot + 1, 1u);  // (y slice zeroed in prep, published at run start)
   }
   RSP_TRACE(5);
 
@@ -570,6 +587,7 @@ __global__ void __launch_bounds__(kThreads, 1) stack_kernel(const StackParams P)
   if (tid == 0) C.S.set_m(M_GEN, ld_relaxed_gpu(P.hdr));  // launch epoch (stable during the launch)
   __syncthreads();
   C.epoch = C.S.m(M_GEN);
+  prep_linear<WT>(P, d0, b, C);
 
   LinDesc d = d0;
   int prev_slot = -1;
@@ -593,8 +611,9 @@ __global__ void __launch_bounds__(kThreads, 1) stack_kernel(const StackParams P)
       dn = P.descs[l + 1];
       pre = !(P.knobs & 2) && preload_operands<WT>(dn, b, C);
     }
-    __syncthreads();  // this CTA's y contributions are issued
+    __syncthreads();  // this CTA's y contributions are issued; shared memory is free
     if (tid == 0) red_release_add(slot_of(P, d.slot), 1u);
+    if (l + 1 < P.count) prep_linear<WT>(P, dn, b, C);
     if (tr && tid == 0) tr[14] = gtimer();
     prev_slot = d.slot;
     d = dn;

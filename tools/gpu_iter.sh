@@ -7,7 +7,7 @@ echo "pytest exit $?" >> gpurun_out/pytest_gpu_$TAG.log
 timeout 300 python tools/stack_trace.py --layers 1 > gpurun_out/stack_trace_$TAG.txt 2>&1
 out=gpurun_out/variants_$TAG.txt
 : > $out
-for v in "" "RSP_KNOBS=2" "RSP_NO_SMEM_OPS=1"; do
+for v in "" "RSP_SMEM_OPS=1"; do
   echo "== $v" >> $out
   env $v timeout 300 python bench.py --no-cpu --steps 10 --warmup 3 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value'],1), 'us/token', round(d['roofline']['frac'],3), 'cublas', round(d.get('dense_cublas_us_per_token',0),1), 'inhouse-dense', round(d.get('dense_inhouse_us_per_token',0),1))" >> $out 2>&1
 done
