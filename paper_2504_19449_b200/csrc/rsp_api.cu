@@ -185,17 +185,22 @@ rsp_status make_plan(const rsp_linear& L, const DevProps& dp, LaunchPlan* out, i
   const int ks_cap = std::max(1, env_int("RSP_MAX_KSPLITS", 32));
   int best_nt = 1, best_ks = 1;
   double best = 1e30;
+  // with a low-rank term, prefer tiles of at most 4 warp columns: that leaves
+  // room for a stage-1 warp group beside the W warps (warp-specialised path)
+  const int c2_pref = (L.rank > 0 && L.k < n) ? 4 : 8;
   for (int c2 = 1; c2 <= 8; c2 *= 2) {  // <= one row of warps (kThreads / 32 = 8)
     const int nt = (wcols + c2 - 1) / c2;
     if (nt > sms || nt > static_cast<int>(rsp::kMaxTickets)) continue;
     const int ks = std::min(sms / nt, ks_cap);
-    const double cost = static_cast<double>(c2) / ks;
+    const double cost = static_cast<double>(c2) / ks * (c2 > c2_pref ? 1.25 : 1.0);
     if (cost < best * 0.99 || (cost <= best * 1.01 && ks <= 24)) {
       best = std::min(best, cost);
       best_nt = nt;
       best_ks = ks;
     }
   }
+  if (best > 1e29 || (wcols + best_nt - 1) / best_nt > 8)
+    return fail(RSP_E_UNSUPPORTED, "no column tiling for m_out %u (%d warp columns)", L.m, wcols);
   int nt = best_nt, ks = best_ks;
   // Small layers: keep >= ~32 KB of streamed bytes per CTA.
   const double bytes = static_cast<double>(L.k + L.rank) * vrow * 16.0 +

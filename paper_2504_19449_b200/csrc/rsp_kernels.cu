@@ -54,7 +54,7 @@ constexpr int kRedFloats = 4096;    // 16 KB cross-group reduction scratch
 // level-1 histogram is dead once the cut is known, so the cross-group
 // reduction scratch reuses it.
 struct SmemLayout {
-  uint32_t off_h1, off_cand, off_h2, off_misc, off_red, off_w, off_u, off_a, off_x, off_abuf, off_bbuf, total;
+  uint32_t off_h1, off_cand, off_h2, off_misc, off_red, off_w, off_u, off_a, off_x, off_abuf, off_bbuf, off_h16, total;
 
   __host__ __device__ static uint32_t up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
 
@@ -83,6 +83,8 @@ struct SmemLayout {
     o = up(o + static_cast<uint32_t>(abuf), 16);
     L.off_bbuf = o;
     o = up(o + static_cast<uint32_t>(bbuf), 16);
+    L.off_h16 = o;  // bf16 activations: 15-bit key histogram
+    o += 4u * kH16Words;
     L.total = up(o, 128);
     return L;
   }
@@ -174,6 +176,17 @@ __device__ __forceinline__ Acc stream_seq(uint32_t coef, int first, int count, i
 #pragma unroll
   for (int e = 0; e < 8; ++e) r.v[e] = e < Vec<WT>::kElems ? acc[e] : 0.f;
   return r;
+}
+
+// Store a lane's VE partial sums (consecutive floats) with 16-byte stores:
+// scalar stores with a 32-byte lane stride would conflict 8 ways.
+template <int VE>
+__device__ __forceinline__ void sts_acc(uint32_t a, const Acc& x) {
+  sts4(a, make_uint4(__float_as_uint(x.v[0]), __float_as_uint(x.v[1]), __float_as_uint(x.v[2]),
+                     __float_as_uint(x.v[3])));
+  if constexpr (VE == 8)
+    sts4(a + 16u, make_uint4(__float_as_uint(x.v[4]), __float_as_uint(x.v[5]), __float_as_uint(x.v[6]),
+                             __float_as_uint(x.v[7])));
 }
 
 // floor(total * i / parts) in 32-bit arithmetic (total * parts < 2^32 for every
@@ -283,10 +296,17 @@ __device__ __forceinline__ Acc stream_list_smem(uint32_t list, int first, int co
 #pragma unroll
   for (int e = 0; e < Vec<WT>::kElems; ++e) acc[e] = 0.f;
   if (lane_ok) {
-#pragma unroll 4
-    for (int i = first; i < count; i += stride) {
-      const uint2 e = lds2(list + 8u * static_cast<uint32_t>(i));
-      Vec<WT>::fma(acc, lds4(sbase + (e.x - static_cast<uint32_t>(uc0)) * row_bytes), __uint_as_float(e.y));
+    constexpr int kB = 8;  // rows per batch: list reads, then row reads, then FMAs
+    for (int i0 = first; i0 < count; i0 += stride * kB) {
+      uint2 e[kB];
+#pragma unroll
+      for (int q = 0; q < kB; ++q) e[q] = lds2(list + 8u * static_cast<uint32_t>(min(i0 + q * stride, count - 1)));
+      uint4 u[kB];
+#pragma unroll
+      for (int q = 0; q < kB; ++q) u[q] = lds4(sbase + (e[q].x - static_cast<uint32_t>(uc0)) * row_bytes);
+#pragma unroll
+      for (int q = 0; q < kB; ++q)
+        Vec<WT>::fma(acc, u[q], i0 + q * stride < count ? __uint_as_float(e[q].y) : 0.f);
     }
   }
   Acc r;
@@ -299,7 +319,7 @@ __device__ __forceinline__ Acc stream_list_smem(uint32_t list, int first, int co
 // tail (off the critical path): zero its slice of y (split-K reductions land
 // there after the t barrier, which orders them after this) and of the next
 // launch's t buffer, and the selection histograms.
-template <typename WT>
+template <typename WT, bool XBF>
 __device__ __forceinline__ void prep_linear(const StackParams& P, const LinDesc& d, int bg, const Ctx& C) {
   const int b = bg - d.cta0, NB = d.grid, tid = threadIdx.x;
   if (b < 0 || b >= NB) return;
@@ -316,7 +336,10 @@ __device__ __forceinline__ void prep_linear(const StackParams& P, const LinDesc&
     const int c0 = part(static_cast<int>(kTAccCap), b, NB), c1 = part(static_cast<int>(kTAccCap), b + 1, NB);
     for (int c = c0 + tid; c < c1; c += kThreads) t_nxt[c] = 0.f;
   }
-  if (!dense) sel_clear(C.S);
+  if (!dense) {
+    if (XBF) sel_clear16(C.S);
+    else sel_clear(C.S);
+  }
 }
 
 // One linear, CTA b < d.grid.  Ends with this CTA's contribution to y issued.
@@ -367,9 +390,17 @@ __device__ __forceinline__ void run_linear(const StackParams& P, const LinDesc& 
   RSP_TRACE(1);
 
   // ---- 1. x -> shared memory + level-1 histogram; the exact cut ----
-  sel_load<XBF>(d.x, d.n, S, !dense);
-  RSP_TRACE(2);
-  const Cut cut = dense ? Cut{0u, INT_MAX} : sel_cut<XBF>(d.n, d.k, S);
+  Cut cut{0u, INT_MAX};
+  if constexpr (XBF) {
+    if (dense) sel_load<true>(d.x, d.n, S, false);
+    else sel_load16(d.x, d.n, S);
+    RSP_TRACE(2);
+    if (!dense) cut = sel_cut16(d.n, d.k, S);
+  } else {
+    sel_load<false>(d.x, d.n, S, !dense);
+    RSP_TRACE(2);
+    if (!dense) cut = sel_cut<false>(d.n, d.k, S);
+  }
   RSP_TRACE(3);
 
   // ---- 2. this CTA's row lists: W rows of S in [wc0, wc1), stage-1 rows of S^c in [uc0, uc1) ----
@@ -385,22 +416,50 @@ __device__ __forceinline__ void run_linear(const StackParams& P, const LinDesc& 
         [&](int i, int j) { sts2(C.list_u + 8u * i, static_cast<uint32_t>(j), sel_bits<XBF>(S, j)); }, &nW, &nU);
   }
   RSP_TRACE(4);
-  // ---- 3. stage 1: partial t over this CTA's S^c slice (B_r^T rows from the
-  // shared-memory slice preloaded while the previous linear drained) ----
+  // ---- 3+4. stage 1 and the W rows ----
+  // With the B_r^T slice resident in shared memory, stage 1 needs no HBM: a
+  // group of C1 warps runs it (and the t hand-off and the arrive) while the
+  // other warps stream W.  Otherwise all warps run stage 1 first.
+  const int vb = d.r_pad * ES / 16;  // 16-B units per B_r^T row
+  const int C1 = max((vb + 31) / 32, 1);
+  const int C2 = max((tw + 31) / 32, 1);
+  const bool spec = !(P.knobs & 8) && has_lr && os.b_smem && C1 < kWarps && C2 <= kWarps - C1;
+  const int WS = spec ? C1 : 0;                // stage-1 warps [0, WS)
+  const int nWW = kWarps - WS;                 // W warps
+  const int wwarp = warp - WS;
+  const int G2 = nWW / C2, g2 = wwarp >= 0 ? wwarp / C2 : G2;
+  const int v = (wwarp >= 0 ? wwarp % C2 : 0) * 32 + lane;
+  const bool ok2 = wwarp >= 0 && g2 < G2 && v < tw;
   if (has_lr) {
-    const int vb = d.r_pad * ES / 16;  // 16-B units per B_r^T row
-    const int C1 = (vb + 31) / 32, G1 = kWarps / C1, g1 = warp / C1;
-    const int v1 = (warp % C1) * 32 + lane;
-    const bool ok = g1 < G1 && v1 < vb;
     if (preloaded) mbar_wait_s(C.bar, parity);  // the operand bulk copies have landed
     RSP_TRACE(10);
+  }
+  if (spec) {
+    if (warp < WS) {
+      const int v1 = warp * 32 + lane;
+      const Acc a1 = stream_list_smem<WT>(C.list_u, 0, nU, 1, v1 < vb, C.obuf + v1 * 16u, uc0, rowB);
+      RSP_TRACE(11);
+      if (v1 < vb) sts_acc<VE>(C.red + 4u * (v1 * VE), a1);
+      named_bar_sync(1, WS * 32);
+      for (int c = tid; c < d.r_pad; c += WS * 32) {
+        const float sum = ldsf(C.red + 4u * c);
+        if (det)
+          P.t_part[static_cast<size_t>(c) * P.nb_pad + b] = sum;
+        else if (sum != 0.f)
+          red_add_f32(t_cur + c, sum);
+      }
+      named_bar_sync(1, WS * 32);  // the group's t contributions are issued
+      if (tid == 0) red_release_add(slot + 1, 1u);
+      RSP_TRACE(12);
+    }
+  } else if (has_lr) {
+    const int G1 = kWarps / C1, g1 = warp / C1;
+    const int v1 = (warp % C1) * 32 + lane;
+    const bool ok = g1 < G1 && v1 < vb;
     const Acc a1 = os.b_smem ? stream_list_smem<WT>(C.list_u, g1, nU, G1, ok, C.obuf + v1 * 16u, uc0, rowB)
                              : stream_list<WT>(C.list_u, g1, nU, G1, ok, Bt + v1 * 16, rowB, C.pol, C.zero);
     RSP_TRACE(11);
-    if (ok) {
-#pragma unroll
-      for (int e = 0; e < VE; ++e) stsf(C.red + 4u * (g1 * d.r_pad + v1 * VE + e), a1.v[e]);
-    }
+    if (ok) sts_acc<VE>(C.red + 4u * (g1 * d.r_pad + v1 * VE), a1);
     __syncthreads();
     for (int c = tid; c < d.r_pad; c += kThreads) {
       float sum = 0.f;
@@ -411,30 +470,31 @@ __device__ __forceinline__ void run_linear(const StackParams& P, const LinDesc& 
         red_add_f32(t_cur + c, sum);
     }
     RSP_TRACE(12);
-  }
-  if (use_bar) {
-    if (has_lr) __syncthreads();  // this CTA's t contributions are issued; `red` is free again
+    __syncthreads();  // this CTA's t contributions are issued; `red` is free again
+    if (tid == 0) red_release_add(slot + 1, 1u);
+  } else if (use_bar) {
     if (tid == 0) red_release_add(slot + 1, 1u);  // (y slice zeroed in prep, published at run start)
   }
   RSP_TRACE(5);
 
-  // ---- 4. W rows of S (HBM): all warps; the t barrier completes meanwhile ----
-  const int C2 = max((tw + 31) / 32, 1), G2 = kWarps / C2, g2 = warp / C2;
-  const int v = (warp % C2) * 32 + lane;
-  const bool ok2 = g2 < G2 && v < tw;
+  // W rows of S (HBM); the t barrier completes meanwhile
   Acc acc = stream_list<WT>(C.list_w, g2, nW, G2, ok2, Wt + static_cast<size_t>(col0) * ES + v * 16, rowW, C.pol,
                             C.zero);
   RSP_TRACE(6);
 
-  // ---- 5. stage 2: A_r^T rows [alo, ahi) (L2) ----
-  // The first batch of this warp's A rows is loaded before waiting on the
-  // barrier (A does not depend on t), so its L2 round trip overlaps the wait.
-  const uint8_t* abase = a_tile + static_cast<size_t>(alo) * rowW + v * 16;
+  // ---- 5. stage 2: A_r^T rows [alo, ahi), all warps (tile mapping gA/vA;
+  // equal to the W mapping unless a stage-1 warp group was split off) ----
+  // The first batch of a warp's A rows is loaded before waiting on the
+  // barrier (A does not depend on t), so its round trip overlaps the wait.
+  const int GA = kWarps / C2, gA = warp / C2;
+  const int vA = (warp % C2) * 32 + lane;
+  const bool okA = gA < GA && vA < tw;
+  const uint8_t* abase = a_tile + static_cast<size_t>(alo) * rowW + vA * 16;
   uint4 ua[kUA];
-  if (has_lr && ok2) {
+  if (has_lr && okA) {
 #pragma unroll
     for (int q = 0; q < kUA; ++q) {  // first global batch (rows past the shared-memory ones)
-      const int i = min(os.na_s + g2 + q * G2, max(na - 1, 0));
+      const int i = min(os.na_s + gA + q * GA, max(na - 1, 0));
       ua[q] = ldg_stream_ef(abase + static_cast<size_t>(i) * rowW, C.pol);
     }
   }
@@ -443,6 +503,9 @@ __device__ __forceinline__ void run_linear(const StackParams& P, const LinDesc& 
     __syncthreads();
   }
   RSP_TRACE(7);
+  Acc accA;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) accA.v[e] = 0.f;
   if (has_lr) {
     if (!det) {
       for (int i = tid; i < na; i += kThreads) stsf(C.coef_a + 4u * i, __ldcg(t_cur + alo + i));
@@ -467,42 +530,47 @@ __device__ __forceinline__ void run_linear(const StackParams& P, const LinDesc& 
       }
     }
     __syncthreads();
-    if (ok2) {
+    if (okA) {
       float acc8[Vec<WT>::kElems];
 #pragma unroll
-      for (int e = 0; e < VE; ++e) acc8[e] = acc.v[e];
+      for (int e = 0; e < VE; ++e) acc8[e] = 0.f;
       // shared-memory rows
       const uint32_t a_s = C.obuf + os.a_off(uc1 - uc0, static_cast<int>(rowB));
 #pragma unroll 4
-      for (int i = g2; i < os.na_s; i += G2)
-        Vec<WT>::fma(acc8, lds4(a_s + (static_cast<uint32_t>(i) * tw + v) * 16u), ldsf(C.coef_a + 4u * i));
+      for (int i = gA; i < os.na_s; i += GA)
+        Vec<WT>::fma(acc8, lds4(a_s + (static_cast<uint32_t>(i) * tw + vA) * 16u), ldsf(C.coef_a + 4u * i));
       // the early global batch
 #pragma unroll
       for (int q = 0; q < kUA; ++q) {
-        const int i = os.na_s + g2 + q * G2;
+        const int i = os.na_s + gA + q * GA;
         Vec<WT>::fma(acc8, ua[q], i < na ? ldsf(C.coef_a + 4u * i) : 0.f);
       }
 #pragma unroll
-      for (int e = 0; e < VE; ++e) acc.v[e] = acc8[e];
+      for (int e = 0; e < VE; ++e) accA.v[e] = acc8[e];
     }
-    const Acc a2 = stream_seq<WT>(C.coef_a, os.na_s + g2 + kUA * G2, na, G2, ok2, abase, rowW, C.pol, C.zero);
+    const Acc a2 = stream_seq<WT>(C.coef_a, os.na_s + gA + kUA * GA, na, GA, okA, abase, rowW, C.pol, C.zero);
 #pragma unroll
-    for (int e = 0; e < VE; ++e) acc.v[e] += a2.v[e];
+    for (int e = 0; e < VE; ++e) accA.v[e] += a2.v[e];
   }
   RSP_TRACE(8);
 
-  // ---- 6. cross-group reduction, then y ----
+  // ---- 6. cross-group reduction, then y: W groups [0, G2), A groups
+  // [G2, G2 + GA) when the mappings differ ----
   const int gstride = C2 * 32 * VE;  // floats per group in `red`
-  if (ok2) {
+  const bool sepA = WS > 0;
+  if (!sepA) {
 #pragma unroll
-    for (int e = 0; e < VE; ++e) stsf(C.red + 4u * (g2 * gstride + v * VE + e), acc.v[e]);
+    for (int e = 0; e < VE; ++e) acc.v[e] += accA.v[e];
   }
+  if (ok2) sts_acc<VE>(C.red + 4u * (g2 * gstride + v * VE), acc);
+  if (sepA && okA) sts_acc<VE>(C.red + 4u * ((G2 + gA) * gstride + vA * VE), accA);
+  const int NG = G2 + (sepA ? GA : 0);
   __syncthreads();
   const int tcw = tw * VE;  // floats in this tile (multiple of 4)
   const bool y16 = (reinterpret_cast<uintptr_t>(d.y) & 15u) == 0;
   for (int q = tid; q < tcw / 4; q += kThreads) {
     float s4[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int g = 0; g < G2; ++g) {
+    for (int g = 0; g < NG; ++g) {
       const uint4 u = lds4(C.red + 4u * (g * gstride + 4 * q));
       s4[0] += __uint_as_float(u.x);
       s4[1] += __uint_as_float(u.y);
@@ -559,6 +627,7 @@ __global__ void __launch_bounds__(kThreads, 1) stack_kernel(const StackParams P)
   C.S.h2a = sb + L.off_h2;
   C.S.h2b = C.S.h2a + 4u * 256;
   C.S.misc = sb + L.off_misc;
+  C.S.h16 = sb + L.off_h16;
   C.list_w = sb + L.off_w;  // {channel j, bits of x_j}: W rows of this CTA in S
   C.list_u = sb + L.off_u;  // stage-1 rows of this CTA in S^c
   C.coef_a = sb + L.off_a;  // t_c of this CTA's A_r^T rows
@@ -578,7 +647,7 @@ __global__ void __launch_bounds__(kThreads, 1) stack_kernel(const StackParams P)
   // x-independent work first: overlaps the previous launch under PDL
   const LinDesc d0 = P.descs ? P.descs[0] : P.one;
   uint32_t parity = 0;
-  bool pre = !(P.knobs & 2) && preload_operands<WT>(d0, b, C);
+  bool pre = !(P.knobs & 6) && preload_operands<WT>(d0, b, C);
   sel_clear(C.S);
   if (P.pdl) {
     griddep_wait();
@@ -587,7 +656,7 @@ __global__ void __launch_bounds__(kThreads, 1) stack_kernel(const StackParams P)
   if (tid == 0) C.S.set_m(M_GEN, ld_relaxed_gpu(P.hdr));  // launch epoch (stable during the launch)
   __syncthreads();
   C.epoch = C.S.m(M_GEN);
-  prep_linear<WT>(P, d0, b, C);
+  prep_linear<WT, XBF>(P, d0, b, C);
 
   LinDesc d = d0;
   int prev_slot = -1;
@@ -603,17 +672,21 @@ __global__ void __launch_bounds__(kThreads, 1) stack_kernel(const StackParams P)
       __syncthreads();
     }
     if (tr && tid == 0) tr[13] = gtimer();
+    if (P.knobs & 4) {  // preload at the linear's start: fills the HBM-idle selection window
+      __syncthreads();  // previous linear's reads of the operand buffer are complete
+      pre = preload_operands<WT>(d, b, C);
+    }
     if (b >= d.cta0 && b < d.cta0 + d.grid) run_linear<WT, XBF>(P, d, C, tr, pre, parity);
     if (pre) parity ^= 1u;
     // next linear's operands towards L2 while this one drains
     LinDesc dn = d;
     if (l + 1 < P.count) {
       dn = P.descs[l + 1];
-      pre = !(P.knobs & 2) && preload_operands<WT>(dn, b, C);
+      pre = !(P.knobs & 6) && preload_operands<WT>(dn, b, C);
     }
     __syncthreads();  // this CTA's y contributions are issued; shared memory is free
     if (tid == 0) red_release_add(slot_of(P, d.slot), 1u);
-    if (l + 1 < P.count) prep_linear<WT>(P, dn, b, C);
+    if (l + 1 < P.count) prep_linear<WT, XBF>(P, dn, b, C);
     if (tr && tid == 0) tr[14] = gtimer();
     prev_slot = d.slot;
     d = dn;
@@ -691,11 +764,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   S.h2a = S.cand + 4u * kCandWords;
   S.h2b = S.h2a + 4u * 256;
   S.misc = S.h2b + 4u * 256;
-  S.xs = S.misc + 4u * kMiscWords;
-  sel_clear(S);
-  __syncthreads();
-  sel_load<XBF>(x, n, S, true);
-  const Cut cut = sel_cut<XBF>(n, k, S);
+  S.h16 = S.misc + 4u * kMiscWords;
+  S.xs = S.h16 + 4u * kH16Words;
+  Cut cut;
+  if constexpr (XBF) {
+    sel_clear16(S);
+    __syncthreads();
+    sel_load16(x, n, S);
+    cut = sel_cut16(n, k, S);
+  } else {
+    sel_clear(S);
+    __syncthreads();
+    sel_load<false>(x, n, S, true);
+    cut = sel_cut<false>(n, k, S);
+  }
   int nk = 0, nr = 0;
   compact2(
       S, 0, n, 0, n, [&](int j) { return in_cut(sel_key<XBF>(S, j), j, cut); },
@@ -712,7 +794,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 size_t select_smem_bytes(int n, bool x_bf16) {
-  return 4u * (kBins + kCandWords + 512 + kMiscWords) + (x_bf16 ? 2u : 4u) * static_cast<size_t>(n) + 16;
+  return 4u * (kBins + kCandWords + 512 + kMiscWords + kH16Words) + (x_bf16 ? 2u : 4u) * static_cast<size_t>(n) + 16;
 }
 
 cudaError_t launch_select(const void* x, bool x_bf16, int n, int k, int32_t* kept, int32_t* rest,

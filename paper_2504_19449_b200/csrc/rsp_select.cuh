@@ -40,6 +40,7 @@
 namespace rsp {
 
 constexpr int kBins = 4096;   // level-1 histogram: key bits 30..19 (exponent + 4 mantissa bits)
+constexpr int kH16Words = 16384;  // 32768 bf16 keys x 16-bit counters (n <= 65535)
 constexpr int kCandWords = 2048;  // gathered boundary-bin members (more: refine over all of x)
 constexpr int kMiscWords = 96;
 
@@ -79,6 +80,7 @@ __device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
 struct SelArea {
   uint32_t xs;    // [n] raw activations (u16 bf16 bits or u32 fp32 bits)
   uint32_t h1;    // [kBins] level-1 histogram of key >> 19
+  uint32_t h16;   // [kH16Words] bf16 activations: full 15-bit key histogram, 16-bit counters
   uint32_t cand;  // [kCandWords] boundary-bin member indices, ascending
   uint32_t h2a;   // [256] refinement histograms (zero between cuts)
   uint32_t h2b;   // [256]
@@ -450,6 +452,181 @@ __device__ __noinline__ Cut sel_cut(int n, int k, SelArea s) {
   RSP_SEL_STAMP(3);
   return Cut{T, static_cast<int>(s.m(M_JLIM))};
 }
+
+// ===========================================================================
+// bf16 activations: |x| has 2^15 distinct keys, so ONE histogram of all of
+// them (16-bit counters packed two per word, 64 KB, zeroed off the critical
+// path) yields the exact k-th key with a single descending scan; only a tie
+// at the cut needs one more pass (lowest `need` indices of the key).
+// ===========================================================================
+__device__ __forceinline__ void sel_clear16(SelArea s) {
+  for (int i = threadIdx.x; i < kH16Words / 4; i += kThreads) sts4(s.h16 + 16u * i, make_uint4(0, 0, 0, 0));
+  if (threadIdx.x < 64) sts4(s.h2a + 16u * threadIdx.x, make_uint4(0, 0, 0, 0));
+  else if (threadIdx.x < 128) sts4(s.h2b + 16u * (threadIdx.x - 64), make_uint4(0, 0, 0, 0));
+}
+
+__device__ __forceinline__ void hist16_add(SelArea s, uint32_t bf_bits /* bf16 << 16 */) {
+  const uint32_t k15 = (bf_bits >> 16) & 0x7fffu;
+  reds_add(s.h16 + 4u * (k15 >> 1), 1u << (16 * (k15 & 1u)));
+}
+
+// x (global, bf16) -> s.xs and the 15-bit histogram (s.h16 zero and
+// published).  Ends with __syncthreads.
+__device__ __forceinline__ void sel_load16(const void* __restrict__ x, int n, SelArea s) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(x);
+  if ((a & 15u) == 0 && (n & 7) == 0) {
+    const uint4* xv = reinterpret_cast<const uint4*>(x);
+    const int nv = n >> 3;
+    for (int base = 0; base < nv; base += 4 * kThreads) {
+      uint4 u[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int i = base + q * kThreads + static_cast<int>(threadIdx.x);
+        u[q] = i < nv ? __ldg(xv + i) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int i = base + q * kThreads + static_cast<int>(threadIdx.x);
+        if (i >= nv) continue;
+        sts4(s.xs + 16u * static_cast<uint32_t>(i), u[q]);
+        const uint32_t w[4] = {u[q].x, u[q].y, u[q].z, u[q].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          hist16_add(s, w[e] << 16);
+          hist16_add(s, w[e] & 0xffff0000u);
+        }
+      }
+    }
+  } else {
+    for (int j = threadIdx.x; j < n; j += kThreads) {
+      const uint16_t raw = static_cast<const uint16_t*>(x)[j];
+      asm volatile("st.shared.u16 [%0], %1;" ::"r"(s.xs + 2u * j), "h"(raw) : "memory");
+      hist16_add(s, static_cast<uint32_t>(raw) << 16);
+    }
+  }
+  __syncthreads();
+}
+
+// The exact cut from the 15-bit histogram.  Thread t owns keys
+// [32768 - 128 (t+1), 32768 - 128 t) (64 words), scanned from the top.
+// Contains __syncthreads.
+__device__ __noinline__ Cut sel_cut16(int n, int k, SelArea s) {
+  if (k <= 0) return Cut{0xffffffffu, 0};
+  if (k >= n) return Cut{0u, INT_MAX};
+  static_assert(kThreads * 128 == 32768, "15-bit histogram ownership");
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t kk = static_cast<uint32_t>(k);
+  const uint32_t base = s.h16 + 4u * static_cast<uint32_t>(kH16Words - 64 * (tid + 1));
+  uint32_t local = 0;
+  // lanes sit 256 B apart: rotate the 16-B chunk order by lane so each
+  // 8-lane phase of an LDS.128 hits 8 distinct bank groups (else 32-way conflicts)
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const uint4 u = lds4(base + 16u * ((q + lane) & 15));
+    local += (u.x & 0xffffu) + (u.x >> 16) + (u.y & 0xffffu) + (u.y >> 16) + (u.z & 0xffffu) + (u.z >> 16) +
+             (u.w & 0xffffu) + (u.w >> 16);
+  }
+  const uint32_t wsum = __reduce_add_sync(0xffffffffu, local);
+  if (lane == 0) s.set_m(M_WSUM + warp, wsum);
+  __syncthreads();
+  const uint32_t tw = lane < kWarps ? s.m(M_WSUM + lane) : 0u;
+  uint32_t inc = tw;
+#pragma unroll
+  for (int o = 1; o < kWarps; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  const int wb = __ffs(__ballot_sync(0xffffffffu, lane < kWarps && inc - tw < kk && kk <= inc)) - 1;
+  if (warp == wb) {
+    const uint32_t wabove = __shfl_sync(0xffffffffu, inc - tw, wb);
+    uint32_t li = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, li, o);
+      if (lane >= o) li += t;
+    }
+    const uint32_t mine_ex = wabove + li - local;
+    const int ol = __ffs(__ballot_sync(0xffffffffu, mine_ex < kk && kk <= mine_ex + local)) - 1;
+    // the owner thread's 128 keys, scanned by the whole warp: lane l takes
+    // words 63-2l and 62-2l of the owner's range (4 keys, descending)
+    const int tb = warp * 32 + ol;
+    const uint32_t above = __shfl_sync(0xffffffffu, mine_ex, ol);
+    const uint32_t wbase = s.h16 + 4u * static_cast<uint32_t>(kH16Words - 64 * (tb + 1));
+    const uint32_t w1 = lds(wbase + 4u * (63 - 2 * lane)), w0 = lds(wbase + 4u * (62 - 2 * lane));
+    const uint32_t c[4] = {w1 >> 16, w1 & 0xffffu, w0 >> 16, w0 & 0xffffu};
+    const uint32_t lsum = c[0] + c[1] + c[2] + c[3];
+    uint32_t linc = lsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, linc, o);
+      if (lane >= o) linc += t;
+    }
+    uint32_t acc = above + linc - lsum;
+    const uint32_t key_top = static_cast<uint32_t>(32768 - 128 * tb - 1) - 4u * lane;  // key of c[0]
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (acc < kk && kk <= acc + c[q]) {
+        s.set_m(M_BIN, key_top - q);
+        s.set_m(M_ABOVE, acc);
+        s.set_m(M_CNT, c[q]);
+      }
+      acc += c[q];
+    }
+  }
+  __syncthreads();
+  const uint32_t key15 = s.m(M_BIN);
+  const uint32_t need = kk - s.m(M_ABOVE), cnt = s.m(M_CNT);
+  const uint32_t T = key15 << 16;  // the exact k-th key (fp32 bits, sign cleared)
+  if (need == cnt) return Cut{T, INT_MAX};  // every channel of the key is in S
+  // ties: the `need` lowest indices among the `cnt` channels of key15
+  if ((n & 7) == 0) {
+    const int nv = n >> 3;
+    const int v0 = static_cast<int>(static_cast<uint32_t>(nv) * tid / kThreads);
+    const int v1 = static_cast<int>(static_cast<uint32_t>(nv) * (tid + 1) / kThreads);
+    uint32_t mine = 0;
+    for (int v = v0; v < v1; ++v) {
+      const uint4 u = lds4(s.xs + 16u * static_cast<uint32_t>(v));
+      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) mine += ((w[e >> 1] >> (16 * (e & 1))) & 0x7fffu) == key15;
+    }
+    const uint32_t ex = block_excl_scan(mine, s.misc + 4u * M_SCAN, nullptr);
+    if (ex < need && need <= ex + mine) {
+      uint32_t c = ex;
+      for (int v = v0; v < v1; ++v) {
+        const uint4 u = lds4(s.xs + 16u * static_cast<uint32_t>(v));
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+        bool done = false;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          if (!done && ((w[e >> 1] >> (16 * (e & 1))) & 0x7fffu) == key15 && ++c == need) {
+            s.set_m(M_JLIM, static_cast<uint32_t>(8 * v + e + 1));
+            done = true;
+          }
+        }
+        if (done) break;
+      }
+    }
+  } else {
+    const int j0 = static_cast<int>(static_cast<uint32_t>(n) * tid / kThreads);
+    const int j1 = static_cast<int>(static_cast<uint32_t>(n) * (tid + 1) / kThreads);
+    uint32_t mine = 0;
+    for (int j = j0; j < j1; ++j) mine += (lds_u16(s.xs + 2u * j) & 0x7fffu) == key15;
+    const uint32_t ex = block_excl_scan(mine, s.misc + 4u * M_SCAN, nullptr);
+    if (ex < need && need <= ex + mine) {
+      uint32_t c = ex;
+      for (int j = j0; j < j1; ++j) {
+        if ((lds_u16(s.xs + 2u * j) & 0x7fffu) == key15 && ++c == need) {
+          s.set_m(M_JLIM, static_cast<uint32_t>(j + 1));
+          break;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  return Cut{T, static_cast<int>(s.m(M_JLIM))};
+}
+
 
 // Deterministic two-list compaction in one sweep: members of range A
 // ([a0, a1), predicate pa) and of range B ([b0, b1), predicate pb), each in

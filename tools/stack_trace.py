@@ -82,6 +82,23 @@ def main():
             if col.size:
                 ph.append(f"{lab}={np.median(col) / args.mhz:.2f}")
         print(f"{name.split('.', 1)[1]:17s} {g:4d} {start:6.2f} {waitd:6.2f} {end:6.2f} {wall:6.2f} | " + " ".join(ph))
+    for i in range(min(7, len(plans))):
+        print(f"stragglers of linear {i} ({plans[i][0]}):")
+        stragglers(t, i, args.mhz)
+
+
+def stragglers(t, i, mhz, top=6):
+    """Phase stamps (us from the CTA's run start) of the CTAs finishing linear i last."""
+    part = t[i, :, 1] > 0
+    idx = np.where(part)[0]
+    end = t[i, idx, 14]
+    order = idx[np.argsort(end)[::-1][:top]]
+    med = {ev: np.median(t[i, idx, ev]) / mhz for ev in PH}
+    print(f"  median: " + " ".join(f"{PH[ev]}={med[ev]:.2f}" for ev in PH))
+    t0 = t[i, idx, 0].min()
+    for c in order:
+        print(f"  cta {c:3d} end={(t[i, c, 14] - t0) / 1e3:6.2f} start={(t[i, c, 0] - t0) / 1e3:5.2f} waitd={(t[i, c, 13] - t0) / 1e3:5.2f} | "
+              + " ".join(f"{PH[ev]}={t[i, c, ev] / mhz:.2f}" for ev in PH))
 
 
 if __name__ == "__main__":
