@@ -164,7 +164,8 @@ void operand_buffers(int avail, int need_a, int need_b, int* abuf, int* bbuf) {
   avail = std::max(0, avail - 1024);
   *abuf = *bbuf = 0;
   if (!env_int("RSP_SMEM_OPS", 0)) return;
-  *abuf = std::min(need_a + need_b + 16, avail) / 16 * 16;
+  const int cap = env_int("RSP_OBUF_KB", 0) > 0 ? env_int("RSP_OBUF_KB", 0) * 1024 : avail;
+  *abuf = std::min(std::min(need_a + need_b + 16, avail), cap) / 16 * 16;
 }
 
 // Decompose one forward over the GPU: col_tiles column tiles x k_splits
@@ -187,7 +188,7 @@ rsp_status make_plan(const rsp_linear& L, const DevProps& dp, LaunchPlan* out, i
   double best = 1e30;
   // with a low-rank term, prefer tiles of at most 4 warp columns: that leaves
   // room for a stage-1 warp group beside the W warps (warp-specialised path)
-  const int c2_pref = (L.rank > 0 && L.k < n) ? 4 : 8;
+  const int c2_pref = (L.rank > 0 && L.k < n) ? env_int("RSP_C2PREF", 4) : 8;
   for (int c2 = 1; c2 <= 8; c2 *= 2) {  // <= one row of warps (kThreads / 32 = 8)
     const int nt = (wcols + c2 - 1) / c2;
     if (nt > sms || nt > static_cast<int>(rsp::kMaxTickets)) continue;
@@ -888,6 +889,7 @@ rsp_status rsp_stack_create_ex(const rsp_linear* const* layers, uint32_t count, 
   // its share of the group's bytes.  Deterministic mode shares one
   // partial-sum scratch, so there every linear waits for the previous one.
   std::vector<LaunchPlan> plans(count);
+  uint32_t pg0 = 0, pg1 = 0;  // the previous group
   for (uint32_t g0 = 0; g0 < count;) {
     uint32_t g1 = g0 + 1;
     while (g1 < count && !det && wait_prev && !wait_prev[g1]) ++g1;
@@ -912,9 +914,15 @@ rsp_status rsp_stack_create_ex(const rsp_linear* const* layers, uint32_t count, 
       const bool wp = i > 0 && (i == g0);
       descs[i] = lin_desc(layers[i], x_devs[i], y_devs[i], dense != 0, static_cast<int>(i),
                           wp ? rsp::kLinWaitPrev : 0, &plans[i], cta0);
+      if (wp) {
+        descs[i].dep0 = static_cast<int>(pg0);
+        descs[i].ndep = static_cast<int>(pg1 - pg0);
+      }
       cta0 += plans[i].grid;
       grid = std::max(grid, cta0);
     }
+    pg0 = g0;
+    pg1 = g1;
     g0 = g1;
   }
   int need_a = 0, need_b = 0;

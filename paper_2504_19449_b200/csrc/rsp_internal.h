@@ -14,7 +14,7 @@ constexpr unsigned kMaxTickets = kSlotWords - 2;
 constexpr unsigned kWsHdrBytes = 256;  // [0] launch epoch, [1] CTAs done in this launch
 
 // Flags of one linear in a stack launch.
-constexpr int kLinWaitPrev = 1;  // its x depends on the previous linear's y: full grid barrier first
+constexpr int kLinWaitPrev = 1;  // its x depends on the previous group's y: wait for that group's CTAs first
 constexpr int kLinDense = 2;     // all n channels through W, no selection, no low-rank term
 
 // One linear of a stack launch (descriptors live in device memory; a
@@ -30,6 +30,7 @@ struct LinDesc {
   int flags;
   int slot;  // index of the linear's barrier slot / t buffers in the workspace
   int cta0;  // first CTA of this linear (linears sharing an input run side by side)
+  int dep0, ndep;  // kLinWaitPrev: wait for linears [dep0, dep0 + ndep) (the previous group) to complete
 };
 
 // Parameters of one launch of the stack kernel (rsp_kernels.cu).

@@ -315,6 +315,78 @@ __device__ __forceinline__ Acc stream_list_smem(uint32_t list, int first, int co
   return r;
 }
 
+// Per-(linear, CTA) constants of run_linear.  Each integer division is a
+// ~20-instruction dependent chain; a linear needs ~20 of them, which cost
+// ~0.5 us at the head of every linear when computed there.  Thread 0
+// computes them in the previous linear's tail (off the critical path) into
+// shared memory (misc[M_PLAN..]); run_linear reads them back.
+struct CtaPlan {
+  int v0, tw, uc0, uc1;   // column tile [v0, v0 + tw) in 16-B units; stage-1 channel slice
+  int alo, na, wc0, wc1;  // A_r^T rows [alo, alo + na); W channel range
+  int ct, ks, na_s, flags;  // tile, split, A rows in shared memory, kPlan* flags
+  int G1, G2, GA, WS;     // stage-1 / W / A warp groups; stage-1 warps split off (spec)
+  uint32_t map1[2], mapW[2], mapA[2];  // per warp, one byte: group | (warp column << 4); group 15 = idle
+  int pad[2];
+};
+constexpr int kPlanBSmem = 1, kPlanSpec = 2, kPlanHasLr = 4;
+union PlanWords {
+  CtaPlan p;
+  uint4 q[6];
+};
+static_assert(sizeof(CtaPlan) == sizeof(uint4) * 6, "plan layout");
+static_assert(M_PLAN + 24 <= kMiscWords, "plan slot");
+
+__device__ __forceinline__ uint32_t warp_map_byte(int w, int first, int C, int G) {
+  const int ww = w - first;
+  int g = ww >= 0 ? ww / C : 15;
+  if (g >= G) g = 15;
+  return static_cast<uint32_t>(g | ((ww >= 0 ? ww % C : 0) << 4));
+}
+
+template <typename WT>
+__device__ __forceinline__ void fill_plan(const StackParams& P, const LinDesc& d, int bg, const Ctx& C) {
+  constexpr int ES = static_cast<int>(sizeof(WT));
+  const int b = bg - d.cta0;
+  if (threadIdx.x != 0 || b < 0 || b >= d.grid) return;
+  PlanWords w;
+  CtaPlan& p = w.p;
+  const int KS = d.k_splits, NB = d.grid;
+  p.ct = b / KS;
+  p.ks = b - p.ct * KS;
+  const int vrow = d.m_pad * ES / 16, wcols = (vrow + 31) / 32;
+  p.v0 = min(vrow, 32 * part(wcols, p.ct, d.col_tiles));
+  p.tw = min(vrow, 32 * part(wcols, p.ct + 1, d.col_tiles)) - p.v0;
+  const bool dense = (d.flags & kLinDense) != 0;
+  const bool has_lr = !dense && d.r > 0 && d.k < d.n;
+  p.uc0 = has_lr ? part(d.n, b, NB) : 0;
+  p.uc1 = has_lr ? part(d.n, b + 1, NB) : 0;
+  p.alo = has_lr ? part(d.r, p.ks, KS) : 0;
+  p.na = has_lr ? part(d.r, p.ks + 1, KS) - p.alo : 0;
+  p.wc0 = part(d.n, p.ks, KS);
+  p.wc1 = part(d.n, p.ks + 1, KS);
+  const OperandSplit os = operand_split<WT>(d, b, C);
+  p.na_s = os.na_s;
+  const int vb = d.r_pad * ES / 16;  // 16-B units per B_r^T row
+  const int C1 = max((vb + 31) / 32, 1);
+  const int C2 = max((p.tw + 31) / 32, 1);
+  const bool spec = !(P.knobs & 8) && has_lr && (os.b_smem || (P.knobs & 16)) && C1 < kWarps && C2 <= kWarps - C1;
+  p.flags = (os.b_smem ? kPlanBSmem : 0) | (spec ? kPlanSpec : 0) | (has_lr ? kPlanHasLr : 0);
+  p.WS = spec ? C1 : 0;
+  p.G1 = kWarps / C1;
+  p.G2 = (kWarps - p.WS) / C2;
+  p.GA = kWarps / C2;
+  p.map1[0] = p.map1[1] = p.mapW[0] = p.mapW[1] = p.mapA[0] = p.mapA[1] = 0u;
+#pragma unroll
+  for (int q = 0; q < kWarps; ++q) {
+    p.map1[q >> 2] |= warp_map_byte(q, 0, C1, p.G1) << (8 * (q & 3));
+    p.mapW[q >> 2] |= warp_map_byte(q, p.WS, C2, p.G2) << (8 * (q & 3));
+    p.mapA[q >> 2] |= warp_map_byte(q, 0, C2, p.GA) << (8 * (q & 3));
+  }
+  p.pad[0] = p.pad[1] = 0;
+#pragma unroll
+  for (int i = 0; i < 6; ++i) sts4(C.S.misc + 4u * M_PLAN + 16u * i, w.q[i]);
+}
+
 // x-independent per-linear setup of CTA bg, done in the previous linear's
 // tail (off the critical path): zero its slice of y (split-K reductions land
 // there after the t barrier, which orders them after this) and of the next
@@ -353,41 +425,39 @@ __device__ __forceinline__ void run_linear(const StackParams& P, const LinDesc& 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int b = static_cast<int>(blockIdx.x) - d.cta0, NB = d.grid;  // index within the linear's partition
   const int KS = d.k_splits;
-  const int ct = b / KS, ks = b % KS;
   const bool dense = (d.flags & kLinDense) != 0;
 #define RSP_TRACE(ev)                                                              \
   do {                                                                             \
     if (trace && tid == 0) trace[ev] = clk() - t_start;                           \
   } while (0)
 
-  // Column tile of this CTA in 16-byte units (whole 32-unit warp columns).
-  const int vrow = d.m_pad * ES / 16;
-  const int wcols = (vrow + 31) / 32;
-  const int v0 = min(vrow, 32 * part(wcols, ct, d.col_tiles)), v1 = min(vrow, 32 * part(wcols, ct + 1, d.col_tiles));
-  const int tw = v1 - v0, col0 = v0 * VE;
-
   const int k_eff = dense ? d.n : d.k;
   const bool has_lr = !dense && d.r > 0 && k_eff < d.n;
   const bool det = P.deterministic != 0;
   const bool use_bar = has_lr || (KS > 1 && !det);
-  // Static ranges: stage-1 rows in channel slice [uc0, uc1), A_r^T rows
-  // [alo, ahi); W rows are split by rank in S below.
-  const int uc0 = has_lr ? part(d.n, b, NB) : 0, uc1 = has_lr ? part(d.n, b + 1, NB) : 0;
-  const int alo = has_lr ? part(d.r, ks, KS) : 0, ahi = has_lr ? part(d.r, ks + 1, KS) : 0;
-  const int na = ahi - alo;
-  const OperandSplit os = operand_split<WT>(d, b, C);  // rows [0, os.na_s) of A in shared memory
-
   const uint8_t* Wt = static_cast<const uint8_t*>(d.Wt);
   const uint8_t* At = static_cast<const uint8_t*>(d.At);
   const uint8_t* Bt = static_cast<const uint8_t*>(d.Bt);
   const uint32_t rowW = static_cast<uint32_t>(d.m_pad) * ES;  // bytes per W^T / A_r^T row
   const uint32_t rowB = static_cast<uint32_t>(d.r_pad) * ES;  // bytes per B_r^T row
-  const uint8_t* a_tile = At + static_cast<size_t>(col0) * ES;
   unsigned* slot = slot_of(P, d.slot);
   float* t_cur = P.t_acc + (static_cast<size_t>(d.slot) * 2 + (C.epoch & 1u)) * kTAccCap;
 
-  __syncthreads();  // prep_linear's zeroing (histograms, y slice) is complete
+  __syncthreads();  // prep_linear's zeroing (histograms, y slice) and the CTA plan are complete
   RSP_TRACE(1);
+  PlanWords pw;
+#pragma unroll
+  for (int i = 0; i < 6; ++i) pw.q[i] = lds4(S.misc + 4u * M_PLAN + 16u * i);
+  const CtaPlan& cp = pw.p;
+  // Column tile of this CTA in 16-byte units (whole 32-unit warp columns).
+  const int v0 = cp.v0, tw = cp.tw, col0 = v0 * VE;
+  const int ct = cp.ct, ks = cp.ks;
+  // Static ranges: stage-1 rows in channel slice [uc0, uc1), A_r^T rows
+  // [alo, alo + na); W rows are split by rank in S below.
+  const int uc0 = cp.uc0, uc1 = cp.uc1, alo = cp.alo, na = cp.na, ahi = alo + na;
+  const int C2 = max((tw + 31) >> 5, 1);  // warp columns in the tile
+  const OperandSplit os{(cp.flags & kPlanBSmem) != 0, cp.na_s};  // rows [0, os.na_s) of A in shared memory
+  const uint8_t* a_tile = At + static_cast<size_t>(col0) * ES;
 
   // ---- 1. x -> shared memory + level-1 histogram; the exact cut ----
   Cut cut{0u, INT_MAX};
@@ -407,10 +477,15 @@ __device__ __forceinline__ void run_linear(const StackParams& P, const LinDesc& 
   // (measured: splitting S by global rank balances the W rows exactly but the
   // extra pass over all n costs more than the imbalance)
   int nW = 0, nU = 0;
-  {
-    const int wc0 = part(d.n, ks, KS), wc1 = part(d.n, ks + 1, KS);
+  if constexpr (XBF) {
+    compact2_16(
+        S, cut, cp.wc0, cp.wc1, uc0, uc1,
+        [&](bool p, int i, int j, uint32_t bits) { sts2_pred(p, C.list_w + 8u * i, static_cast<uint32_t>(j), bits); },
+        [&](bool p, int i, int j, uint32_t bits) { sts2_pred(p, C.list_u + 8u * i, static_cast<uint32_t>(j), bits); },
+        &nW, &nU);
+  } else {
     compact2(
-        S, wc0, wc1, uc0, uc1, [&](int j) { return in_cut(sel_key<XBF>(S, j), j, cut); },
+        S, cp.wc0, cp.wc1, uc0, uc1, [&](int j) { return in_cut(sel_key<XBF>(S, j), j, cut); },
         [&](int j) { return !in_cut(sel_key<XBF>(S, j), j, cut); },
         [&](int i, int j) { sts2(C.list_w + 8u * i, static_cast<uint32_t>(j), sel_bits<XBF>(S, j)); },
         [&](int i, int j) { sts2(C.list_u + 8u * i, static_cast<uint32_t>(j), sel_bits<XBF>(S, j)); }, &nW, &nU);
@@ -421,15 +496,12 @@ __device__ __forceinline__ void run_linear(const StackParams& P, const LinDesc& 
   // group of C1 warps runs it (and the t hand-off and the arrive) while the
   // other warps stream W.  Otherwise all warps run stage 1 first.
   const int vb = d.r_pad * ES / 16;  // 16-B units per B_r^T row
-  const int C1 = max((vb + 31) / 32, 1);
-  const int C2 = max((tw + 31) / 32, 1);
-  const bool spec = !(P.knobs & 8) && has_lr && os.b_smem && C1 < kWarps && C2 <= kWarps - C1;
-  const int WS = spec ? C1 : 0;                // stage-1 warps [0, WS)
-  const int nWW = kWarps - WS;                 // W warps
-  const int wwarp = warp - WS;
-  const int G2 = nWW / C2, g2 = wwarp >= 0 ? wwarp / C2 : G2;
-  const int v = (wwarp >= 0 ? wwarp % C2 : 0) * 32 + lane;
-  const bool ok2 = wwarp >= 0 && g2 < G2 && v < tw;
+  const bool spec = (cp.flags & kPlanSpec) != 0;
+  const int WS = cp.WS;                        // stage-1 warps [0, WS)
+  const uint32_t bW = ((warp < 4 ? cp.mapW[0] : cp.mapW[1]) >> (8 * (warp & 3))) & 0xffu;
+  const int G2 = cp.G2, g2 = static_cast<int>(bW & 15u);
+  const int v = static_cast<int>(bW >> 4) * 32 + lane;
+  const bool ok2 = g2 < G2 && v < tw;
   if (has_lr) {
     if (preloaded) mbar_wait_s(C.bar, parity);  // the operand bulk copies have landed
     RSP_TRACE(10);
@@ -437,7 +509,8 @@ __device__ __forceinline__ void run_linear(const StackParams& P, const LinDesc& 
   if (spec) {
     if (warp < WS) {
       const int v1 = warp * 32 + lane;
-      const Acc a1 = stream_list_smem<WT>(C.list_u, 0, nU, 1, v1 < vb, C.obuf + v1 * 16u, uc0, rowB);
+      const Acc a1 = os.b_smem ? stream_list_smem<WT>(C.list_u, 0, nU, 1, v1 < vb, C.obuf + v1 * 16u, uc0, rowB)
+                               : stream_list<WT>(C.list_u, 0, nU, 1, v1 < vb, Bt + v1 * 16, rowB, C.pol, C.zero);
       RSP_TRACE(11);
       if (v1 < vb) sts_acc<VE>(C.red + 4u * (v1 * VE), a1);
       named_bar_sync(1, WS * 32);
@@ -453,8 +526,9 @@ __device__ __forceinline__ void run_linear(const StackParams& P, const LinDesc& 
       RSP_TRACE(12);
     }
   } else if (has_lr) {
-    const int G1 = kWarps / C1, g1 = warp / C1;
-    const int v1 = (warp % C1) * 32 + lane;
+    const uint32_t b1 = ((warp < 4 ? cp.map1[0] : cp.map1[1]) >> (8 * (warp & 3))) & 0xffu;
+    const int G1 = cp.G1, g1 = static_cast<int>(b1 & 15u);
+    const int v1 = static_cast<int>(b1 >> 4) * 32 + lane;
     const bool ok = g1 < G1 && v1 < vb;
     const Acc a1 = os.b_smem ? stream_list_smem<WT>(C.list_u, g1, nU, G1, ok, C.obuf + v1 * 16u, uc0, rowB)
                              : stream_list<WT>(C.list_u, g1, nU, G1, ok, Bt + v1 * 16, rowB, C.pol, C.zero);
@@ -486,8 +560,9 @@ __device__ __forceinline__ void run_linear(const StackParams& P, const LinDesc& 
   // equal to the W mapping unless a stage-1 warp group was split off) ----
   // The first batch of a warp's A rows is loaded before waiting on the
   // barrier (A does not depend on t), so its round trip overlaps the wait.
-  const int GA = kWarps / C2, gA = warp / C2;
-  const int vA = (warp % C2) * 32 + lane;
+  const uint32_t bA = ((warp < 4 ? cp.mapA[0] : cp.mapA[1]) >> (8 * (warp & 3))) & 0xffu;
+  const int GA = cp.GA, gA = static_cast<int>(bA & 15u);
+  const int vA = static_cast<int>(bA >> 4) * 32 + lane;
   const bool okA = gA < GA && vA < tw;
   const uint8_t* abase = a_tile + static_cast<size_t>(alo) * rowW + vA * 16;
   uint4 ua[kUA];
@@ -642,12 +717,14 @@ __global__ void __launch_bounds__(kThreads, 1) stack_kernel(const StackParams P)
   __syncthreads();
   C.pol = l2_evict_first_policy();
   C.zero = static_cast<uint32_t>(P.knobs) & 0x40000000u;  // bit 30 of knobs is never set
+  C.S.zero = C.zero;
   const int tid = threadIdx.x, b = blockIdx.x, NB = gridDim.x;
 
   // x-independent work first: overlaps the previous launch under PDL
   const LinDesc d0 = P.descs ? P.descs[0] : P.one;
   uint32_t parity = 0;
   bool pre = !(P.knobs & 6) && preload_operands<WT>(d0, b, C);
+  fill_plan<WT>(P, d0, b, C);
   sel_clear(C.S);
   if (P.pdl) {
     griddep_wait();
@@ -659,16 +736,21 @@ __global__ void __launch_bounds__(kThreads, 1) stack_kernel(const StackParams P)
   prep_linear<WT, XBF>(P, d0, b, C);
 
   LinDesc d = d0;
-  int prev_slot = -1;
   for (int l = 0; l < P.count; ++l) {
     // debug trace of (linear l, CTA b): [0] globaltimer at iteration start,
     // [13] globaltimer after the dependency wait, [1..12] clock64 phases
     long long* tr = P.trace ? P.trace + (static_cast<size_t>(l) * NB + b) * 16 : nullptr;
     if (tr && tid == 0) tr[0] = gtimer();
-    if (prev_slot >= 0 && (d.flags & kLinWaitPrev)) {
-      // x of this linear is the output of the previous one: all CTAs' y
-      // contributions of linear l-1 must have landed
-      if (tid == 0) spin_until_count(slot_of(P, prev_slot), static_cast<unsigned>(NB));
+    if (d.flags & kLinWaitPrev) {
+      // x of this group is the output of the previous group: every member
+      // CTA of each of its linears must have issued its y contributions
+      // (every CTA waits here, members of this group's later linears too)
+      if (tid == 0) {
+        for (int j = d.dep0; j < d.dep0 + d.ndep; ++j) {
+          const LinDesc* q = P.descs + j;
+          spin_until_count(slot_of(P, q->slot), static_cast<unsigned>(q->grid));
+        }
+      }
       __syncthreads();
     }
     if (tr && tid == 0) tr[13] = gtimer();
@@ -676,7 +758,8 @@ __global__ void __launch_bounds__(kThreads, 1) stack_kernel(const StackParams P)
       __syncthreads();  // previous linear's reads of the operand buffer are complete
       pre = preload_operands<WT>(d, b, C);
     }
-    if (b >= d.cta0 && b < d.cta0 + d.grid) run_linear<WT, XBF>(P, d, C, tr, pre, parity);
+    const bool member = b >= d.cta0 && b < d.cta0 + d.grid;
+    if (member) run_linear<WT, XBF>(P, d, C, tr, pre, parity);
     if (pre) parity ^= 1u;
     // next linear's operands towards L2 while this one drains
     LinDesc dn = d;
@@ -685,10 +768,12 @@ __global__ void __launch_bounds__(kThreads, 1) stack_kernel(const StackParams P)
       pre = !(P.knobs & 6) && preload_operands<WT>(dn, b, C);
     }
     __syncthreads();  // this CTA's y contributions are issued; shared memory is free
-    if (tid == 0) red_release_add(slot_of(P, d.slot), 1u);
-    if (l + 1 < P.count) prep_linear<WT, XBF>(P, dn, b, C);
+    if (member && tid == 0) red_release_add(slot_of(P, d.slot), 1u);
+    if (l + 1 < P.count) {
+      fill_plan<WT>(P, dn, b, C);
+      prep_linear<WT, XBF>(P, dn, b, C);
+    }
     if (tr && tid == 0) tr[14] = gtimer();
-    prev_slot = d.slot;
     d = dn;
   }
 
@@ -755,7 +840,7 @@ cudaError_t launch_stack(const StackParams& p, int elem_bytes, bool x_bf16, int 
 // ---------------------------------------------------------------------------
 template <bool XBF>
 __global__ void __launch_bounds__(kThreads, 1)
-    select_kernel(const void* x, int n, int k, int32_t* kept, int32_t* rest, float* sparse_x) {
+    select_kernel(const void* x, int n, int k, int32_t* kept, int32_t* rest, float* sparse_x, uint32_t zero) {
   extern __shared__ __align__(16) uint8_t smem_sel[];
   const uint32_t sb = smem_base_pinned(smem_sel);
   SelArea S;
@@ -766,6 +851,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   S.misc = S.h2b + 4u * 256;
   S.h16 = S.misc + 4u * kMiscWords;
   S.xs = S.h16 + 4u * kH16Words;
+  S.zero = zero;
   Cut cut;
   if constexpr (XBF) {
     sel_clear16(S);
@@ -779,18 +865,32 @@ __global__ void __launch_bounds__(kThreads, 1)
     cut = sel_cut<false>(n, k, S);
   }
   int nk = 0, nr = 0;
-  compact2(
-      S, 0, n, 0, n, [&](int j) { return in_cut(sel_key<XBF>(S, j), j, cut); },
-      [&](int j) { return !in_cut(sel_key<XBF>(S, j), j, cut); },
-      [&](int i, int j) {
-        if (kept) kept[i] = j;
-        if (sparse_x) sparse_x[j] = __uint_as_float(sel_bits<XBF>(S, j));
-      },
-      [&](int i, int j) {
-        if (rest) rest[i] = j;
-        if (sparse_x) sparse_x[j] = 0.f;
-      },
-      &nk, &nr);
+  if constexpr (XBF) {
+    compact2_16(
+        S, cut, 0, n, 0, n,
+        [&](bool p, int i, int j, uint32_t bits) {
+          if (p && kept) kept[i] = j;
+          if (p && sparse_x) sparse_x[j] = __uint_as_float(bits);
+        },
+        [&](bool p, int i, int j, uint32_t) {
+          if (p && rest) rest[i] = j;
+          if (p && sparse_x) sparse_x[j] = 0.f;
+        },
+        &nk, &nr);
+  } else {
+    compact2(
+        S, 0, n, 0, n, [&](int j) { return in_cut(sel_key<XBF>(S, j), j, cut); },
+        [&](int j) { return !in_cut(sel_key<XBF>(S, j), j, cut); },
+        [&](int i, int j) {
+          if (kept) kept[i] = j;
+          if (sparse_x) sparse_x[j] = __uint_as_float(sel_bits<XBF>(S, j));
+        },
+        [&](int i, int j) {
+          if (rest) rest[i] = j;
+          if (sparse_x) sparse_x[j] = 0.f;
+        },
+        &nk, &nr);
+  }
 }
 
 size_t select_smem_bytes(int n, bool x_bf16) {
@@ -806,9 +906,9 @@ cudaError_t launch_select(const void* x, bool x_bf16, int n, int k, int32_t* kep
                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   if (x_bf16)
-    select_kernel<true><<<1, kThreads, smem, stream>>>(x, n, k, kept, rest, sparse_x);
+    select_kernel<true><<<1, kThreads, smem, stream>>>(x, n, k, kept, rest, sparse_x, 0u);
   else
-    select_kernel<false><<<1, kThreads, smem, stream>>>(x, n, k, kept, rest, sparse_x);
+    select_kernel<false><<<1, kThreads, smem, stream>>>(x, n, k, kept, rest, sparse_x, 0u);
   return cudaGetLastError();
 }
 

@@ -42,7 +42,7 @@ namespace rsp {
 constexpr int kBins = 4096;   // level-1 histogram: key bits 30..19 (exponent + 4 mantissa bits)
 constexpr int kH16Words = 16384;  // 32768 bf16 keys x 16-bit counters (n <= 65535)
 constexpr int kCandWords = 2048;  // gathered boundary-bin members (more: refine over all of x)
-constexpr int kMiscWords = 96;
+constexpr int kMiscWords = 128;
 
 // misc[] word slots
 enum : int {
@@ -53,6 +53,9 @@ enum : int {
   M_MBAR = 88,   // [88, 90): the stack kernel's operand mbarrier (8-byte aligned)
   M_LISTA = 32,  // [32, 48): per-warp member counts, list A
   M_LISTB = 48,  // [48, 64): per-warp member counts, list B
+  M_TCNT = 23,   // tie members appended so far (fast tie path)
+  M_OVER = 24,   // bf16 keys >= kWinHi (sel_load16)
+  M_PLAN = 96,   // [96, 128): the stack kernel's per-CTA plan of the next linear
 };
 
 struct Cut {
@@ -85,6 +88,7 @@ struct SelArea {
   uint32_t h2a;   // [256] refinement histograms (zero between cuts)
   uint32_t h2b;   // [256]
   uint32_t misc;  // [kMiscWords]
+  uint32_t zero;  // 0 at run time, opaque to the compiler (load-batching dependences)
   __device__ __forceinline__ uint32_t m(int slot) const { return lds(misc + 4u * slot); }
   __device__ __forceinline__ void set_m(int slot, uint32_t v) const { sts(misc + 4u * slot, v); }
 };
@@ -463,6 +467,7 @@ __device__ __forceinline__ void sel_clear16(SelArea s) {
   for (int i = threadIdx.x; i < kH16Words / 4; i += kThreads) sts4(s.h16 + 16u * i, make_uint4(0, 0, 0, 0));
   if (threadIdx.x < 64) sts4(s.h2a + 16u * threadIdx.x, make_uint4(0, 0, 0, 0));
   else if (threadIdx.x < 128) sts4(s.h2b + 16u * (threadIdx.x - 64), make_uint4(0, 0, 0, 0));
+  if (threadIdx.x == 0) s.set_m(M_OVER, 0u);
 }
 
 __device__ __forceinline__ void hist16_add(SelArea s, uint32_t bf_bits /* bf16 << 16 */) {
@@ -470,31 +475,64 @@ __device__ __forceinline__ void hist16_add(SelArea s, uint32_t bf_bits /* bf16 <
   reds_add(s.h16 + 4u * (k15 >> 1), 1u << (16 * (k15 & 1u)));
 }
 
-// x (global, bf16) -> s.xs and the 15-bit histogram (s.h16 zero and
-// published).  Ends with __syncthreads.
+// The histogram window scanned first: keys [kWinLo, kWinHi), |x| in
+// [2^-40, 2^24) -- 8192 keys, 16 KB of the 64 KB histogram.  The exact cut
+// falls there for any realistic activation vector; otherwise (counted: the
+// keys at or above kWinHi, or too few keys in the window) the whole
+// histogram is scanned.
+constexpr uint32_t kWinHi = 151u << 7, kWinKeys = 8192u, kWinLo = kWinHi - kWinKeys;
+
+// Packed-pair key tests on a word holding two bf16 activations (keys are
+// the 15 magnitude bits of each half; every sum below stays inside its half).
+//   bit 15 / 31 set  <=>  low / high key > t   (t < 0x7fff)
+__device__ __forceinline__ uint32_t pair_gt(uint32_t w, uint32_t t) {
+  return ((w & 0x7fff7fffu) + (0x7fffu - t) * 0x10001u) & 0x80008000u;
+}
+//   bit 15 / 31 set  <=>  low / high key == t   (t <= 0x7fff)
+__device__ __forceinline__ uint32_t pair_eq(uint32_t w, uint32_t t) {
+  const uint32_t z = (w & 0x7fff7fffu) ^ (t * 0x10001u);
+  return ~(z + 0x7fff7fffu) & 0x80008000u;
+}
+// 8 channels' flags (bits 15 / 31 of four words, channel 2i / 2i+1 in word i) -> bits 0..7.
+__device__ __forceinline__ uint32_t pack8(uint32_t f0, uint32_t f1, uint32_t f2, uint32_t f3) {
+  const uint32_t t = (f0 >> 15) | (f1 >> 13) | (f2 >> 11) | (f3 >> 9);  // even at 0,2,4,6; odd at 16,18,20,22
+  return (t & 0x55u) | ((t >> 15) & 0xaau);
+}
+
+// x (global, bf16) -> s.xs, the 15-bit histogram (s.h16 zero and published)
+// and misc[M_OVER] = #keys >= kWinHi.  Ends with __syncthreads.
 __device__ __forceinline__ void sel_load16(const void* __restrict__ x, int n, SelArea s) {
   const uintptr_t a = reinterpret_cast<uintptr_t>(x);
+  uint32_t over = 0;
   if ((a & 15u) == 0 && (n & 7) == 0) {
     const uint4* xv = reinterpret_cast<const uint4*>(x);
     const int nv = n >> 3;
-    for (int base = 0; base < nv; base += 4 * kThreads) {
-      uint4 u[4];
+    constexpr int kB = 8;  // n <= 16384 in one round trip
+    for (int base = 0; base < nv; base += kB * kThreads) {
+      uint4 u[kB];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < kB; ++q) {
         const int i = base + q * kThreads + static_cast<int>(threadIdx.x);
         u[q] = i < nv ? __ldg(xv + i) : make_uint4(0, 0, 0, 0);
       }
+      // every histogram update waits on every load of the round (see stream_list)
+      uint32_t dep = 0;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < kB; ++q) dep ^= u[q].x;
+      dep &= s.zero;
+#pragma unroll
+      for (int q = 0; q < kB; ++q) {
         const int i = base + q * kThreads + static_cast<int>(threadIdx.x);
         if (i >= nv) continue;
         sts4(s.xs + 16u * static_cast<uint32_t>(i), u[q]);
-        const uint32_t w[4] = {u[q].x, u[q].y, u[q].z, u[q].w};
+        const uint32_t w[4] = {u[q].x | dep, u[q].y, u[q].z, u[q].w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           hist16_add(s, w[e] << 16);
           hist16_add(s, w[e] & 0xffff0000u);
         }
+        over += __popc(pack8(pair_gt(w[0], kWinHi - 1), pair_gt(w[1], kWinHi - 1), pair_gt(w[2], kWinHi - 1),
+                             pair_gt(w[3], kWinHi - 1)));
       }
     }
   } else {
@@ -502,30 +540,23 @@ __device__ __forceinline__ void sel_load16(const void* __restrict__ x, int n, Se
       const uint16_t raw = static_cast<const uint16_t*>(x)[j];
       asm volatile("st.shared.u16 [%0], %1;" ::"r"(s.xs + 2u * j), "h"(raw) : "memory");
       hist16_add(s, static_cast<uint32_t>(raw) << 16);
+      over += (raw & 0x7fffu) >= kWinHi;
     }
   }
+  over = __reduce_add_sync(0xffffffffu, over);
+  if ((threadIdx.x & 31) == 0 && over) reds_add(s.misc + 4u * M_OVER, over);
   __syncthreads();
 }
 
-// The exact cut from the 15-bit histogram.  Thread t owns keys
-// [32768 - 128 (t+1), 32768 - 128 t) (64 words), scanned from the top.
-// Contains __syncthreads.
-__device__ __noinline__ Cut sel_cut16(int n, int k, SelArea s) {
-  if (k <= 0) return Cut{0xffffffffu, 0};
-  if (k >= n) return Cut{0u, INT_MAX};
-  static_assert(kThreads * 128 == 32768, "15-bit histogram ownership");
+// Descending search over per-thread key ranges: thread t holds `local`, the
+// count of keys in [top - PER (t+1), top - PER t), with `above0` keys above
+// `top`.  Writes misc[M_BIN / M_ABOVE / M_CNT] for the key where the
+// cumulative count reaches kk (M_BIN untouched when it lies outside).
+// Two __syncthreads.
+template <int PER>
+__device__ __forceinline__ void search_desc16(SelArea s, uint32_t local, uint32_t top, uint32_t above0, uint32_t kk) {
+  static_assert(PER == 32 || PER == 128, "keys per thread");
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t kk = static_cast<uint32_t>(k);
-  const uint32_t base = s.h16 + 4u * static_cast<uint32_t>(kH16Words - 64 * (tid + 1));
-  uint32_t local = 0;
-  // lanes sit 256 B apart: rotate the 16-B chunk order by lane so each
-  // 8-lane phase of an LDS.128 hits 8 distinct bank groups (else 32-way conflicts)
-#pragma unroll
-  for (int q = 0; q < 16; ++q) {
-    const uint4 u = lds4(base + 16u * ((q + lane) & 15));
-    local += (u.x & 0xffffu) + (u.x >> 16) + (u.y & 0xffffu) + (u.y >> 16) + (u.z & 0xffffu) + (u.z >> 16) +
-             (u.w & 0xffffu) + (u.w >> 16);
-  }
   const uint32_t wsum = __reduce_add_sync(0xffffffffu, local);
   if (lane == 0) s.set_m(M_WSUM + warp, wsum);
   __syncthreads();
@@ -536,9 +567,10 @@ __device__ __noinline__ Cut sel_cut16(int n, int k, SelArea s) {
     const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
     if (lane >= o) inc += t;
   }
-  const int wb = __ffs(__ballot_sync(0xffffffffu, lane < kWarps && inc - tw < kk && kk <= inc)) - 1;
+  const int wb =
+      __ffs(__ballot_sync(0xffffffffu, (lane < kWarps) & (above0 + inc - tw < kk) & (kk <= above0 + inc))) - 1;
   if (warp == wb) {
-    const uint32_t wabove = __shfl_sync(0xffffffffu, inc - tw, wb);
+    const uint32_t wabove = above0 + __shfl_sync(0xffffffffu, inc - tw, wb);
     uint32_t li = local;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -546,15 +578,19 @@ __device__ __noinline__ Cut sel_cut16(int n, int k, SelArea s) {
       if (lane >= o) li += t;
     }
     const uint32_t mine_ex = wabove + li - local;
-    const int ol = __ffs(__ballot_sync(0xffffffffu, mine_ex < kk && kk <= mine_ex + local)) - 1;
-    // the owner thread's 128 keys, scanned by the whole warp: lane l takes
-    // words 63-2l and 62-2l of the owner's range (4 keys, descending)
+    const int ol = __ffs(__ballot_sync(0xffffffffu, (mine_ex < kk) & (kk <= mine_ex + local))) - 1;
     const int tb = warp * 32 + ol;
     const uint32_t above = __shfl_sync(0xffffffffu, mine_ex, ol);
-    const uint32_t wbase = s.h16 + 4u * static_cast<uint32_t>(kH16Words - 64 * (tb + 1));
-    const uint32_t w1 = lds(wbase + 4u * (63 - 2 * lane)), w0 = lds(wbase + 4u * (62 - 2 * lane));
-    const uint32_t c[4] = {w1 >> 16, w1 & 0xffffu, w0 >> 16, w0 & 0xffffu};
-    const uint32_t lsum = c[0] + c[1] + c[2] + c[3];
+    const uint32_t ktop = top - static_cast<uint32_t>(PER) * static_cast<uint32_t>(tb);  // owner's keys: [ktop - PER, ktop)
+    constexpr int KL = PER / 32;  // keys per lane, descending from ktop - 1 - KL * lane
+    uint32_t c[KL];
+    uint32_t lsum = 0;
+#pragma unroll
+    for (int q = 0; q < KL; ++q) {
+      const uint32_t key = ktop - 1u - static_cast<uint32_t>(KL * lane + q);
+      c[q] = (lds(s.h16 + 4u * (key >> 1)) >> (16 * (key & 1u))) & 0xffffu;
+      lsum += c[q];
+    }
     uint32_t linc = lsum;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -562,52 +598,101 @@ __device__ __noinline__ Cut sel_cut16(int n, int k, SelArea s) {
       if (lane >= o) linc += t;
     }
     uint32_t acc = above + linc - lsum;
-    const uint32_t key_top = static_cast<uint32_t>(32768 - 128 * tb - 1) - 4u * lane;  // key of c[0]
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if (acc < kk && kk <= acc + c[q]) {
-        s.set_m(M_BIN, key_top - q);
-        s.set_m(M_ABOVE, acc);
-        s.set_m(M_CNT, c[q]);
-      }
+    for (int q = 0; q < KL; ++q) {
+      const bool hitq = (acc < kk) & (kk <= acc + c[q]);
+      sts_pred(hitq, s.misc + 4u * M_BIN, ktop - 1u - static_cast<uint32_t>(KL * lane + q));
+      sts_pred(hitq, s.misc + 4u * M_ABOVE, acc);
+      sts_pred(hitq, s.misc + 4u * M_CNT, c[q]);
       acc += c[q];
     }
   }
   __syncthreads();
+}
+
+// The exact cut from the 15-bit histogram: the window first (thread t owns
+// 32 keys, 4 LDS.128), the whole histogram only if the cut lies outside it
+// (thread t owns 128 keys).  Ties at the cut key resolved in ascending index
+// order.  Contains __syncthreads.
+__device__ __noinline__ Cut sel_cut16(int n, int k, SelArea s) {
+  if (k <= 0) return Cut{0xffffffffu, 0};
+  if (k >= n) return Cut{0u, INT_MAX};
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t kk = static_cast<uint32_t>(k);
+  if (tid == 0) {
+    s.set_m(M_TCNT, 0u);
+    s.set_m(M_BIN, 0xffffffffu);
+  }
+  const uint32_t over = s.m(M_OVER);  // published by sel_load16's __syncthreads
+  RSP_SEL_STAMP(1);
+  if (over < kk) {
+    static_assert(kThreads * 32 == static_cast<int>(kWinKeys), "window ownership");
+    // threads sit 64 B apart: rotate the chunk order by lane / 2 so each
+    // 8-lane phase of an LDS.128 hits 8 distinct bank groups
+    const uint32_t base = s.h16 + 4u * ((kWinHi - 32u * static_cast<uint32_t>(tid + 1)) >> 1);
+    uint4 u[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) u[q] = lds4(base + 16u * ((q + (lane >> 1)) & 3));
+    uint32_t packed = 0;  // counter pairs summed as words: low halves total <= n < 65536
+#pragma unroll
+    for (int q = 0; q < 4; ++q) packed += u[q].x + u[q].y + u[q].z + u[q].w;
+    search_desc16<32>(s, (packed & 0xffffu) + (packed >> 16), kWinHi, over, kk);
+  } else {
+    __syncthreads();  // M_BIN sentinel visible
+  }
+  RSP_SEL_STAMP(2);
+  if (s.m(M_BIN) == 0xffffffffu) {  // outside the window: the whole histogram
+    static_assert(kThreads * 128 == 32768, "15-bit histogram ownership");
+    const uint32_t base = s.h16 + 4u * static_cast<uint32_t>(kH16Words - 64 * (tid + 1));
+    uint4 u[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) u[q] = lds4(base + 16u * ((q + lane) & 15));
+    uint32_t packed = 0;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) packed += u[q].x + u[q].y + u[q].z + u[q].w;
+    search_desc16<128>(s, (packed & 0xffffu) + (packed >> 16), 32768u, 0u, kk);
+  }
+  RSP_SEL_STAMP(4);
   const uint32_t key15 = s.m(M_BIN);
   const uint32_t need = kk - s.m(M_ABOVE), cnt = s.m(M_CNT);
   const uint32_t T = key15 << 16;  // the exact k-th key (fp32 bits, sign cleared)
   if (need == cnt) return Cut{T, INT_MAX};  // every channel of the key is in S
+  RSP_SEL_STAMP(8);
   // ties: the `need` lowest indices among the `cnt` channels of key15
-  if ((n & 7) == 0) {
+  if (cnt <= 32 && (n & 7) == 0) {
+    // few channels share the key (the common case): packed-pair equality
+    // tests, the rare hits appended to a short list, one warp ranks them
     const int nv = n >> 3;
-    const int v0 = static_cast<int>(static_cast<uint32_t>(nv) * tid / kThreads);
-    const int v1 = static_cast<int>(static_cast<uint32_t>(nv) * (tid + 1) / kThreads);
-    uint32_t mine = 0;
-    for (int v = v0; v < v1; ++v) {
-      const uint4 u = lds4(s.xs + 16u * static_cast<uint32_t>(v));
-      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+    for (int v0 = 0; v0 < nv; v0 += 4 * kThreads) {
+      uint4 u4[4];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) mine += ((w[e >> 1] >> (16 * (e & 1))) & 0x7fffu) == key15;
-    }
-    const uint32_t ex = block_excl_scan(mine, s.misc + 4u * M_SCAN, nullptr);
-    if (ex < need && need <= ex + mine) {
-      uint32_t c = ex;
-      for (int v = v0; v < v1; ++v) {
-        const uint4 u = lds4(s.xs + 16u * static_cast<uint32_t>(v));
-        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-        bool done = false;
+      for (int q = 0; q < 4; ++q) u4[q] = lds4(s.xs + 16u * static_cast<uint32_t>(min(v0 + q * kThreads + tid, nv - 1)));
+      uint32_t hit = 0;  // bit 8q + e: channel 8 v_q + e has the key
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          if (!done && ((w[e >> 1] >> (16 * (e & 1))) & 0x7fffu) == key15 && ++c == need) {
-            s.set_m(M_JLIM, static_cast<uint32_t>(8 * v + e + 1));
-            done = true;
-          }
-        }
-        if (done) break;
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t m = pack8(pair_eq(u4[q].x, key15), pair_eq(u4[q].y, key15), pair_eq(u4[q].z, key15),
+                                 pair_eq(u4[q].w, key15));
+        hit |= (v0 + q * kThreads + tid < nv ? m : 0u) << (8 * q);
+      }
+      while (hit) {  // rare
+        const int bpos = __ffs(hit) - 1;
+        hit &= hit - 1u;
+        const uint32_t pos = atoms_add(s.misc + 4u * M_TCNT, 1u);
+        sts(s.cand + 4u * pos, static_cast<uint32_t>(8 * (v0 + (bpos >> 3) * kThreads + tid) + (bpos & 7)));
       }
     }
+    RSP_SEL_STAMP(6);
+    __syncthreads();
+    RSP_SEL_STAMP(7);
+    if (warp == 0) {
+      const uint32_t j = lane < static_cast<int>(cnt) ? lds(s.cand + 4u * lane) : 0xffffffffu;
+      uint32_t rank = 0;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) rank += __shfl_sync(0xffffffffu, j, i) < j;
+      sts_pred((lane < static_cast<int>(cnt)) & (rank == need - 1), s.misc + 4u * M_JLIM, j + 1);
+    }
   } else {
+    // many ties (e.g. zeros): per-thread contiguous ranges, one block scan
     const int j0 = static_cast<int>(static_cast<uint32_t>(n) * tid / kThreads);
     const int j1 = static_cast<int>(static_cast<uint32_t>(n) * (tid + 1) / kThreads);
     uint32_t mine = 0;
@@ -624,9 +709,9 @@ __device__ __noinline__ Cut sel_cut16(int n, int k, SelArea s) {
     }
   }
   __syncthreads();
+  RSP_SEL_STAMP(5);
   return Cut{T, static_cast<int>(s.m(M_JLIM))};
 }
-
 
 // Deterministic two-list compaction in one sweep: members of range A
 // ([a0, a1), predicate pa) and of range B ([b0, b1), predicate pb), each in
@@ -689,6 +774,102 @@ __device__ __forceinline__ void compact2(SelArea s, int a0, int a1, int b0, int 
     const uint32_t bal = __ballot_sync(0xffffffffu, in);
     if (in) fb(offb + __popc(bal & lt), j);
     offb += __popc(bal);
+  }
+  __syncthreads();
+}
+
+
+// bf16 activations: membership bits of the 8 channels [j8, j8 + 8) (j8 a
+// multiple of 8) -- in S when `in_s`, in S^c otherwise -- restricted to
+// [lo, hi); `u` returns their raw bits.  Packed-pair tests, no branches.
+__device__ __forceinline__ uint32_t chunk_members16(SelArea s, int j8, int lo, int hi, const Cut& cut, bool in_s,
+                                                    uint4& u) {
+  // (chunks past hi load the last in-range vector: every bit is masked off)
+  u = lds4(s.xs + 2u * static_cast<uint32_t>(min(j8, (hi - 1) & ~7)));
+  uint32_t m_in = 0;
+  if (cut.T <= 0x7fff0000u) {  // else S is empty
+    const uint32_t t15 = cut.T >> 16;
+    const uint32_t gt = t15 < 0x7fffu ? pack8(pair_gt(u.x, t15), pair_gt(u.y, t15), pair_gt(u.z, t15), pair_gt(u.w, t15))
+                                      : 0u;
+    const uint32_t eq = pack8(pair_eq(u.x, t15), pair_eq(u.y, t15), pair_eq(u.z, t15), pair_eq(u.w, t15));
+    const int jl = min(max(cut.jlim - j8, 0), 8);  // channels of the vector below jlim
+    m_in = gt | (eq & (0xffu >> (8 - jl)));
+  }
+  const int lo_off = min(max(lo - j8, 0), 8), hi_off = min(max(hi - j8, 0), 8);
+  const uint32_t range = (0xffu >> (8 - hi_off)) & (0xffu << lo_off);
+  return (in_s ? m_in : ~m_in) & range;
+}
+
+// compact2 for bf16 activations, 8 channels per lane per 16-byte load:
+// S-members of [a0, a1) -> fa(p, i, j, bits), S^c-members of [b0, b1) -> fb(p, i, j, bits),
+// each ascending (i = position in its list, bits = the fp32 bits of x_j); f is
+// called for all 8 channels of a lane with p = membership (write only if p).
+// A warp sweeps whole 256-channel chunks; positions inside a chunk come from
+// eight ballots (no shuffle chains).  Two __syncthreads.
+template <class FA, class FB>
+__device__ __forceinline__ void compact2_16(SelArea s, const Cut& cut, int a0, int a1, int b0, int b1, FA&& fa,
+                                            FB&& fb, int* na, int* nb) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int A0 = a0 & ~7, B0 = b0 & ~7;
+  const int ca = a1 > a0 ? (a1 - A0 + 255) >> 8 : 0, cb = b1 > b0 ? (b1 - B0 + 255) >> 8 : 0;
+  const int pera = (ca + kWarps - 1) / kWarps, perb = (cb + kWarps - 1) / kWarps;
+  const int ca0 = min(ca, warp * pera), ca1 = min(ca, (warp + 1) * pera);
+  const int cb0 = min(cb, warp * perb), cb1 = min(cb, (warp + 1) * perb);
+  uint4 u;
+  uint32_t cnta = 0, cntb = 0;
+#pragma unroll 1
+  for (int c = ca0; c < ca1; ++c) cnta += __popc(chunk_members16(s, A0 + 256 * c + 8 * lane, a0, a1, cut, true, u));
+#pragma unroll 1
+  for (int c = cb0; c < cb1; ++c) cntb += __popc(chunk_members16(s, B0 + 256 * c + 8 * lane, b0, b1, cut, false, u));
+  cnta = __reduce_add_sync(0xffffffffu, cnta);
+  cntb = __reduce_add_sync(0xffffffffu, cntb);
+  if (lane == 0) {
+    s.set_m(M_LISTA + warp, cnta);
+    s.set_m(M_LISTB + warp, cntb);
+  }
+  __syncthreads();
+  const uint4 la0 = lds4(s.misc + 4u * M_LISTA), la1 = lds4(s.misc + 4u * (M_LISTA + 4));
+  const uint4 lb0 = lds4(s.misc + 4u * M_LISTB), lb1 = lds4(s.misc + 4u * (M_LISTB + 4));
+  const uint32_t wa[8] = {la0.x, la0.y, la0.z, la0.w, la1.x, la1.y, la1.z, la1.w};
+  const uint32_t wb[8] = {lb0.x, lb0.y, lb0.z, lb0.w, lb1.x, lb1.y, lb1.z, lb1.w};
+  uint32_t offa = 0, offb = 0, tota = 0, totb = 0;
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) {
+    offa += w < warp ? wa[w] : 0u;
+    offb += w < warp ? wb[w] : 0u;
+    tota += wa[w];
+    totb += wb[w];
+  }
+  *na = static_cast<int>(tota);
+  *nb = static_cast<int>(totb);
+  const uint32_t lt = lanemask_lt();
+  auto emit = [&](int j8, uint32_t m, const uint4& uu, uint32_t& off, auto&& f) {
+    uint32_t pre = 0, tot = 0;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const uint32_t bal = __ballot_sync(0xffffffffu, (m >> e) & 1u);
+      pre += __popc(bal & lt);
+      tot += __popc(bal);
+    }
+    const uint32_t w[4] = {uu.x, uu.y, uu.z, uu.w};
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const uint32_t bits = (e & 1) ? (w[e >> 1] & 0xffff0000u) : (w[e >> 1] << 16);
+      f(((m >> e) & 1u) != 0, static_cast<int>(off + pre + __popc(m & ((1u << e) - 1u))), j8 + e, bits);
+    }
+    off += tot;
+  };
+#pragma unroll 1
+  for (int c = ca0; c < ca1; ++c) {
+    const int j8 = A0 + 256 * c + 8 * lane;
+    const uint32_t m = chunk_members16(s, j8, a0, a1, cut, true, u);
+    emit(j8, m, u, offa, fa);
+  }
+#pragma unroll 1
+  for (int c = cb0; c < cb1; ++c) {
+    const int j8 = B0 + 256 * c + 8 * lane;
+    const uint32_t m = chunk_members16(s, j8, b0, b1, cut, false, u);
+    emit(j8, m, u, offb, fb);
   }
   __syncthreads();
 }

@@ -82,6 +82,13 @@ def _selector_inputs(rng, n):
     yield "signed_zeros", z
     yield "sign_dups", np.repeat(rng.standard_normal((n + 1) // 2).astype(np.float32), 2)[:n] * \
         np.where(np.arange(n) % 2, -1, 1).astype(np.float32)
+    # magnitudes outside the bf16 selector's first histogram window [2^-40, 2^24)
+    yield "huge", (rng.standard_normal(n) * 2.0 ** 30).astype(np.float32)
+    yield "tiny", (rng.standard_normal(n) * 2.0 ** -60).astype(np.float32)
+    yield "straddle", np.where(rng.random(n) < 0.3, rng.standard_normal(n) * 2.0 ** 40,
+                               rng.standard_normal(n) * 2.0 ** -50).astype(np.float32)
+    # a few (<= 32) channels per repeated value: the short-list tie path
+    yield "few_dups", rng.choice(rng.standard_normal(max(1, n // 6)), size=n).astype(np.float32)
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
