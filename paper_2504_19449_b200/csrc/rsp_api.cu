@@ -144,6 +144,7 @@ struct rsp_stack {
   cudaGraphExec_t exec = nullptr;
   void* ws = nullptr;
   LinDesc* descs = nullptr;  // device array
+  void* plans = nullptr;     // device plan table [count][grid]
   StackParams params = {};   // the captured launch (re-launched by the debug trace)
   int es = 2, grid = 1;
   bool x_bf16 = false;
@@ -955,6 +956,11 @@ rsp_status rsp_stack_create_ex(const rsp_linear* const* layers, uint32_t count, 
   if (e == cudaSuccess) e = cudaMalloc(&s->descs, sizeof(LinDesc) * count);
   if (e == cudaSuccess) e = cudaMemcpy(s->descs, descs.data(), sizeof(LinDesc) * count, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+  const int knobs = env_int("RSP_KNOBS", 0);
+  if (e == cudaSuccess) e = cudaMalloc(&s->plans, static_cast<size_t>(count) * grid * rsp::kPlanBytes);
+  if (e == cudaSuccess)
+    e = rsp::launch_plans(s->descs, static_cast<int>(count), grid, knobs, abuf, h0->es, s->plans, cs);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
   if (e == cudaSuccess) e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
   if (e == cudaSuccess) {
     StackParams p = {};
@@ -969,7 +975,8 @@ rsp_status rsp_stack_create_ex(const rsp_linear* const* layers, uint32_t count, 
     p.bbuf_bytes = bbuf;
     p.nb_pad = nb_pad;
     p.deterministic = det ? 1 : 0;
-    p.knobs = env_int("RSP_KNOBS", 0);
+    p.knobs = knobs;
+    p.plans = s->plans;
     bind_workspace(&p, s->ws, wl);
     s->params = p;
     s->es = h0->es;
@@ -1022,6 +1029,7 @@ void rsp_stack_destroy(rsp_stack* s) {
   if (s->graph) cudaGraphDestroy(s->graph);
   cudaFree(s->ws);
   cudaFree(s->descs);
+  cudaFree(s->plans);
   delete s;
 }
 

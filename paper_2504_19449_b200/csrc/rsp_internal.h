@@ -12,6 +12,7 @@ constexpr unsigned kTAccCap = 2048;  // floats per stage-1 t buffer (r_pad <= 20
 constexpr unsigned kSlotWords = 32;  // per-linear barrier slot: [0] y arrivals, [1] t arrivals, [2..] tickets
 constexpr unsigned kMaxTickets = kSlotWords - 2;
 constexpr unsigned kWsHdrBytes = 256;  // [0] launch epoch, [1] CTAs done in this launch
+constexpr int kPlanBytes = 96;        // one (linear, CTA) entry of a stack's plan table
 
 // Flags of one linear in a stack launch.
 constexpr int kLinWaitPrev = 1;  // its x depends on the previous group's y: wait for that group's CTAs first
@@ -50,6 +51,7 @@ struct StackParams {
   int pdl;                         // 1: launched with programmatic dependent launch
   int knobs;                       // experiment switches (env RSP_KNOBS): 1 no W prefetch, 2 no A/B prefetch
   long long* trace;                // debug: [grid][16] phase timestamps of the last linear (null in production)
+  const void* plans;               // [count][grid] per-CTA plans (plan_kernel), or null: computed in the kernel
 };
 
 // Workspace byte layout for `slots` linears; t_part/y_part sized for the
@@ -74,6 +76,9 @@ size_t stack_smem_bytes(int n_max, bool x_bf16, int cap_w, int cap_u, int cap_a,
                         int bbuf_bytes = 0);
 
 cudaError_t stack_set_smem(size_t smem);
+// Fill a stack's plan table (count x grid entries of kPlanBytes) from its device descriptors.
+cudaError_t launch_plans(const LinDesc* descs, int count, int grid, int knobs, int obuf_bytes, int elem_bytes,
+                         void* out, cudaStream_t stream);
 cudaError_t launch_stack(const StackParams& p, int elem_bytes, bool x_bf16, int grid, size_t smem,
                          cudaStream_t stream, bool pdl);
 

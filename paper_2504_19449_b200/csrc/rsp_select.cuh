@@ -42,7 +42,7 @@ namespace rsp {
 constexpr int kBins = 4096;   // level-1 histogram: key bits 30..19 (exponent + 4 mantissa bits)
 constexpr int kH16Words = 16384;  // 32768 bf16 keys x 16-bit counters (n <= 65535)
 constexpr int kCandWords = 2048;  // gathered boundary-bin members (more: refine over all of x)
-constexpr int kMiscWords = 128;
+constexpr int kMiscWords = 208;
 
 // misc[] word slots
 enum : int {
@@ -55,7 +55,10 @@ enum : int {
   M_LISTB = 48,  // [48, 64): per-warp member counts, list B
   M_TCNT = 23,   // tie members appended so far (fast tie path)
   M_OVER = 24,   // bf16 keys >= kWinHi (sel_load16)
-  M_PLAN = 96,   // [96, 128): the stack kernel's per-CTA plan of the next linear
+  M_PLAN = 96,    // [96, 120): the stack kernel's per-CTA plan, slot 0
+  M_PLAN1 = 128,  // [128, 152): plan slot 1
+  M_DESC0 = 160,  // [160, 184): staged linear descriptor, slot 0
+  M_DESC1 = 184,  // [184, 208): slot 1
 };
 
 struct Cut {
