@@ -24,6 +24,7 @@
 #include "rsp_internal.h"
 
 using rsp::LinDesc;
+using rsp::BatchParams;
 using rsp::StackParams;
 using rsp::WsLayout;
 
@@ -583,7 +584,8 @@ rsp_status rsp_linear_info_get(const rsp_linear* h, rsp_linear_info* o) {
 }
 
 size_t rsp_linear_workspace_size(const rsp_linear* h, uint32_t /*batch*/) {
-  return h ? h->plan.ws_bytes : 0;
+  // single-token area, then the batch > 1 area (counters, cuts, t accumulator)
+  return h ? h->plan.ws_bytes + rsp::kBatchWsBytes(static_cast<int>(h->r_pad)) : 0;
 }
 
 rsp_status rsp_workspace_init(void* ws, size_t bytes, void* stream) {
@@ -591,12 +593,76 @@ rsp_status rsp_workspace_init(void* ws, size_t bytes, void* stream) {
   return RSP_OK;
 }
 
+namespace {
+
+// Decomposition of a batched forward: 64 x cw output columns per CTA, ks
+// channel splits, the most CTAs (<= #SMs) whose per-CTA activation slab
+// (B x n/ks bf16) and shared-memory carve-up fit.
+bool batch_plan(const rsp_linear* h, int B, const DevProps& dp, BatchParams* out) {
+  const int n = static_cast<int>(h->m_in), m = static_cast<int>(h->m), sms = std::max(1, dp.sms);
+  bool found = false;
+  BatchParams best = {};
+  for (int cw = 1; cw <= 8; cw *= 2) {
+    const int tiles = (m + 64 * cw - 1) / (64 * cw);
+    if (tiles > sms) continue;
+    const int ks = std::max(1, std::min({sms / tiles, 32, n}));
+    BatchParams p = {};
+    p.n = n;
+    p.m = m;
+    p.m_pad = static_cast<int>(h->m_pad);
+    p.r = static_cast<int>(h->rank);
+    p.r_pad = static_cast<int>(h->r_pad);
+    p.k = static_cast<int>(h->k);
+    p.B = B;
+    p.cw = cw;
+    p.ks = ks;
+    p.grid = tiles * ks;
+    p.range_max = (n + ks - 1) / ks + 1;
+    p.slice_max = (n + p.grid - 1) / p.grid + 1;
+    p.na_max = (p.r + ks - 1) / ks + 1;
+    if (2 * B * p.range_max > 96 * 1024) continue;
+    if (rsp::batch_smem_bytes(p) > static_cast<size_t>(dp.smem_optin)) continue;
+    if (!found || p.grid > best.grid) {
+      best = p;
+      found = true;
+    }
+  }
+  if (found) *out = best;
+  return found;
+}
+
+}  // namespace
+
 rsp_status rsp_linear_forward(const rsp_linear* h, const void* x, rsp_dtype xdt, float* y,
                               uint32_t batch, void* ws, size_t ws_bytes, void* stream) {
   if (!h || !x || !y) return fail(RSP_E_USAGE, "null handle or buffer");
   if (rsp_status st = check_x_dtype(xdt)) return st;
   if (batch == 0) return RSP_OK;
   DeviceGuard g(h->device);
+  // batch > 1, bf16 weights and activations: one pass over the union of the
+  // tokens' selected rows on the tensor cores (rsp_batch.cu)
+  BatchParams bp;
+  if (batch > 1 && batch <= static_cast<uint32_t>(rsp::kBatchMax) && h->es == 2 && xdt == RSP_BF16 &&
+      !h->deterministic && !env_int("RSP_BATCH_LOOP", 0) &&
+      batch_plan(h, static_cast<int>(batch), device_props(h->device), &bp)) {
+    if (!ws || ws_bytes < rsp_linear_workspace_size(h, batch))
+      return fail(RSP_E_USAGE, "workspace of %zu bytes is smaller than the %zu required", ws_bytes,
+                  rsp_linear_workspace_size(h, batch));
+    uint8_t* area = static_cast<uint8_t*>(ws) + h->plan.ws_bytes;
+    bp.Wt = h->Wt;
+    bp.At = h->At;
+    bp.Bt = h->Bt;
+    bp.x = x;
+    bp.y = y;
+    bp.ctr = reinterpret_cast<unsigned*>(area);
+    bp.cuts = reinterpret_cast<int2*>(area + 256);
+    bp.t_acc = reinterpret_cast<float*>(area + 512);
+    const cudaStream_t cs = static_cast<cudaStream_t>(stream);
+    if (bp.ks > 1) RSP_CUDA(cudaMemsetAsync(y, 0, sizeof(float) * h->m * batch, cs));
+    cudaError_t e = rsp::launch_batch(bp, true, cs);
+    if (e != cudaSuccess) return fail(RSP_E_CUDA, "batched forward launch: %s", cudaGetErrorString(e));
+    return RSP_OK;
+  }
   const size_t xs = static_cast<size_t>(h->m_in) * (xdt == RSP_BF16 ? 2 : 4);
   for (uint32_t t = 0; t < batch; ++t) {
     rsp_status st = launch_forward(h, static_cast<const uint8_t*>(x) + t * xs, xdt, y + static_cast<size_t>(t) * h->m,

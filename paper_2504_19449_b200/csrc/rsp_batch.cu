@@ -1,0 +1,451 @@
+// rsp_batch.cu -- the batch > 1 forward of one R-Sparse linear (config 3,
+// SURVEY §8(f)#1), bf16 weights and activations.
+//
+// Reference semantics: B independent `forward` calls (SPEC.md:325,
+// layer.cpp:95-123): token b keeps its own top-k set S_b.  Restated for one
+// pass over the weights:
+//
+//   U      = union of the S_b                     (W rows read once per batch)
+//   Y[b]   = sum_{j in U} [j in S_b] x_bj W[:, j]  +  A_r t_b
+//   t_b    = sum_{j not in S_b} x_bj B_r[:, j]
+//
+// Every product is a gathered-row contraction with per-token coefficients,
+// run on the tensor cores (mma.sync m16n8k16 bf16 -> fp32; the 16 tokens are
+// the M dimension, output columns N, channels K): each warp loads 16 rows x
+// 64 columns per step with 16-byte loads (4 steps in flight), stages them
+// through a swizzled shared tile and feeds ldmatrix.trans -> mma.  At <= 16
+// FLOP/byte the op stays HBM-bound; the tensor cores only keep the issue rate
+// (8 x 16 FMAs per 16-byte load on CUDA cores) off the critical path.
+//
+// Kernels:
+//   batch_cut_kernel      one CTA per token: the exact cut (T, jlim) of token b
+//                         (the same selector as the batch-1 path);
+//   batch_forward_kernel  grid = column tiles x channel splits (<= #SMs, one
+//                         CTA per SM): lists of U and of each token's
+//                         complement, stage 1 into an L2 t accumulator, a
+//                         counting barrier, W rows, stage 2, combine.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "rsp_device.cuh"
+#include "rsp_internal.h"
+#include "rsp_select.cuh"
+
+namespace rsp {
+
+namespace {
+
+constexpr int kColsPerWarp = 64;  // 8 n-blocks of the m16n8k16 product
+constexpr int kStage = 16;        // rows per mma step (K)
+constexpr int kDepth = 4;         // steps in flight per warp
+
+__device__ __forceinline__ int bpart(int total, int i, int parts) {
+  return static_cast<int>(static_cast<uint32_t>(total) * static_cast<uint32_t>(i) / static_cast<uint32_t>(parts));
+}
+
+__device__ __forceinline__ void ldsm_x4_trans(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr)
+               : "memory");
+}
+
+__device__ __forceinline__ void mma_bf16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(uint32_t lo, uint32_t hi) { return (lo & 0xffffu) | (hi << 16); }
+
+// One warp's accumulator: 16 tokens x 64 columns (n-block q: token g / g+8,
+// columns 8q + 2t, 8q + 2t + 1 with g = lane / 4, t = lane % 4).
+struct Frag {
+  float d[8][4];
+};
+
+// A step: rows kk = 0..15 of a 16 x 64 bf16 tile.  Lane l loads chunk
+// (l & 7) of rows (l >> 3) + 4 i, i < 4.
+struct StepLoad {
+  uint4 u[4];
+};
+
+// Stage the step into the warp's swizzled tile (chunk c of row kk at
+// c ^ (kk & 7)) and accumulate coef(16 x 16) x tile into D.
+__device__ __forceinline__ void mma_step(Frag& D, const StepLoad& s, uint32_t tile, const uint32_t (&a)[4],
+                                         int lane) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int kk = (lane >> 3) + 4 * i, c = lane & 7;
+    sts4(tile + static_cast<uint32_t>(kk * 8 + (c ^ (kk & 7))) * 16u, s.u[i]);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {  // n-blocks 2p, 2p + 1
+    const int kk = (lane & 7) + 8 * ((lane >> 3) & 1), cc = 2 * p + (lane >> 4);
+    uint32_t r0, r1, r2, r3;
+    ldsm_x4_trans(tile + static_cast<uint32_t>(kk * 8 + (cc ^ (kk & 7))) * 16u, r0, r1, r2, r3);
+    mma_bf16(D.d[2 * p], a, r0, r1);
+    mma_bf16(D.d[2 * p + 1], a, r2, r3);
+  }
+  __syncwarp();  // the tile is rewritten by the next step
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Kernel 1: token blockIdx.x's exact cut.
+// ---------------------------------------------------------------------------
+template <bool XBF>
+__global__ void __launch_bounds__(kThreads, 1)
+    batch_cut_kernel(const void* x, int n, int k, int2* cuts, uint32_t zero) {
+  extern __shared__ __align__(16) uint8_t smem_bc[];
+  const uint32_t sb = smem_base_pinned(smem_bc);
+  SelArea S;
+  S.h1 = sb;
+  S.cand = S.h1 + 4u * kBins;
+  S.h2a = S.cand + 4u * kCandWords;
+  S.h2b = S.h2a + 4u * 256;
+  S.misc = S.h2b + 4u * 256;
+  S.h16 = S.misc + 4u * kMiscWords;
+  S.xs = S.h16 + 4u * kH16Words;
+  S.zero = zero;
+  const uint8_t* xb = static_cast<const uint8_t*>(x) + static_cast<size_t>(blockIdx.x) * n * (XBF ? 2 : 4);
+  Cut cut;
+  if constexpr (XBF) {
+    sel_clear16(S);
+    __syncthreads();
+    sel_load16(xb, n, S);
+    cut = sel_cut16(n, k, S);
+  } else {
+    sel_clear(S);
+    __syncthreads();
+    sel_load<false>(xb, n, S, true);
+    cut = sel_cut<false>(n, k, S);
+  }
+  if (threadIdx.x == 0) cuts[blockIdx.x] = make_int2(static_cast<int>(cut.T), cut.jlim);
+}
+
+// ---------------------------------------------------------------------------
+// Kernel 2: the batched forward of one linear.
+// ---------------------------------------------------------------------------
+struct BatchSmem {
+  uint32_t cuts, xs, xu, lw, lu, misc, tiles, tco, red, total;
+  __host__ __device__ static uint32_t up(uint32_t v) { return (v + 15u) / 16u * 16u; }
+  __host__ __device__ static BatchSmem make(const BatchParams& P) {
+    BatchSmem L;
+    uint32_t o = 0;
+    L.cuts = o;
+    o += 8u * kBatchMax;
+    L.misc = o;
+    o += 4u * 96;
+    L.xs = o;  // [B][range] bf16
+    o = up(o + 2u * P.B * P.range_max);
+    L.xu = o;  // [B][slice] bf16
+    o = up(o + 2u * P.B * P.slice_max);
+    L.lw = o;  // {channel, token mask} of U in the W range
+    o = up(o + 8u * P.range_max);
+    L.lu = o;  // {channel, token mask} of the complements in the stage-1 slice
+    o = up(o + 8u * P.slice_max);
+    L.tiles = o;  // per warp: one 16 x 64 bf16 step tile
+    o += static_cast<uint32_t>(kWarps) * kStage * 128u;
+    L.tco = o;  // t of the CTA's A rows: [hi/lo][B][na] bf16
+    o = up(o + 4u * P.B * P.na_max);
+    L.red = o;  // cross-group reduction [RG][16][64 CW] fp32
+    o += 4u * 16u * static_cast<uint32_t>(kWarps) * kColsPerWarp;
+    L.total = o;
+    return L;
+  }
+};
+
+__global__ void __launch_bounds__(kThreads, 1) batch_forward_kernel(const BatchParams P) {
+  extern __shared__ __align__(16) uint8_t smem_bf[];
+  const BatchSmem L = BatchSmem::make(P);
+  const uint32_t sb = smem_base_pinned(smem_bf);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
+  const int bid = blockIdx.x, NB = gridDim.x, KS = P.ks, B = P.B;
+  const int ct = bid / KS, ks = bid - ct * KS;
+  const int CW = P.cw, RG = kWarps / CW, cw = warp % CW, rg = warp / CW;
+  const int wc0 = bpart(P.n, ks, KS), wc1 = bpart(P.n, ks + 1, KS), rw = wc1 - wc0;
+  const int uc0 = bpart(P.n, bid, NB), uc1 = bpart(P.n, bid + 1, NB), ru = uc1 - uc0;
+  const bool has_lr = P.r > 0 && P.k < P.n;
+  const int alo = has_lr ? bpart(P.r, ks, KS) : 0, ahi = has_lr ? bpart(P.r, ks + 1, KS) : 0, na = ahi - alo;
+  const int colw = ct * kColsPerWarp * CW + cw * kColsPerWarp;  // this warp's first output column
+  const uint32_t tile = sb + L.tiles + static_cast<uint32_t>(warp) * kStage * 128u;
+  const uint64_t pol = l2_evict_first_policy();
+
+  SelArea S{};  // compact2 scratch (misc counters)
+  S.misc = sb + L.misc;
+
+  // ---- cuts and the activations of the CTA's channel ranges ----
+  if (tid < B) {
+    const int2 c = P.cuts[tid];
+    sts2(sb + L.cuts + 8u * tid, static_cast<uint32_t>(c.x), static_cast<uint32_t>(c.y));
+  }
+  const uint16_t* x16 = static_cast<const uint16_t*>(P.x);
+  for (int b = 0; b < B; ++b) {
+    for (int jj = tid; jj < rw; jj += kThreads)
+      asm volatile("st.shared.u16 [%0], %1;" ::"r"(sb + L.xs + 2u * (b * P.range_max + jj)),
+                   "h"(x16[static_cast<size_t>(b) * P.n + wc0 + jj]) : "memory");
+    for (int jj = tid; jj < ru; jj += kThreads)
+      asm volatile("st.shared.u16 [%0], %1;" ::"r"(sb + L.xu + 2u * (b * P.slice_max + jj)),
+                   "h"(x16[static_cast<size_t>(b) * P.n + uc0 + jj]) : "memory");
+  }
+  __syncthreads();
+  // token mask of channel j (x row base `xr`, offset jj): bit b = j in S_b
+  auto in_mask = [&](uint32_t xr, int stride, int jj, int j) {
+    uint32_t m = 0;
+    for (int b = 0; b < B; ++b) {
+      const uint2 c = lds2(sb + L.cuts + 8u * b);
+      const uint32_t key = (lds_u16(xr + 2u * (b * stride + jj)) << 16) & 0x7fffffffu;
+      m |= static_cast<uint32_t>(in_cut(key, j, Cut{c.x, static_cast<int>(c.y)})) << b;
+    }
+    return m;
+  };
+  const uint32_t all = (B >= 32) ? 0xffffffffu : ((1u << B) - 1u);
+  int nW = 0, nU = 0;
+  compact2(
+      S, wc0, wc1, uc0, uc1, [&](int j) { return in_mask(sb + L.xs, P.range_max, j - wc0, j) != 0u; },
+      [&](int j) { return has_lr && in_mask(sb + L.xu, P.slice_max, j - uc0, j) != all; },
+      [&](int i, int j) { sts2(sb + L.lw + 8u * i, static_cast<uint32_t>(j), in_mask(sb + L.xs, P.range_max, j - wc0, j)); },
+      [&](int i, int j) {
+        sts2(sb + L.lu + 8u * i, static_cast<uint32_t>(j), all & ~in_mask(sb + L.xu, P.slice_max, j - uc0, j));
+      },
+      &nW, &nU);
+
+  // A fragment of gathered rows: coef(m, kk) = mask_m ? x_m[row kk] : 0,
+  // rows from list entries e0 + stride * kk (kk < 16, beyond cnt: 0).
+  auto frag_list = [&](uint32_t list, int e0, int stride, int cnt, uint32_t xr, int xstride, int jbase,
+                       uint32_t (&a)[4]) {
+    uint32_t lo[2][2], hi[2][2];  // [row pair 2t / 2t+8][token g / g+8] as (k, k+1) halves
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int kk = 2 * t4 + 8 * h + q;
+        const int e = e0 + stride * kk;
+        const bool ok = e < cnt;
+        const uint2 ent = lds2(list + 8u * static_cast<uint32_t>(ok ? e : 0));
+        const int jj = static_cast<int>(ent.x) - jbase;
+        const uint32_t v0 = ((ent.y >> g) & 1u) && ok && g < B ? lds_u16(xr + 2u * (g * xstride + jj)) : 0u;
+        const uint32_t v1 =
+            ((ent.y >> (g + 8)) & 1u) && ok && g + 8 < B ? lds_u16(xr + 2u * ((g + 8) * xstride + jj)) : 0u;
+        if (q == 0) {
+          lo[h][0] = v0;
+          lo[h][1] = v1;
+        } else {
+          hi[h][0] = v0;
+          hi[h][1] = v1;
+        }
+      }
+    }
+    a[0] = pack_bf16(lo[0][0], hi[0][0]);
+    a[1] = pack_bf16(lo[0][1], hi[0][1]);
+    a[2] = pack_bf16(lo[1][0], hi[1][0]);
+    a[3] = pack_bf16(lo[1][1], hi[1][1]);
+  };
+  // Loads of one step: rows from `rowaddr(kk)` (16-B aligned segment start),
+  // chunks >= vch clamped to chunk 0 (their columns are discarded).
+  auto load_step = [&](StepLoad& s, auto&& rowaddr, int vch) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int kk = (lane >> 3) + 4 * i, c = lane & 7;
+      s.u[i] = ldg_stream_ef(static_cast<const uint8_t*>(rowaddr(kk)) + 16 * (c < vch ? c : 0), pol);
+    }
+  };
+  auto zero_frag = [&](Frag& D) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) D.d[q][e] = 0.f;
+  };
+  // Run `nsteps` steps with kDepth in flight: rows(step, kk) -> address, coef(step, a).
+  auto run_steps = [&](Frag& D, int nsteps, auto&& rowaddr_of, auto&& coef_of, int vch) {
+    StepLoad s[kDepth];
+#pragma unroll
+    for (int d = 0; d < kDepth; ++d)
+      if (d < nsteps) load_step(s[d], [&](int kk) { return rowaddr_of(d, kk); }, vch);
+    for (int st0 = 0; st0 < nsteps; st0 += kDepth) {
+#pragma unroll
+      for (int d = 0; d < kDepth; ++d) {
+        const int st = st0 + d;
+        if (st < nsteps) {
+          uint32_t a[4];
+          coef_of(st, a);
+          mma_step(D, s[d], tile, a, lane);
+          if (st + kDepth < nsteps) load_step(s[d], [&](int kk) { return rowaddr_of(st + kDepth, kk); }, vch);
+        }
+      }
+    }
+  };
+
+  const __nv_bfloat16* Wt = static_cast<const __nv_bfloat16*>(P.Wt);
+  const __nv_bfloat16* At = static_cast<const __nv_bfloat16*>(P.At);
+  const __nv_bfloat16* Bt = static_cast<const __nv_bfloat16*>(P.Bt);
+
+  // ---- stage 1: t_b += sum over the slice's complement rows (all r columns) ----
+  if (has_lr) {
+    const int nch = (P.r_pad + kColsPerWarp - 1) / kColsPerWarp;
+    const int nsteps = (nU + kStage - 1) / kStage;
+    for (int q = warp; q < nch && nU > 0; q += kWarps) {
+      Frag D;
+      zero_frag(D);
+      const int c0 = q * kColsPerWarp;
+      const int vch = min(8, (P.r_pad - c0) / 8);
+      run_steps(
+          D, nsteps,
+          [&](int st, int kk) {
+            const int e = min(st * kStage + kk, nU - 1);
+            const uint32_t j = lds(sb + L.lu + 8u * static_cast<uint32_t>(e));
+            return static_cast<const void*>(Bt + static_cast<size_t>(j) * P.r_pad + c0);
+          },
+          [&](int st, uint32_t(&a)[4]) { frag_list(sb + L.lu, st * kStage, 1, nU, sb + L.xu, P.slice_max, uc0, a); },
+          vch);
+#pragma unroll
+      for (int nb = 0; nb < 8; ++nb) {
+        const int c = c0 + 8 * nb + 2 * t4;
+        if (c < P.r_pad) {
+          if (g < B) {
+            red_add_f32(P.t_acc + static_cast<size_t>(g) * P.r_pad + c, D.d[nb][0]);
+            red_add_f32(P.t_acc + static_cast<size_t>(g) * P.r_pad + c + 1, D.d[nb][1]);
+          }
+          if (g + 8 < B) {
+            red_add_f32(P.t_acc + static_cast<size_t>(g + 8) * P.r_pad + c, D.d[nb][2]);
+            red_add_f32(P.t_acc + static_cast<size_t>(g + 8) * P.r_pad + c + 1, D.d[nb][3]);
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (tid == 0) red_release_add(P.ctr, 1u);
+
+  // ---- W rows of U (this warp: row group rg, columns [colw, colw + 64)) ----
+  Frag D;
+  zero_frag(D);
+  {
+    const int vch = max(0, min(8, (P.m_pad - colw) / 8));
+    const int mine = nW > rg ? (nW - rg + RG - 1) / RG : 0;  // entries rg, rg + RG, ...
+    const int nsteps = (mine + kStage - 1) / kStage;
+    if (vch > 0)
+      run_steps(
+          D, nsteps,
+          [&](int st, int kk) {
+            const int e = rg + RG * min(st * kStage + kk, mine - 1);
+            const uint32_t j = lds(sb + L.lw + 8u * static_cast<uint32_t>(e));
+            return static_cast<const void*>(Wt + static_cast<size_t>(j) * P.m_pad + colw);
+          },
+          [&](int st, uint32_t(&a)[4]) {
+            frag_list(sb + L.lw, rg + RG * st * kStage, RG, nW, sb + L.xs, P.range_max, wc0, a);
+          },
+          vch);
+  }
+
+  // ---- t barrier, then stage 2 over the A_r^T rows [alo, ahi) ----
+  if (has_lr) {
+    if (tid == 0) spin_until_count(P.ctr, static_cast<unsigned>(NB));
+    __syncthreads();
+    // t -> bf16 hi + lo (t ~= hi + lo to ~2^-16 relative), [hi/lo][b][c - alo]
+    for (int i = tid; i < B * na; i += kThreads) {
+      const int b = i / na, c = i - b * na;
+      const float v = __ldcg(P.t_acc + static_cast<size_t>(b) * P.r_pad + alo + c);
+      const __nv_bfloat16 h = __float2bfloat16_rn(v);
+      const __nv_bfloat16 l = __float2bfloat16_rn(v - __bfloat162float(h));
+      asm volatile("st.shared.u16 [%0], %1;" ::"r"(sb + L.tco + 2u * (b * P.na_max + c)),
+                   "h"(__bfloat16_as_ushort(h)) : "memory");
+      asm volatile("st.shared.u16 [%0], %1;" ::"r"(sb + L.tco + 2u * (B * P.na_max + b * P.na_max + c)),
+                   "h"(__bfloat16_as_ushort(l)) : "memory");
+    }
+    __syncthreads();
+    const int vch = max(0, min(8, (P.m_pad - colw) / 8));
+    const int steps_all = (na + kStage - 1) / kStage;
+    const int mine = steps_all > rg ? (steps_all - rg + RG - 1) / RG : 0;  // steps rg, rg + RG, ...
+    for (int part_ = 0; part_ < 2 && vch > 0; ++part_) {  // hi, then lo coefficients
+      const uint32_t tc = sb + L.tco + 2u * static_cast<uint32_t>(part_ * B * P.na_max);
+      run_steps(
+          D, mine,
+          [&](int st, int kk) {
+            const int c = min((rg + RG * st) * kStage + kk, na - 1);
+            return static_cast<const void*>(At + static_cast<size_t>(alo + c) * P.m_pad + colw);
+          },
+          [&](int st, uint32_t(&a)[4]) {
+            const int cb = (rg + RG * st) * kStage;
+            uint32_t v[2][2][2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+              for (int tk = 0; tk < 2; ++tk)
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                  const int c = cb + 2 * t4 + 8 * h + q, m = g + 8 * tk;
+                  v[h][tk][q] = (c < na && m < B) ? lds_u16(tc + 2u * (m * P.na_max + c)) : 0u;
+                }
+            a[0] = pack_bf16(v[0][0][0], v[0][0][1]);
+            a[1] = pack_bf16(v[0][1][0], v[0][1][1]);
+            a[2] = pack_bf16(v[1][0][0], v[1][0][1]);
+            a[3] = pack_bf16(v[1][1][0], v[1][1][1]);
+          },
+          vch);
+    }
+  }
+
+  // ---- combine the row groups, then y (split-K reductions at L2) ----
+  const uint32_t red = sb + L.red;
+  const int tcols = kColsPerWarp * CW;
+#pragma unroll
+  for (int nb = 0; nb < 8; ++nb) {
+    const int c = cw * kColsPerWarp + 8 * nb + 2 * t4;
+    sts2(red + 4u * ((rg * 16 + g) * tcols + c), __float_as_uint(D.d[nb][0]), __float_as_uint(D.d[nb][1]));
+    sts2(red + 4u * ((rg * 16 + g + 8) * tcols + c), __float_as_uint(D.d[nb][2]), __float_as_uint(D.d[nb][3]));
+  }
+  __syncthreads();
+  const int col0 = ct * tcols;
+  for (int i = tid; i < B * tcols; i += kThreads) {
+    const int b = i / tcols, c = i - b * tcols;
+    if (col0 + c >= P.m) continue;
+    float s = 0.f;
+    for (int q = 0; q < RG; ++q) s += ldsf(red + 4u * ((q * 16 + b) * tcols + c));
+    float* yp = P.y + static_cast<size_t>(b) * P.m + col0 + c;
+    if (KS > 1)
+      red_add_f32(yp, s);
+    else
+      *yp = s;
+  }
+
+  // ---- the last CTA leaves the t accumulator and the counters zero ----
+  __syncthreads();
+  if (tid == 0) S.set_m(0, atom_add_acq_rel_gpu(P.ctr + 1, 1u) == static_cast<unsigned>(NB - 1));
+  __syncthreads();
+  if (S.m(0)) {
+    for (int i = tid; i < B * P.r_pad; i += kThreads) P.t_acc[i] = 0.f;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      P.ctr[0] = 0u;
+      P.ctr[1] = 0u;
+    }
+  }
+}
+
+size_t batch_smem_bytes(const BatchParams& p) { return BatchSmem::make(p).total; }
+
+cudaError_t launch_batch(const BatchParams& p, bool x_bf16, cudaStream_t stream) {
+  if (!x_bf16) return cudaErrorInvalidValue;
+  const size_t cut_smem = select_smem_bytes(p.n, true);
+  cudaError_t e = cudaFuncSetAttribute(batch_cut_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(cut_smem));
+  if (e != cudaSuccess) return e;
+  batch_cut_kernel<true><<<p.B, kThreads, cut_smem, stream>>>(p.x, p.n, p.k, p.cuts, 0u);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const size_t smem = batch_smem_bytes(p);
+  e = cudaFuncSetAttribute(batch_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  batch_forward_kernel<<<p.grid, kThreads, smem, stream>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace rsp

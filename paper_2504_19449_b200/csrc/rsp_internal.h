@@ -82,6 +82,25 @@ cudaError_t launch_plans(const LinDesc* descs, int count, int grid, int knobs, i
 cudaError_t launch_stack(const StackParams& p, int elem_bytes, bool x_bf16, int grid, size_t smem,
                          cudaStream_t stream, bool pdl);
 
+// Batch > 1 forward of one linear (rsp_batch.cu): bf16 W and x, B <= kBatchMax.
+constexpr int kBatchMax = 16;
+struct BatchParams {
+  const void* Wt;   // bf16 [n][m_pad]
+  const void* At;   // bf16 [r][m_pad]
+  const void* Bt;   // bf16 [n][r_pad]
+  const void* x;    // bf16 [B][n]
+  float* y;         // fp32 [B][m]  (zero on entry when ks > 1)
+  int2* cuts;       // [B] per-token cuts (workspace)
+  float* t_acc;     // [B][r_pad] (workspace; zero on entry, left zero)
+  unsigned* ctr;    // [0] t arrivals, [1] CTAs done (workspace; zero on entry, left zero)
+  int n, m, m_pad, r, r_pad, k, B;
+  int cw, ks, grid;  // 64 x cw output columns per CTA, ks channel splits, grid = tiles x ks
+  int range_max, slice_max, na_max;  // shared-memory carve-up
+};
+constexpr size_t kBatchWsBytes(int r_pad) { return 512 + static_cast<size_t>(kBatchMax) * r_pad * 4; }
+size_t batch_smem_bytes(const BatchParams& p);
+cudaError_t launch_batch(const BatchParams& p, bool x_bf16, cudaStream_t stream);
+
 // Stand-alone selector: one CTA.  Any of kept/rest/sparse may be null.
 size_t select_smem_bytes(int n, bool x_bf16);
 cudaError_t launch_select(const void* x, bool x_bf16, int n, int k, int32_t* kept, int32_t* rest,

@@ -216,7 +216,7 @@ __device__ __forceinline__ void warp_find_desc(SelArea s, uint32_t hist, int nb,
 // index runs) and a block scan finds the need-th lowest index.
 // Serial work is done by one warp (all 16 warps issuing it would cost 4x:
 // four warps share each scheduler).
-__device__ __noinline__ Cut sel_cut_bf16_tail(int n, SelArea s, uint32_t bin, uint32_t need) {
+static __device__ __noinline__ Cut sel_cut_bf16_tail(int n, SelArea s, uint32_t bin, uint32_t need) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nv = n >> 3;
   const int v0 = static_cast<int>(static_cast<uint32_t>(nv) * tid / kThreads);
@@ -293,7 +293,7 @@ __device__ __noinline__ Cut sel_cut_bf16_tail(int n, SelArea s, uint32_t bin, ui
 // Contains __syncthreads; latency-bound, so loads are batched ahead of their
 // uses and every phase is block-parallel.
 template <bool XBF>
-__device__ __noinline__ Cut sel_cut(int n, int k, SelArea s) {
+static __device__ __noinline__ Cut sel_cut(int n, int k, SelArea s) {
   if (k <= 0) return Cut{0xffffffffu, 0};
   if (k >= n) return Cut{0u, INT_MAX};
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -617,7 +617,7 @@ __device__ __forceinline__ void search_desc16(SelArea s, uint32_t local, uint32_
 // 32 keys, 4 LDS.128), the whole histogram only if the cut lies outside it
 // (thread t owns 128 keys).  Ties at the cut key resolved in ascending index
 // order.  Contains __syncthreads.
-__device__ __noinline__ Cut sel_cut16(int n, int k, SelArea s) {
+static __device__ __noinline__ Cut sel_cut16(int n, int k, SelArea s) {
   if (k <= 0) return Cut{0xffffffffu, 0};
   if (k >= n) return Cut{0u, INT_MAX};
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;

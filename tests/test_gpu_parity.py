@@ -366,3 +366,51 @@ def test_stack_deterministic_bit_reproducible(cuda):
         assert all(torch.equal(a, b) for a, b in zip(outs[0], o))
     for l, x, y in zip(layers, xs, ys):
         assert torch.equal(y, l.forward(x))
+
+
+# ----------------------------------------------------------------------------- batch > 1 (config 3)
+TOL_BATCH = 1e-4  # mma accumulation order + t split into bf16 hi/lo (~2^-16 relative)
+
+
+@pytest.mark.parametrize("shape", [(4096, 4096, 0.5, 256), (11008, 4096, 0.27, 687), (4096, 11008, 0.19, 933),
+                                   (1000, 700, 0.3, 40), (64, 8192, 0.5, 16), (300, 128, 0.0, 64),
+                                   (256, 256, 1.0, 0), (136, 520, 0.77, 8)])
+@pytest.mark.parametrize("batch", [2, 5, 16])
+def test_batched_forward_matches_per_token_oracle(coracle, cuda, shape, batch):
+    """bf16 W and x, 2 <= B <= 16: the union-of-masks tensor-core path
+    (rsp_batch.cu).  Each token must equal its own batch-1 forward (the
+    reference semantics: B independent `forward` calls)."""
+    m, n, s, r = shape
+    rng = np.random.default_rng(m * 7 + n + batch)
+    w = torch.from_numpy(rng.standard_normal((m, n)).astype(np.float32) * 0.02)
+    a = torch.from_numpy(rng.standard_normal((m, r)).astype(np.float32) * 0.05)
+    b = torch.from_numpy(rng.standard_normal((r, n)).astype(np.float32) * 0.05)
+    layer = rsp.DecomposedLayer(w.to(cuda), a.to(cuda), b.to(cuda), rsp.SparsityPlan(s, r), weight_dtype="bf16")
+    xs = []
+    for t in range(batch):
+        x = wl.heavy_tailed_x(n, rng)
+        if t % 3 == 2:  # repeated values: ties at the cut
+            x = rng.choice(x[: max(1, n // 6)], size=n).astype(np.float32)
+        xs.append(x)
+    X = torch.from_numpy(np.stack(xs)).to(cuda).to(torch.bfloat16)
+    Y = layer.forward(X).cpu().numpy()
+    W, A, Bm = layer.export()
+    for t in range(batch):
+        want = coracle.forward(np.ascontiguousarray(W.T), A, Bm, layer.plan.keep_fraction, as_seen(X[t]))
+        assert maxrel(Y[t], want) <= TOL_BATCH, (t, maxrel(Y[t], want))
+        one = layer.forward(X[t]).cpu().numpy()
+        assert maxrel(Y[t], one) <= TOL_BATCH, (t, maxrel(Y[t], one))
+
+
+def test_batched_forward_repeatable_and_host(cuda):
+    """Back-to-back batched launches reuse the workspace (counters and the t
+    accumulator are left zero); the host-buffer entry point takes the same path."""
+    c = wl.config1_layer("gate_proj", 11008, 4096, device="cuda")
+    layer = rsp.DecomposedLayer(c["w"], c["a_r"], c["b_r"], rsp.SparsityPlan(0.5, c["rank"]), weight_dtype="bf16")
+    rng = np.random.default_rng(11)
+    X = torch.stack([torch.from_numpy(wl.heavy_tailed_x(4096, rng)) for _ in range(8)]).to(cuda).to(torch.bfloat16)
+    y1 = layer.forward(X).cpu().numpy()
+    y2 = layer.forward(X).cpu().numpy()
+    assert maxrel(y2, y1) <= 1e-6
+    for t in range(8):
+        assert maxrel(y1[t], layer.forward(X[t]).cpu().numpy()) <= TOL_BATCH
