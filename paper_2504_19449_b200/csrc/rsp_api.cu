@@ -617,8 +617,8 @@ bool batch_plan(const rsp_linear* h, int B, const DevProps& dp, BatchParams* out
     p.cw = cw;
     p.ks = ks;
     p.grid = tiles * ks;
-    p.range_max = (n + ks - 1) / ks + 1;
-    p.slice_max = (n + p.grid - 1) / p.grid + 1;
+    p.range_max = ((n + ks - 1) / ks + 16 + 7) / 8 * 8;  // 8-aligned rows around [wc0, wc1)
+    p.slice_max = ((n + p.grid - 1) / p.grid + 16 + 7) / 8 * 8;
     p.na_max = (p.r + ks - 1) / ks + 1;
     if (2 * B * p.range_max > 96 * 1024) continue;
     if (rsp::batch_smem_bytes(p) > static_cast<size_t>(dp.smem_optin)) continue;

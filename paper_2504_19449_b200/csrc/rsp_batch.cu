@@ -185,36 +185,113 @@ __global__ void __launch_bounds__(kThreads, 1) batch_forward_kernel(const BatchP
     const int2 c = P.cuts[tid];
     sts2(sb + L.cuts + 8u * tid, static_cast<uint32_t>(c.x), static_cast<uint32_t>(c.y));
   }
+  // Activations of the CTA's channel ranges, all tokens, in shared memory:
+  // rows start at the 8-aligned channels wb0 / ub0 (16-byte vectors).
+  const int wb0 = wc0 & ~7, ub0 = uc0 & ~7;
   const uint16_t* x16 = static_cast<const uint16_t*>(P.x);
-  for (int b = 0; b < B; ++b) {
-    for (int jj = tid; jj < rw; jj += kThreads)
-      asm volatile("st.shared.u16 [%0], %1;" ::"r"(sb + L.xs + 2u * (b * P.range_max + jj)),
-                   "h"(x16[static_cast<size_t>(b) * P.n + wc0 + jj]) : "memory");
-    for (int jj = tid; jj < ru; jj += kThreads)
-      asm volatile("st.shared.u16 [%0], %1;" ::"r"(sb + L.xu + 2u * (b * P.slice_max + jj)),
-                   "h"(x16[static_cast<size_t>(b) * P.n + uc0 + jj]) : "memory");
-  }
+  auto stage_x = [&](uint32_t dst, int stride, int c0, int c1) {  // channels [c0 & ~7, c1)
+    const int b0 = c0 & ~7;
+    if ((P.n & 7) == 0) {
+      const int nvec = (c1 - b0 + 7) >> 3;
+      for (int v = tid; v < nvec; v += kThreads) {
+        uint4 u[kBatchMax];
+#pragma unroll
+        for (int b = 0; b < kBatchMax; ++b)
+          if (b < B) u[b] = __ldg(reinterpret_cast<const uint4*>(x16 + static_cast<size_t>(b) * P.n + b0) + v);
+#pragma unroll
+        for (int b = 0; b < kBatchMax; ++b)
+          if (b < B) sts4(dst + 2u * (b * stride) + 16u * v, u[b]);
+      }
+    } else {
+      for (int b = 0; b < B; ++b)
+        for (int jj = tid; jj < c1 - b0; jj += kThreads)
+          asm volatile("st.shared.u16 [%0], %1;" ::"r"(dst + 2u * (b * stride + jj)),
+                       "h"(x16[static_cast<size_t>(b) * P.n + b0 + jj]) : "memory");
+    }
+  };
+  stage_x(sb + L.xs, P.range_max, wc0, wc1);
+  if (has_lr) stage_x(sb + L.xu, P.slice_max, uc0, uc1);
   __syncthreads();
-  // token mask of channel j (x row base `xr`, offset jj): bit b = j in S_b
-  auto in_mask = [&](uint32_t xr, int stride, int jj, int j) {
-    uint32_t m = 0;
+  const uint32_t all = (1u << B) - 1u;
+  // Membership of the 8 channels [j8, j8 + 8): tm[e] = tokens with channel
+  // j8 + e in their S_b (packed-pair key tests against each token's cut).
+  auto token_masks = [&](uint32_t xr, int stride, int base, int j8, uint32_t (&tm)[8]) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) tm[e] = 0u;
     for (int b = 0; b < B; ++b) {
       const uint2 c = lds2(sb + L.cuts + 8u * b);
-      const uint32_t key = (lds_u16(xr + 2u * (b * stride + jj)) << 16) & 0x7fffffffu;
-      m |= static_cast<uint32_t>(in_cut(key, j, Cut{c.x, static_cast<int>(c.y)})) << b;
+      const uint4 u = lds4(xr + 2u * (b * stride + (j8 - base)));
+      uint32_t m8 = 0;
+      if (c.x <= 0x7fff0000u) {
+        const uint32_t t15 = c.x >> 16;
+        const uint32_t gt =
+            t15 < 0x7fffu ? pack8(pair_gt(u.x, t15), pair_gt(u.y, t15), pair_gt(u.z, t15), pair_gt(u.w, t15)) : 0u;
+        const uint32_t eq = pack8(pair_eq(u.x, t15), pair_eq(u.y, t15), pair_eq(u.z, t15), pair_eq(u.w, t15));
+        const int jl = min(max(static_cast<int>(c.y) - j8, 0), 8);
+        m8 = gt | (eq & (0xffu >> (8 - jl)));
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) tm[e] |= ((m8 >> e) & 1u) << b;
     }
-    return m;
   };
-  const uint32_t all = (B >= 32) ? 0xffffffffu : ((1u << B) - 1u);
-  int nW = 0, nU = 0;
-  compact2(
-      S, wc0, wc1, uc0, uc1, [&](int j) { return in_mask(sb + L.xs, P.range_max, j - wc0, j) != 0u; },
-      [&](int j) { return has_lr && in_mask(sb + L.xu, P.slice_max, j - uc0, j) != all; },
-      [&](int i, int j) { sts2(sb + L.lw + 8u * i, static_cast<uint32_t>(j), in_mask(sb + L.xs, P.range_max, j - wc0, j)); },
-      [&](int i, int j) {
-        sts2(sb + L.lu + 8u * i, static_cast<uint32_t>(j), all & ~in_mask(sb + L.xu, P.slice_max, j - uc0, j));
-      },
-      &nW, &nU);
+  // Ascending list of {channel, token mask} over [lo, hi): the channels some
+  // token selects (want_s) or some token leaves to the low-rank term (!want_s).
+  // Warp-contiguous 256-channel chunks, ballot prefix sums.  Two __syncthreads.
+  auto build_list = [&](uint32_t xr, int stride, int lo, int hi, bool want_s, uint32_t list, int slot) {
+    const int base = lo & ~7;
+    const int nch = hi > lo ? (hi - base + 255) >> 8 : 0;
+    const int per = (nch + kWarps - 1) / kWarps, ch0 = min(nch, warp * per), ch1 = min(nch, (warp + 1) * per);
+    auto member_bits = [&](int j8, uint32_t (&tm)[8]) {
+      token_masks(xr, stride, base, j8, tm);
+      const int lo_off = min(max(lo - j8, 0), 8), hi_off = min(max(hi - j8, 0), 8);
+      const uint32_t range = (0xffu >> (8 - hi_off)) & (0xffu << lo_off);
+      uint32_t m = 0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        if (!want_s) tm[e] = all & ~tm[e];
+        m |= static_cast<uint32_t>(tm[e] != 0u) << e;
+      }
+      return m & range;
+    };
+    uint32_t cnt = 0;
+    for (int c = ch0; c < ch1; ++c) {
+      const int j8 = base + 256 * c + 8 * lane;
+      uint32_t tm[8];
+      cnt += j8 < hi ? __popc(member_bits(j8, tm)) : 0u;
+    }
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    if (lane == 0) S.set_m(slot + warp, cnt);
+    __syncthreads();
+    uint32_t off = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      const uint32_t v = S.m(slot + w);
+      off += w < warp ? v : 0u;
+      tot += v;
+    }
+    const uint32_t lt = lanemask_lt();
+    for (int c = ch0; c < ch1; ++c) {
+      const int j8 = base + 256 * c + 8 * lane;
+      uint32_t tm[8];
+      const uint32_t m = j8 < hi ? member_bits(j8, tm) : 0u;
+      uint32_t pre = 0, sum = 0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const uint32_t bal = __ballot_sync(0xffffffffu, (m >> e) & 1u);
+        pre += __popc(bal & lt);
+        sum += __popc(bal);
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        sts2_pred((m >> e) & 1u, list + 8u * (off + pre + __popc(m & ((1u << e) - 1u))),
+                  static_cast<uint32_t>(j8 + e), tm[e]);
+      off += sum;
+    }
+    __syncthreads();
+    return static_cast<int>(tot);
+  };
+  const int nW = build_list(sb + L.xs, P.range_max, wc0, wc1, true, sb + L.lw, M_LISTA);
+  const int nU = has_lr ? build_list(sb + L.xu, P.slice_max, uc0, uc1, false, sb + L.lu, M_LISTB) : 0;
 
   // A fragment of gathered rows: coef(m, kk) = mask_m ? x_m[row kk] : 0,
   // rows from list entries e0 + stride * kk (kk < 16, beyond cnt: 0).
@@ -302,7 +379,7 @@ __global__ void __launch_bounds__(kThreads, 1) batch_forward_kernel(const BatchP
             const uint32_t j = lds(sb + L.lu + 8u * static_cast<uint32_t>(e));
             return static_cast<const void*>(Bt + static_cast<size_t>(j) * P.r_pad + c0);
           },
-          [&](int st, uint32_t(&a)[4]) { frag_list(sb + L.lu, st * kStage, 1, nU, sb + L.xu, P.slice_max, uc0, a); },
+          [&](int st, uint32_t(&a)[4]) { frag_list(sb + L.lu, st * kStage, 1, nU, sb + L.xu, P.slice_max, ub0, a); },
           vch);
 #pragma unroll
       for (int nb = 0; nb < 8; ++nb) {
@@ -339,7 +416,7 @@ __global__ void __launch_bounds__(kThreads, 1) batch_forward_kernel(const BatchP
             return static_cast<const void*>(Wt + static_cast<size_t>(j) * P.m_pad + colw);
           },
           [&](int st, uint32_t(&a)[4]) {
-            frag_list(sb + L.lw, rg + RG * st * kStage, RG, nW, sb + L.xs, P.range_max, wc0, a);
+            frag_list(sb + L.lw, rg + RG * st * kStage, RG, nW, sb + L.xs, P.range_max, wb0, a);
           },
           vch);
   }
