@@ -133,10 +133,13 @@ rsp_status rsp_workspace_init(void* workspace, size_t bytes, void* stream);
 
 /* Replaces rsparse::forward(const DecomposedLayer&, span<const double> x)
  * (layer.hpp:75, layer.cpp:95-123).  x_dev: batch x m_in (x_dtype F32/BF16);
- * y_dev: batch x (row_end-row_begin) fp32.  One fused kernel: selection,
- * gathered-row GEMV and the two-stage low-rank term.  batch must be 1 in
- * ABI v1 (batch > 1 tokens are run as independent per-token forwards, which
- * is the reference semantics). */
+ * y_dev: batch x (row_end-row_begin) fp32.  batch 1: one fused kernel
+ * (selection, gathered-row GEMV, two-stage low-rank term).  2 <= batch <= 16
+ * with bf16 weights and bf16 x: each token keeps its own top-k set (the
+ * reference semantics: B independent forwards) and one launch
+ * reads the union of the tokens' selected W rows once, on the tensor cores;
+ * other combinations run as per-token forwards.  The workspace must be
+ * rsp_linear_workspace_size bytes (any batch). */
 rsp_status rsp_linear_forward(const rsp_linear* h, const void* x_dev, rsp_dtype x_dtype,
                               float* y_dev, uint32_t batch, void* workspace,
                               size_t workspace_bytes, void* stream);
