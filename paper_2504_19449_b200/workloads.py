@@ -149,6 +149,27 @@ def config2_plans(seed: int = 2, budget: float = 0.5, shapes=LLAMA2_7B,
     return out
 
 
+def config4_plans(sparsity: float, rank: int, n_layers: int = N_LAYERS):
+    """Config 4 (BASELINE.json configs[4]): the Llama-3-8B stack at model-level
+    sparsity `sparsity` with every linear at rank `rank`: keep fraction
+    s = (1 - sparsity) - r (m + n) / (m n) so each linear's reference io_cost
+    is 1 - sparsity.  Where that s is negative (GQA k/v at
+    high sparsity / rank) the rank is clamped to floor((1 - sparsity) m n /
+    (m + n)) with s = 0, and the clamp is reported: returns (plans, clamped)."""
+    out, clamped = [], []
+    for layer in range(n_layers):
+        for (name, m, n) in LLAMA3_8B:
+            r = rank
+            s = (1.0 - sparsity) - r * (m + n) / (m * n)
+            if s < 0.0:
+                r = int(np.floor((1.0 - sparsity) * m * n / (m + n)))
+                s = 0.0
+                if layer == 0:
+                    clamped.append((name, rank, r))
+            out.append((f"layers.{layer}.{name}", m, n, float(s), int(r)))
+    return out, clamped
+
+
 def stack_bytes(plans, elem: int = 2) -> Tuple[int, int]:
     """(R-Sparse kernel weight bytes, dense bytes) for a list of plans, using
     the SURVEY §8(d) byte model elem*(k*m + (n-k)*r + r*m) vs elem*m*n."""
