@@ -782,48 +782,46 @@ __device__ __forceinline__ void compact2(SelArea s, int a0, int a1, int b0, int 
 }
 
 
-// bf16 activations: membership bits of the 8 channels [j8, j8 + 8) (j8 a
-// multiple of 8) -- in S when `in_s`, in S^c otherwise -- restricted to
-// [lo, hi); `u` returns their raw bits.  Packed-pair tests, no branches.
-__device__ __forceinline__ uint32_t chunk_members16(SelArea s, int j8, int lo, int hi, const Cut& cut, bool in_s,
-                                                    uint4& u) {
-  // (chunks past hi load the last in-range vector: every bit is masked off)
-  u = lds4(s.xs + 2u * static_cast<uint32_t>(min(j8, (hi - 1) & ~7)));
+// Membership bits of channels j2, j2 + 1 (j2 even) -- in S when `in_s`, in
+// S^c otherwise -- restricted to [lo, hi); `w` returns their raw bf16 pair.
+__device__ __forceinline__ uint32_t pair_members16(SelArea s, int j2, int lo, int hi, const Cut& cut, bool in_s,
+                                                   uint32_t& w) {
+  w = lds(s.xs + 2u * static_cast<uint32_t>(min(j2, (hi - 1) & ~1)));
   uint32_t m_in = 0;
   if (cut.T <= 0x7fff0000u) {  // else S is empty
     const uint32_t t15 = cut.T >> 16;
-    const uint32_t gt = t15 < 0x7fffu ? pack8(pair_gt(u.x, t15), pair_gt(u.y, t15), pair_gt(u.z, t15), pair_gt(u.w, t15))
-                                      : 0u;
-    const uint32_t eq = pack8(pair_eq(u.x, t15), pair_eq(u.y, t15), pair_eq(u.z, t15), pair_eq(u.w, t15));
-    const int jl = min(max(cut.jlim - j8, 0), 8);  // channels of the vector below jlim
-    m_in = gt | (eq & (0xffu >> (8 - jl)));
+    const uint32_t gt = t15 < 0x7fffu ? pair_gt(w, t15) : 0u;
+    const uint32_t eq = pair_eq(w, t15);
+    const int jl = min(max(cut.jlim - j2, 0), 2);
+    m_in = ((gt >> 15) & 1u) | ((gt >> 30) & 2u) | ((((eq >> 15) & 1u) | ((eq >> 30) & 2u)) & ((1u << jl) - 1u));
   }
-  const int lo_off = min(max(lo - j8, 0), 8), hi_off = min(max(hi - j8, 0), 8);
-  const uint32_t range = (0xffu >> (8 - hi_off)) & (0xffu << lo_off);
+  const int lo_off = min(max(lo - j2, 0), 2), hi_off = min(max(hi - j2, 0), 2);
+  const uint32_t range = ((1u << hi_off) - 1u) & ~((1u << lo_off) - 1u);
   return (in_s ? m_in : ~m_in) & range;
 }
 
-// compact2 for bf16 activations, 8 channels per lane per 16-byte load:
-// S-members of [a0, a1) -> fa(p, i, j, bits), S^c-members of [b0, b1) -> fb(p, i, j, bits),
-// each ascending (i = position in its list, bits = the fp32 bits of x_j); f is
-// called for all 8 channels of a lane with p = membership (write only if p).
-// A warp sweeps whole 256-channel chunks; positions inside a chunk come from
-// eight ballots (no shuffle chains).  Two __syncthreads.
+// compact2 for bf16 activations: S-members of [a0, a1) -> fa(p, i, j, bits),
+// S^c-members of [b0, b1) -> fb(p, i, j, bits), each ascending (i = position
+// in its list, bits = the fp32 bits of x_j); f is called for both channels of
+// a lane with p = membership (write only if p).  2 channels per lane: the
+// 64-channel chunks of both ranges are spread over all warps (the lists of
+// one CTA are short, so the critical path is one or two chunks per warp);
+// positions from two ballots per chunk.  Two __syncthreads.
 template <class FA, class FB>
 __device__ __forceinline__ void compact2_16(SelArea s, const Cut& cut, int a0, int a1, int b0, int b1, FA&& fa,
                                             FB&& fb, int* na, int* nb) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int A0 = a0 & ~7, B0 = b0 & ~7;
-  const int ca = a1 > a0 ? (a1 - A0 + 255) >> 8 : 0, cb = b1 > b0 ? (b1 - B0 + 255) >> 8 : 0;
-  const int pera = (ca + kWarps - 1) / kWarps, perb = (cb + kWarps - 1) / kWarps;
-  const int ca0 = min(ca, warp * pera), ca1 = min(ca, (warp + 1) * pera);
-  const int cb0 = min(cb, warp * perb), cb1 = min(cb, (warp + 1) * perb);
-  uint4 u;
+  const int A0 = a0 & ~1, B0 = b0 & ~1;
+  const int ca = a1 > a0 ? (a1 - A0 + 63) >> 6 : 0, cb = b1 > b0 ? (b1 - B0 + 63) >> 6 : 0;
+  const int ctot = ca + cb, per = (ctot + kWarps - 1) / kWarps;
+  const int c0 = min(ctot, warp * per), c1 = min(ctot, (warp + 1) * per);
+  uint32_t w;
   uint32_t cnta = 0, cntb = 0;
 #pragma unroll 1
-  for (int c = ca0; c < ca1; ++c) cnta += __popc(chunk_members16(s, A0 + 256 * c + 8 * lane, a0, a1, cut, true, u));
-#pragma unroll 1
-  for (int c = cb0; c < cb1; ++c) cntb += __popc(chunk_members16(s, B0 + 256 * c + 8 * lane, b0, b1, cut, false, u));
+  for (int c = c0; c < c1; ++c) {
+    if (c < ca) cnta += __popc(pair_members16(s, A0 + 64 * c + 2 * lane, a0, a1, cut, true, w));
+    else cntb += __popc(pair_members16(s, B0 + 64 * (c - ca) + 2 * lane, b0, b1, cut, false, w));
+  }
   cnta = __reduce_add_sync(0xffffffffu, cnta);
   cntb = __reduce_add_sync(0xffffffffu, cntb);
   if (lane == 0) {
@@ -837,42 +835,33 @@ __device__ __forceinline__ void compact2_16(SelArea s, const Cut& cut, int a0, i
   const uint32_t wb[8] = {lb0.x, lb0.y, lb0.z, lb0.w, lb1.x, lb1.y, lb1.z, lb1.w};
   uint32_t offa = 0, offb = 0, tota = 0, totb = 0;
 #pragma unroll
-  for (int w = 0; w < kWarps; ++w) {
-    offa += w < warp ? wa[w] : 0u;
-    offb += w < warp ? wb[w] : 0u;
-    tota += wa[w];
-    totb += wb[w];
+  for (int q = 0; q < kWarps; ++q) {
+    offa += q < warp ? wa[q] : 0u;
+    offb += q < warp ? wb[q] : 0u;
+    tota += wa[q];
+    totb += wb[q];
   }
   *na = static_cast<int>(tota);
   *nb = static_cast<int>(totb);
   const uint32_t lt = lanemask_lt();
-  auto emit = [&](int j8, uint32_t m, const uint4& uu, uint32_t& off, auto&& f) {
-    uint32_t pre = 0, tot = 0;
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const uint32_t bal = __ballot_sync(0xffffffffu, (m >> e) & 1u);
-      pre += __popc(bal & lt);
-      tot += __popc(bal);
-    }
-    const uint32_t w[4] = {uu.x, uu.y, uu.z, uu.w};
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const uint32_t bits = (e & 1) ? (w[e >> 1] & 0xffff0000u) : (w[e >> 1] << 16);
-      f(((m >> e) & 1u) != 0, static_cast<int>(off + pre + __popc(m & ((1u << e) - 1u))), j8 + e, bits);
-    }
-    off += tot;
+  auto emit = [&](int j2, uint32_t m, uint32_t ww, uint32_t& off, auto&& f) {
+    const uint32_t bal0 = __ballot_sync(0xffffffffu, m & 1u), bal1 = __ballot_sync(0xffffffffu, (m >> 1) & 1u);
+    const uint32_t pre = __popc(bal0 & lt) + __popc(bal1 & lt);
+    f((m & 1u) != 0, static_cast<int>(off + pre), j2, ww << 16);
+    f((m & 2u) != 0, static_cast<int>(off + pre + (m & 1u)), j2 + 1, ww & 0xffff0000u);
+    off += __popc(bal0) + __popc(bal1);
   };
 #pragma unroll 1
-  for (int c = ca0; c < ca1; ++c) {
-    const int j8 = A0 + 256 * c + 8 * lane;
-    const uint32_t m = chunk_members16(s, j8, a0, a1, cut, true, u);
-    emit(j8, m, u, offa, fa);
-  }
-#pragma unroll 1
-  for (int c = cb0; c < cb1; ++c) {
-    const int j8 = B0 + 256 * c + 8 * lane;
-    const uint32_t m = chunk_members16(s, j8, b0, b1, cut, false, u);
-    emit(j8, m, u, offb, fb);
+  for (int c = c0; c < c1; ++c) {
+    if (c < ca) {
+      const int j2 = A0 + 64 * c + 2 * lane;
+      const uint32_t m = pair_members16(s, j2, a0, a1, cut, true, w);
+      emit(j2, m, w, offa, fa);
+    } else {
+      const int j2 = B0 + 64 * (c - ca) + 2 * lane;
+      const uint32_t m = pair_members16(s, j2, b0, b1, cut, false, w);
+      emit(j2, m, w, offb, fb);
+    }
   }
   __syncthreads();
 }
