@@ -560,28 +560,24 @@ template <int PER>
 __device__ __forceinline__ void search_desc16(SelArea s, uint32_t local, uint32_t top, uint32_t above0, uint32_t kk) {
   static_assert(PER == 32 || PER == 128, "keys per thread");
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t wsum = __reduce_add_sync(0xffffffffu, local);
-  if (lane == 0) s.set_m(M_WSUM + warp, wsum);
-  __syncthreads();
-  const uint32_t tw = lane < kWarps ? s.m(M_WSUM + lane) : 0u;
-  uint32_t inc = tw;
+  // every warp scans its lanes at once; one barrier publishes the warp totals
+  uint32_t li = local;
 #pragma unroll
-  for (int o = 1; o < kWarps; o <<= 1) {
-    const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= o) inc += t;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, li, o);
+    if (lane >= o) li += t;
   }
-  const int wb =
-      __ffs(__ballot_sync(0xffffffffu, (lane < kWarps) & (above0 + inc - tw < kk) & (kk <= above0 + inc))) - 1;
-  if (warp == wb) {
-    const uint32_t wabove = above0 + __shfl_sync(0xffffffffu, inc - tw, wb);
-    uint32_t li = local;
+  if (lane == 31) s.set_m(M_WSUM + warp, li);
+  __syncthreads();
+  const uint4 w0 = lds4(s.misc + 4u * M_WSUM), w1 = lds4(s.misc + 4u * (M_WSUM + 4));
+  const uint32_t wt[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+  uint32_t wabove = above0;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t t = __shfl_up_sync(0xffffffffu, li, o);
-      if (lane >= o) li += t;
-    }
-    const uint32_t mine_ex = wabove + li - local;
-    const int ol = __ffs(__ballot_sync(0xffffffffu, (mine_ex < kk) & (kk <= mine_ex + local))) - 1;
+  for (int q = 0; q < kWarps; ++q) wabove += q < warp ? wt[q] : 0u;
+  const uint32_t mine_ex = wabove + li - local;
+  const uint32_t own = __ballot_sync(0xffffffffu, (mine_ex < kk) & (kk <= mine_ex + local));
+  if (own) {  // this warp holds the owner thread of the k-th key
+    const int ol = __ffs(own) - 1;
     const int tb = warp * 32 + ol;
     const uint32_t above = __shfl_sync(0xffffffffu, mine_ex, ol);
     const uint32_t ktop = top - static_cast<uint32_t>(PER) * static_cast<uint32_t>(tb);  // owner's keys: [ktop - PER, ktop)
