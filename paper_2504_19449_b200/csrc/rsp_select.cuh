@@ -685,9 +685,10 @@ static __device__ __noinline__ Cut sel_cut16(int n, int k, SelArea s) {
     RSP_SEL_STAMP(7);
     if (warp == 0) {
       const uint32_t j = lane < static_cast<int>(cnt) ? lds(s.cand + 4u * lane) : 0xffffffffu;
-      uint32_t rank = 0;
+      uint32_t r4[4] = {0u, 0u, 0u, 0u};  // four independent chains
 #pragma unroll
-      for (int i = 0; i < 32; ++i) rank += __shfl_sync(0xffffffffu, j, i) < j;
+      for (int i = 0; i < 32; ++i) r4[i & 3] += __shfl_sync(0xffffffffu, j, i) < j;
+      const uint32_t rank = (r4[0] + r4[1]) + (r4[2] + r4[3]);
       sts_pred((lane < static_cast<int>(cnt)) & (rank == need - 1), s.misc + 4u * M_JLIM, j + 1);
     }
   } else {
