@@ -258,6 +258,11 @@ rsp_status rsp_debug_forward_trace(const rsp_linear* h, const void* x_dev, rsp_d
  * [13] after its dependency wait, [14] at its end, [1..12] %clock64 phase
  * stamps relative to the CTA's start of the linear.  *grid_out = grid. */
 rsp_status rsp_debug_stack_trace(rsp_stack* s, int64_t* trace_dev, uint32_t* grid_out, void* stream);
+/* Debug: per-CTA phase clocks of the last batched forward run with the
+ * environment variable RSP_BATCH_TRACE=1: host[cta * 16 + phase] (clock64
+ * since the CTA started; phases 1 staging, 2 lists, 3 stage 1, 4 arrive,
+ * 5 W rows, 6 t barrier, 7 stage 2, 8 combine). */
+rsp_status rsp_debug_batch_trace(int64_t* host, uint32_t ctas);
 
 /* -- device helpers ------------------------------------------------------------- */
 int rsp_device_sm_count(int device);

@@ -24,7 +24,7 @@ EXPORTS = [
     "rsp_linear_selected", "rsp_linear_io_cost", "rsp_linear_export",
     "rsp_top_k_by_magnitude", "rsp_threshold_sparsify", "rsp_stack_create", "rsp_stack_create_ex",
     "rsp_stack_launch", "rsp_stack_destroy", "rsp_device_sm_count", "rsp_debug_forward_trace",
-    "rsp_debug_stack_trace", "rsp_rspl_read", "rsp_linear_load_rspl", "rsp_linear_save_rspl", "rsp_linear_components",
+    "rsp_debug_stack_trace", "rsp_debug_batch_trace", "rsp_rspl_read", "rsp_linear_load_rspl", "rsp_linear_save_rspl", "rsp_linear_components",
 ]
 
 
@@ -134,6 +134,7 @@ def lib() -> ct.CDLL:
         "rsp_device_sm_count": (ct.c_int, [ct.c_int]),
         "rsp_debug_forward_trace": (ct.c_int, [vp, vp, ct.c_int, vp, vp, ct.c_size_t, vp, ct.c_int, vp]),
         "rsp_debug_stack_trace": (ct.c_int, [vp, vp, ct.POINTER(u32), vp]),
+        "rsp_debug_batch_trace": (ct.c_int, [vp, u32]),
         "rsp_rspl_read": (ct.c_int, [ct.c_char_p, ct.POINTER(RsplHeader), vp, vp, vp, vp]),
         "rsp_linear_load_rspl": (ct.c_int, [ct.c_char_p, ct.POINTER(LinearDesc), ct.POINTER(vp)]),
         "rsp_linear_save_rspl": (ct.c_int, [vp, ct.c_char_p]),

@@ -657,6 +657,7 @@ rsp_status rsp_linear_forward(const rsp_linear* h, const void* x, rsp_dtype xdt,
     bp.ctr = reinterpret_cast<unsigned*>(area);
     bp.cuts = reinterpret_cast<int2*>(area + 256);
     bp.t_acc = reinterpret_cast<float*>(area + 512);
+    bp.trace = env_int("RSP_BATCH_TRACE", 0);
     const cudaStream_t cs = static_cast<cudaStream_t>(stream);
     if (bp.ks > 1) RSP_CUDA(cudaMemsetAsync(y, 0, sizeof(float) * h->m * batch, cs));
     cudaError_t e = rsp::launch_batch(bp, true, cs);
@@ -669,6 +670,12 @@ rsp_status rsp_linear_forward(const rsp_linear* h, const void* x, rsp_dtype xdt,
                                    ws, ws_bytes, static_cast<cudaStream_t>(stream), false);
     if (st) return st;
   }
+  return RSP_OK;
+}
+
+extern "C" rsp_status rsp_debug_batch_trace(int64_t* host, uint32_t ctas) {
+  if (!host || ctas > 160) return fail(RSP_E_USAGE, "bad trace buffer");
+  RSP_CUDA(rsp::batch_trace_copy(reinterpret_cast<long long*>(host), static_cast<int>(ctas)));
   return RSP_OK;
 }
 

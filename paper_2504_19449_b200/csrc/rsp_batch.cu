@@ -28,6 +28,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "rsp_device.cuh"
 #include "rsp_internal.h"
 #include "rsp_select.cuh"
@@ -75,8 +77,9 @@ struct StepLoad {
 
 // Stage the step into the warp's swizzled tile (chunk c of row kk at
 // c ^ (kk & 7)) and accumulate coef(16 x 16) x tile into D.
+template <bool kTwo = false>
 __device__ __forceinline__ void mma_step(Frag& D, const StepLoad& s, uint32_t tile, const uint32_t (&a)[4],
-                                         int lane) {
+                                         int lane, const uint32_t* a2 = nullptr) {
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int kk = (lane >> 3) + 4 * i, c = lane & 7;
@@ -90,6 +93,11 @@ __device__ __forceinline__ void mma_step(Frag& D, const StepLoad& s, uint32_t ti
     ldsm_x4_trans(tile + static_cast<uint32_t>(kk * 8 + (cc ^ (kk & 7))) * 16u, r0, r1, r2, r3);
     mma_bf16(D.d[2 * p], a, r0, r1);
     mma_bf16(D.d[2 * p + 1], a, r2, r3);
+    if constexpr (kTwo) {  // a second coefficient set on the same staged rows
+      const uint32_t b4[4] = {a2[0], a2[1], a2[2], a2[3]};
+      mma_bf16(D.d[2 * p], b4, r0, r1);
+      mma_bf16(D.d[2 * p + 1], b4, r2, r3);
+    }
   }
   __syncwarp();  // the tile is rewritten by the next step
 }
@@ -161,8 +169,20 @@ struct BatchSmem {
   }
 };
 
+__device__ long long g_batch_trace[160 * 16];
+
 __global__ void __launch_bounds__(kThreads, 1) batch_forward_kernel(const BatchParams P) {
   extern __shared__ __align__(16) uint8_t smem_bf[];
+  long long t_start;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(t_start));
+#define BT_STAMP(i)                                                        \
+  do {                                                                     \
+    if (P.trace && threadIdx.x == 0) {                                     \
+      long long c_;                                                        \
+      asm volatile("mov.u64 %0, %%clock64;" : "=l"(c_));                  \
+      g_batch_trace[blockIdx.x * 16 + (i)] = c_ - t_start;                 \
+    }                                                                      \
+  } while (0)
   const BatchSmem L = BatchSmem::make(P);
   const uint32_t sb = smem_base_pinned(smem_bf);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
@@ -189,109 +209,105 @@ __global__ void __launch_bounds__(kThreads, 1) batch_forward_kernel(const BatchP
   // rows start at the 8-aligned channels wb0 / ub0 (16-byte vectors).
   const int wb0 = wc0 & ~7, ub0 = uc0 & ~7;
   const uint16_t* x16 = static_cast<const uint16_t*>(P.x);
-  auto stage_x = [&](uint32_t dst, int stride, int c0, int c1) {  // channels [c0 & ~7, c1)
-    const int b0 = c0 & ~7;
-    if ((P.n & 7) == 0) {
-      const int nvec = (c1 - b0 + 7) >> 3;
-      for (int v = tid; v < nvec; v += kThreads) {
-        uint4 u[kBatchMax];
+  // both ranges in one round trip: vectors [0, nvw) of the W range, then [0, nvu) of the slice
+  if ((P.n & 7) == 0) {
+    const int nvw = (wc1 - wb0 + 7) >> 3, nvu = has_lr ? (uc1 - ub0 + 7) >> 3 : 0;
+    for (int v = tid; v < nvw + nvu; v += kThreads) {
+      const bool w_side = v < nvw;
+      const int vv = w_side ? v : v - nvw;
+      const int c0 = w_side ? wb0 : ub0;
+      const uint32_t dst = (w_side ? sb + L.xs : sb + L.xu) + 16u * vv;
+      const int stride = w_side ? P.range_max : P.slice_max;
+      uint4 u[kBatchMax];
 #pragma unroll
-        for (int b = 0; b < kBatchMax; ++b)
-          if (b < B) u[b] = __ldg(reinterpret_cast<const uint4*>(x16 + static_cast<size_t>(b) * P.n + b0) + v);
+      for (int b = 0; b < kBatchMax; ++b)
+        if (b < B) u[b] = __ldg(reinterpret_cast<const uint4*>(x16 + static_cast<size_t>(b) * P.n + c0) + vv);
 #pragma unroll
-        for (int b = 0; b < kBatchMax; ++b)
-          if (b < B) sts4(dst + 2u * (b * stride) + 16u * v, u[b]);
-      }
-    } else {
-      for (int b = 0; b < B; ++b)
-        for (int jj = tid; jj < c1 - b0; jj += kThreads)
-          asm volatile("st.shared.u16 [%0], %1;" ::"r"(dst + 2u * (b * stride + jj)),
-                       "h"(x16[static_cast<size_t>(b) * P.n + b0 + jj]) : "memory");
+      for (int b = 0; b < kBatchMax; ++b)
+        if (b < B) sts4(dst + 2u * (b * stride), u[b]);
     }
-  };
-  stage_x(sb + L.xs, P.range_max, wc0, wc1);
-  if (has_lr) stage_x(sb + L.xu, P.slice_max, uc0, uc1);
+  } else {
+    for (int b = 0; b < B; ++b) {
+      for (int jj = tid; jj < wc1 - wb0; jj += kThreads)
+        asm volatile("st.shared.u16 [%0], %1;" ::"r"(sb + L.xs + 2u * (b * P.range_max + jj)),
+                     "h"(x16[static_cast<size_t>(b) * P.n + wb0 + jj]) : "memory");
+      for (int jj = tid; has_lr && jj < uc1 - ub0; jj += kThreads)
+        asm volatile("st.shared.u16 [%0], %1;" ::"r"(sb + L.xu + 2u * (b * P.slice_max + jj)),
+                     "h"(x16[static_cast<size_t>(b) * P.n + ub0 + jj]) : "memory");
+    }
+  }
   __syncthreads();
+  BT_STAMP(1);
   const uint32_t all = (1u << B) - 1u;
-  // Membership of the 8 channels [j8, j8 + 8): tm[e] = tokens with channel
-  // j8 + e in their S_b (packed-pair key tests against each token's cut).
-  auto token_masks = [&](uint32_t xr, int stride, int base, int j8, uint32_t (&tm)[8]) {
-#pragma unroll
-    for (int e = 0; e < 8; ++e) tm[e] = 0u;
+  // Token masks of channels j2, j2 + 1 (j2 even): bit b = channel in S_b
+  // (packed-pair key tests against each token's cut).
+  auto token_masks2 = [&](uint32_t xr, int stride, int base, int j2, uint32_t& t0, uint32_t& t1) {
+    t0 = t1 = 0u;
     for (int b = 0; b < B; ++b) {
       const uint2 c = lds2(sb + L.cuts + 8u * b);
-      const uint4 u = lds4(xr + 2u * (b * stride + (j8 - base)));
-      uint32_t m8 = 0;
+      const uint32_t w = lds(xr + 2u * (b * stride + (j2 - base)));
       if (c.x <= 0x7fff0000u) {
         const uint32_t t15 = c.x >> 16;
-        const uint32_t gt =
-            t15 < 0x7fffu ? pack8(pair_gt(u.x, t15), pair_gt(u.y, t15), pair_gt(u.z, t15), pair_gt(u.w, t15)) : 0u;
-        const uint32_t eq = pack8(pair_eq(u.x, t15), pair_eq(u.y, t15), pair_eq(u.z, t15), pair_eq(u.w, t15));
-        const int jl = min(max(static_cast<int>(c.y) - j8, 0), 8);
-        m8 = gt | (eq & (0xffu >> (8 - jl)));
+        const uint32_t gt = t15 < 0x7fffu ? pair_gt(w, t15) : 0u;
+        const uint32_t eq = pair_eq(w, t15);
+        const int jl = static_cast<int>(c.y) - j2;  // channels below jlim: j2 if jl > 0, j2 + 1 if jl > 1
+        t0 |= ((((gt >> 15) & 1u) | (((eq >> 15) & 1u) & static_cast<uint32_t>(jl > 0)))) << b;
+        t1 |= ((((gt >> 31) & 1u) | (((eq >> 31) & 1u) & static_cast<uint32_t>(jl > 1)))) << b;
       }
-#pragma unroll
-      for (int e = 0; e < 8; ++e) tm[e] |= ((m8 >> e) & 1u) << b;
     }
   };
   // Ascending list of {channel, token mask} over [lo, hi): the channels some
-  // token selects (want_s) or some token leaves to the low-rank term (!want_s).
-  // Warp-contiguous 256-channel chunks, ballot prefix sums.  Two __syncthreads.
+  // token selects (want_s) or some token leaves to the low-rank term
+  // (!want_s).  64-channel chunks over all warps, ballot prefix sums.
+  // Two __syncthreads.
   auto build_list = [&](uint32_t xr, int stride, int lo, int hi, bool want_s, uint32_t list, int slot) {
     const int base = lo & ~7;
-    const int nch = hi > lo ? (hi - base + 255) >> 8 : 0;
+    const int lo2 = lo & ~1;
+    const int nch = hi > lo ? (hi - lo2 + 63) >> 6 : 0;
     const int per = (nch + kWarps - 1) / kWarps, ch0 = min(nch, warp * per), ch1 = min(nch, (warp + 1) * per);
-    auto member_bits = [&](int j8, uint32_t (&tm)[8]) {
-      token_masks(xr, stride, base, j8, tm);
-      const int lo_off = min(max(lo - j8, 0), 8), hi_off = min(max(hi - j8, 0), 8);
-      const uint32_t range = (0xffu >> (8 - hi_off)) & (0xffu << lo_off);
-      uint32_t m = 0;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        if (!want_s) tm[e] = all & ~tm[e];
-        m |= static_cast<uint32_t>(tm[e] != 0u) << e;
+    auto members = [&](int j2, uint32_t& t0, uint32_t& t1) {
+      const int jr = min(j2, (hi - 1) & ~1);  // in-range load address
+      token_masks2(xr, stride, base, jr, t0, t1);
+      if (!want_s) {
+        t0 = all & ~t0;
+        t1 = all & ~t1;
       }
-      return m & range;
+      const uint32_t m = static_cast<uint32_t>(t0 != 0u) | (static_cast<uint32_t>(t1 != 0u) << 1);
+      const int lo_off = min(max(lo - j2, 0), 2), hi_off = min(max(hi - j2, 0), 2);
+      return m & ((1u << hi_off) - 1u) & ~((1u << lo_off) - 1u);
     };
     uint32_t cnt = 0;
     for (int c = ch0; c < ch1; ++c) {
-      const int j8 = base + 256 * c + 8 * lane;
-      uint32_t tm[8];
-      cnt += j8 < hi ? __popc(member_bits(j8, tm)) : 0u;
+      uint32_t t0, t1;
+      cnt += __popc(members(lo2 + 64 * c + 2 * lane, t0, t1));
     }
     cnt = __reduce_add_sync(0xffffffffu, cnt);
     if (lane == 0) S.set_m(slot + warp, cnt);
     __syncthreads();
     uint32_t off = 0, tot = 0;
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) {
-      const uint32_t v = S.m(slot + w);
-      off += w < warp ? v : 0u;
+    for (int q = 0; q < kWarps; ++q) {
+      const uint32_t v = S.m(slot + q);
+      off += q < warp ? v : 0u;
       tot += v;
     }
     const uint32_t lt = lanemask_lt();
     for (int c = ch0; c < ch1; ++c) {
-      const int j8 = base + 256 * c + 8 * lane;
-      uint32_t tm[8];
-      const uint32_t m = j8 < hi ? member_bits(j8, tm) : 0u;
-      uint32_t pre = 0, sum = 0;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const uint32_t bal = __ballot_sync(0xffffffffu, (m >> e) & 1u);
-        pre += __popc(bal & lt);
-        sum += __popc(bal);
-      }
-#pragma unroll
-      for (int e = 0; e < 8; ++e)
-        sts2_pred((m >> e) & 1u, list + 8u * (off + pre + __popc(m & ((1u << e) - 1u))),
-                  static_cast<uint32_t>(j8 + e), tm[e]);
-      off += sum;
+      const int j2 = lo2 + 64 * c + 2 * lane;
+      uint32_t t0, t1;
+      const uint32_t m = members(j2, t0, t1);
+      const uint32_t bal0 = __ballot_sync(0xffffffffu, m & 1u), bal1 = __ballot_sync(0xffffffffu, (m >> 1) & 1u);
+      const uint32_t pre = off + __popc(bal0 & lt) + __popc(bal1 & lt);
+      sts2_pred(m & 1u, list + 8u * pre, static_cast<uint32_t>(j2), t0);
+      sts2_pred((m >> 1) & 1u, list + 8u * (pre + (m & 1u)), static_cast<uint32_t>(j2 + 1), t1);
+      off += __popc(bal0) + __popc(bal1);
     }
     __syncthreads();
     return static_cast<int>(tot);
   };
   const int nW = build_list(sb + L.xs, P.range_max, wc0, wc1, true, sb + L.lw, M_LISTA);
   const int nU = has_lr ? build_list(sb + L.xu, P.slice_max, uc0, uc1, false, sb + L.lu, M_LISTB) : 0;
+  BT_STAMP(2);
 
   // A fragment of gathered rows: coef(m, kk) = mask_m ? x_m[row kk] : 0,
   // rows from list entries e0 + stride * kk (kk < 16, beyond cnt: 0).
@@ -339,66 +355,83 @@ __global__ void __launch_bounds__(kThreads, 1) batch_forward_kernel(const BatchP
 #pragma unroll
       for (int e = 0; e < 4; ++e) D.d[q][e] = 0.f;
   };
-  // Run `nsteps` steps with kDepth in flight: rows(step, kk) -> address, coef(step, a).
-  auto run_steps = [&](Frag& D, int nsteps, auto&& rowaddr_of, auto&& coef_of, int vch) {
+  // Run `nsteps` steps with kDepth in flight: rows(step, kk) -> address,
+  // coef(step, a, a2) -> one (or, kTwo, two) coefficient fragments,
+  // done(step) after each step's products.
+  auto run_steps = [&](auto two, Frag& D, int nsteps, auto&& rowaddr_of, auto&& coef_of, auto&& vch_of,
+                       auto&& done) {
+    constexpr bool kTwo = decltype(two)::value;
     StepLoad s[kDepth];
 #pragma unroll
     for (int d = 0; d < kDepth; ++d)
-      if (d < nsteps) load_step(s[d], [&](int kk) { return rowaddr_of(d, kk); }, vch);
+      if (d < nsteps) load_step(s[d], [&](int kk) { return rowaddr_of(d, kk); }, vch_of(d));
     for (int st0 = 0; st0 < nsteps; st0 += kDepth) {
 #pragma unroll
       for (int d = 0; d < kDepth; ++d) {
         const int st = st0 + d;
         if (st < nsteps) {
-          uint32_t a[4];
-          coef_of(st, a);
-          mma_step(D, s[d], tile, a, lane);
-          if (st + kDepth < nsteps) load_step(s[d], [&](int kk) { return rowaddr_of(st + kDepth, kk); }, vch);
+          uint32_t a[4], a2[4];
+          coef_of(st, a, a2);
+          mma_step<kTwo>(D, s[d], tile, a, lane, a2);
+          done(st);
+          if (st + kDepth < nsteps)
+            load_step(s[d], [&](int kk) { return rowaddr_of(st + kDepth, kk); }, vch_of(st + kDepth));
         }
       }
     }
   };
+  auto nothing = [](int) {};
 
   const __nv_bfloat16* Wt = static_cast<const __nv_bfloat16*>(P.Wt);
   const __nv_bfloat16* At = static_cast<const __nv_bfloat16*>(P.At);
   const __nv_bfloat16* Bt = static_cast<const __nv_bfloat16*>(P.Bt);
 
-  // ---- stage 1: t_b += sum over the slice's complement rows (all r columns) ----
-  if (has_lr) {
+  // ---- stage 1: t_b += sum over the slice's complement rows (all r columns).
+  // Warp w owns 64-column chunks w, w + 8, ...; its steps run chunk after
+  // chunk in one pipeline (the next chunk's rows load while the previous
+  // chunk finishes), and each chunk is reduced into the L2 t accumulator once. ----
+  if (has_lr && nU > 0) {
     const int nch = (P.r_pad + kColsPerWarp - 1) / kColsPerWarp;
     const int nsteps = (nU + kStage - 1) / kStage;
-    for (int q = warp; q < nch && nU > 0; q += kWarps) {
-      Frag D;
-      zero_frag(D);
-      const int c0 = q * kColsPerWarp;
-      const int vch = min(8, (P.r_pad - c0) / 8);
-      run_steps(
-          D, nsteps,
-          [&](int st, int kk) {
-            const int e = min(st * kStage + kk, nU - 1);
-            const uint32_t j = lds(sb + L.lu + 8u * static_cast<uint32_t>(e));
-            return static_cast<const void*>(Bt + static_cast<size_t>(j) * P.r_pad + c0);
-          },
-          [&](int st, uint32_t(&a)[4]) { frag_list(sb + L.lu, st * kStage, 1, nU, sb + L.xu, P.slice_max, ub0, a); },
-          vch);
+    const int mych = nch > warp ? (nch - warp + kWarps - 1) / kWarps : 0;
+    Frag Dt;
+    zero_frag(Dt);
+    run_steps(
+        std::false_type{}, Dt, mych * nsteps,
+        [&](int i, int kk) {
+          const int qi = i / nsteps, st = i - qi * nsteps, q = warp + kWarps * qi;
+          const int e = min(st * kStage + kk, nU - 1);
+          const uint32_t j = lds(sb + L.lu + 8u * static_cast<uint32_t>(e));
+          return static_cast<const void*>(Bt + static_cast<size_t>(j) * P.r_pad + q * kColsPerWarp);
+        },
+        [&](int i, uint32_t(&a)[4], uint32_t(&)[4]) {
+          const int qi = i / nsteps, st = i - qi * nsteps;
+          frag_list(sb + L.lu, st * kStage, 1, nU, sb + L.xu, P.slice_max, ub0, a);
+        },
+        [&](int i) {
+          const int q = warp + kWarps * (i / nsteps);
+          return min(8, (P.r_pad - q * kColsPerWarp) / 8);
+        },
+        [&](int i) {
+          const int qi = i / nsteps, st = i - qi * nsteps;
+          if (st != nsteps - 1) return;
+          const int c0 = (warp + kWarps * qi) * kColsPerWarp;
 #pragma unroll
-      for (int nb = 0; nb < 8; ++nb) {
-        const int c = c0 + 8 * nb + 2 * t4;
-        if (c < P.r_pad) {
-          if (g < B) {
-            red_add_f32(P.t_acc + static_cast<size_t>(g) * P.r_pad + c, D.d[nb][0]);
-            red_add_f32(P.t_acc + static_cast<size_t>(g) * P.r_pad + c + 1, D.d[nb][1]);
+          for (int nb = 0; nb < 8; ++nb) {
+            const int c = c0 + 8 * nb + 2 * t4;
+            if (c < P.r_pad) {
+              if (g < B) red_add_v2(P.t_acc + static_cast<size_t>(g) * P.r_pad + c, Dt.d[nb][0], Dt.d[nb][1]);
+              if (g + 8 < B) red_add_v2(P.t_acc + static_cast<size_t>(g + 8) * P.r_pad + c, Dt.d[nb][2], Dt.d[nb][3]);
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) Dt.d[nb][e] = 0.f;
           }
-          if (g + 8 < B) {
-            red_add_f32(P.t_acc + static_cast<size_t>(g + 8) * P.r_pad + c, D.d[nb][2]);
-            red_add_f32(P.t_acc + static_cast<size_t>(g + 8) * P.r_pad + c + 1, D.d[nb][3]);
-          }
-        }
-      }
-    }
+        });
   }
   __syncthreads();
+  BT_STAMP(3);
   if (tid == 0) red_release_add(P.ctr, 1u);
+  BT_STAMP(4);
 
   // ---- W rows of U (this warp: row group rg, columns [colw, colw + 64)) ----
   Frag D;
@@ -409,22 +442,24 @@ __global__ void __launch_bounds__(kThreads, 1) batch_forward_kernel(const BatchP
     const int nsteps = (mine + kStage - 1) / kStage;
     if (vch > 0)
       run_steps(
-          D, nsteps,
+          std::false_type{}, D, nsteps,
           [&](int st, int kk) {
             const int e = rg + RG * min(st * kStage + kk, mine - 1);
             const uint32_t j = lds(sb + L.lw + 8u * static_cast<uint32_t>(e));
             return static_cast<const void*>(Wt + static_cast<size_t>(j) * P.m_pad + colw);
           },
-          [&](int st, uint32_t(&a)[4]) {
+          [&](int st, uint32_t(&a)[4], uint32_t(&)[4]) {
             frag_list(sb + L.lw, rg + RG * st * kStage, RG, nW, sb + L.xs, P.range_max, wb0, a);
           },
-          vch);
+          [&](int) { return vch; }, nothing);
   }
 
   // ---- t barrier, then stage 2 over the A_r^T rows [alo, ahi) ----
+  BT_STAMP(5);
   if (has_lr) {
     if (tid == 0) spin_until_count(P.ctr, static_cast<unsigned>(NB));
     __syncthreads();
+    BT_STAMP(6);
     // t -> bf16 hi + lo (t ~= hi + lo to ~2^-16 relative), [hi/lo][b][c - alo]
     for (int i = tid; i < B * na; i += kThreads) {
       const int b = i / na, c = i - b * na;
@@ -440,35 +475,41 @@ __global__ void __launch_bounds__(kThreads, 1) batch_forward_kernel(const BatchP
     const int vch = max(0, min(8, (P.m_pad - colw) / 8));
     const int steps_all = (na + kStage - 1) / kStage;
     const int mine = steps_all > rg ? (steps_all - rg + RG - 1) / RG : 0;  // steps rg, rg + RG, ...
-    for (int part_ = 0; part_ < 2 && vch > 0; ++part_) {  // hi, then lo coefficients
-      const uint32_t tc = sb + L.tco + 2u * static_cast<uint32_t>(part_ * B * P.na_max);
+    if (vch > 0) {  // hi and lo coefficients on the same staged rows
+      const uint32_t th = sb + L.tco, tl = sb + L.tco + 2u * static_cast<uint32_t>(B * P.na_max);
       run_steps(
-          D, mine,
+          std::true_type{}, D, mine,
           [&](int st, int kk) {
             const int c = min((rg + RG * st) * kStage + kk, na - 1);
             return static_cast<const void*>(At + static_cast<size_t>(alo + c) * P.m_pad + colw);
           },
-          [&](int st, uint32_t(&a)[4]) {
+          [&](int st, uint32_t(&a)[4], uint32_t(&a2)[4]) {
             const int cb = (rg + RG * st) * kStage;
-            uint32_t v[2][2][2];
 #pragma unroll
-            for (int h = 0; h < 2; ++h)
+            for (int part_ = 0; part_ < 2; ++part_) {
+              const uint32_t tc = part_ ? tl : th;
+              uint32_t v[2][2][2];
 #pragma unroll
-              for (int tk = 0; tk < 2; ++tk)
+              for (int h = 0; h < 2; ++h)
 #pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                  const int c = cb + 2 * t4 + 8 * h + q, m = g + 8 * tk;
-                  v[h][tk][q] = (c < na && m < B) ? lds_u16(tc + 2u * (m * P.na_max + c)) : 0u;
-                }
-            a[0] = pack_bf16(v[0][0][0], v[0][0][1]);
-            a[1] = pack_bf16(v[0][1][0], v[0][1][1]);
-            a[2] = pack_bf16(v[1][0][0], v[1][0][1]);
-            a[3] = pack_bf16(v[1][1][0], v[1][1][1]);
+                for (int tk = 0; tk < 2; ++tk)
+#pragma unroll
+                  for (int q = 0; q < 2; ++q) {
+                    const int c = cb + 2 * t4 + 8 * h + q, m = g + 8 * tk;
+                    v[h][tk][q] = (c < na && m < B) ? lds_u16(tc + 2u * (m * P.na_max + c)) : 0u;
+                  }
+              uint32_t* o = part_ ? a2 : a;
+              o[0] = pack_bf16(v[0][0][0], v[0][0][1]);
+              o[1] = pack_bf16(v[0][1][0], v[0][1][1]);
+              o[2] = pack_bf16(v[1][0][0], v[1][0][1]);
+              o[3] = pack_bf16(v[1][1][0], v[1][1][1]);
+            }
           },
-          vch);
+          [&](int) { return vch; }, nothing);
     }
   }
 
+  BT_STAMP(7);
   // ---- combine the row groups, then y (split-K reductions at L2) ----
   const uint32_t red = sb + L.red;
   const int tcols = kColsPerWarp * CW;
@@ -480,20 +521,37 @@ __global__ void __launch_bounds__(kThreads, 1) batch_forward_kernel(const BatchP
   }
   __syncthreads();
   const int col0 = ct * tcols;
-  for (int i = tid; i < B * tcols; i += kThreads) {
-    const int b = i / tcols, c = i - b * tcols;
+  const bool vec = (P.m & 3) == 0;
+  for (int i = tid; i < B * (tcols / 4); i += kThreads) {  // 4 consecutive columns per thread
+    const int b = i / (tcols / 4), c = 4 * (i - b * (tcols / 4));
     if (col0 + c >= P.m) continue;
-    float s = 0.f;
-    for (int q = 0; q < RG; ++q) s += ldsf(red + 4u * ((q * 16 + b) * tcols + c));
+    float s4[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int q = 0; q < RG; ++q) {
+      const uint4 u = lds4(red + 4u * ((q * 16 + b) * tcols + c));
+      s4[0] += __uint_as_float(u.x);
+      s4[1] += __uint_as_float(u.y);
+      s4[2] += __uint_as_float(u.z);
+      s4[3] += __uint_as_float(u.w);
+    }
     float* yp = P.y + static_cast<size_t>(b) * P.m + col0 + c;
-    if (KS > 1)
-      red_add_f32(yp, s);
-    else
-      *yp = s;
+    if (vec && col0 + c + 3 < P.m) {
+      if (KS > 1)
+        red_add_v4(yp, s4[0], s4[1], s4[2], s4[3]);
+      else
+        *reinterpret_cast<float4*>(yp) = make_float4(s4[0], s4[1], s4[2], s4[3]);
+    } else {
+      for (int e = 0; e < 4 && col0 + c + e < P.m; ++e) {
+        if (KS > 1)
+          red_add_f32(yp + e, s4[e]);
+        else
+          yp[e] = s4[e];
+      }
+    }
   }
 
   // ---- the last CTA leaves the t accumulator and the counters zero ----
   __syncthreads();
+  BT_STAMP(8);
   if (tid == 0) S.set_m(0, atom_add_acq_rel_gpu(P.ctr + 1, 1u) == static_cast<unsigned>(NB - 1));
   __syncthreads();
   if (S.m(0)) {
@@ -508,6 +566,10 @@ __global__ void __launch_bounds__(kThreads, 1) batch_forward_kernel(const BatchP
 }
 
 size_t batch_smem_bytes(const BatchParams& p) { return BatchSmem::make(p).total; }
+
+cudaError_t batch_trace_copy(long long* host, int count) {
+  return cudaMemcpyFromSymbol(host, g_batch_trace, sizeof(long long) * static_cast<size_t>(count) * 16);
+}
 
 cudaError_t launch_batch(const BatchParams& p, bool x_bf16, cudaStream_t stream) {
   if (!x_bf16) return cudaErrorInvalidValue;

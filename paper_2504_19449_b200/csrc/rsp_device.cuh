@@ -379,6 +379,9 @@ __device__ __forceinline__ uint4 ldg_stream_ef(const void* p, uint64_t pol) {
 
 // Vector float reduction into global memory (sm_90+): no return value,
 // performed at L2.  p must be 16-byte aligned.
+__device__ __forceinline__ void red_add_v2(float* p, float a, float b) {
+  asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(a), "f"(b) : "memory");
+}
 __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
                : "memory");

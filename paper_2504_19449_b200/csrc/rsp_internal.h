@@ -96,7 +96,9 @@ struct BatchParams {
   int n, m, m_pad, r, r_pad, k, B;
   int cw, ks, grid;  // 64 x cw output columns per CTA, ks channel splits, grid = tiles x ks
   int range_max, slice_max, na_max;  // shared-memory carve-up
+  int trace;                         // debug: per-CTA phase clocks into g_batch_trace
 };
+cudaError_t batch_trace_copy(long long* host, int count);
 constexpr size_t kBatchWsBytes(int r_pad) { return 512 + static_cast<size_t>(kBatchMax) * r_pad * 4; }
 size_t batch_smem_bytes(const BatchParams& p);
 cudaError_t launch_batch(const BatchParams& p, bool x_bf16, cudaStream_t stream);
