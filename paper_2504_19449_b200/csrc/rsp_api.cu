@@ -145,6 +145,7 @@ struct rsp_stack {
   cudaGraphExec_t exec = nullptr;
   void* ws = nullptr;
   LinDesc* descs = nullptr;  // device array
+  rsp::LinCtl* ctl = nullptr;  // device control table
   void* plans = nullptr;     // device plan table [count][grid]
   StackParams params = {};   // the captured launch (re-launched by the debug trace)
   int es = 2, grid = 1;
@@ -1013,13 +1014,13 @@ rsp_status rsp_stack_create_ex(const rsp_linear* const* layers, uint32_t count, 
     ks_max = std::max(ks_max, plans[i].k_splits);
     m_pad_max = std::max(m_pad_max, static_cast<int>(h->m_pad));
   }
-  smem = rsp::stack_smem_bytes(n_max, xdt == RSP_BF16, cap_w, cap_u, cap_a);
+  smem = rsp::stack_smem_bytes(n_max, xdt == RSP_BF16, cap_w, cap_u, cap_a, 0, 0, static_cast<int>(count));
   const DevProps& dp = dpx;
   if (smem > static_cast<size_t>(dp.smem_optin))
     return fail(RSP_E_UNSUPPORTED, "stack needs %zu B shared memory (> %d)", smem, dp.smem_optin);
   int abuf = 0, bbuf = 0;
   operand_buffers(static_cast<int>(dp.smem_optin - smem), need_a, need_b, &abuf, &bbuf);
-  smem = rsp::stack_smem_bytes(n_max, xdt == RSP_BF16, cap_w, cap_u, cap_a, abuf, bbuf);
+  smem = rsp::stack_smem_bytes(n_max, xdt == RSP_BF16, cap_w, cap_u, cap_a, abuf, bbuf, static_cast<int>(count));
   const WsLayout wl = WsLayout::make(static_cast<int>(count), nb_pad, r_pad_max, ks_max, m_pad_max);
   auto* s = new rsp_stack();
   s->device = dev;
@@ -1028,6 +1029,11 @@ rsp_status rsp_stack_create_ex(const rsp_linear* const* layers, uint32_t count, 
   if (e == cudaSuccess) e = cudaMemset(s->ws, 0, wl.bytes);
   if (e == cudaSuccess) e = cudaMalloc(&s->descs, sizeof(LinDesc) * count);
   if (e == cudaSuccess) e = cudaMemcpy(s->descs, descs.data(), sizeof(LinDesc) * count, cudaMemcpyHostToDevice);
+  std::vector<rsp::LinCtl> ctl(count);
+  for (uint32_t i = 0; i < count; ++i)
+    ctl[i] = rsp::LinCtl{descs[i].flags, descs[i].dep0, descs[i].ndep, descs[i].cta0, descs[i].grid, descs[i].slot, 0, 0};
+  if (e == cudaSuccess) e = cudaMalloc(&s->ctl, sizeof(rsp::LinCtl) * count);
+  if (e == cudaSuccess) e = cudaMemcpy(s->ctl, ctl.data(), sizeof(rsp::LinCtl) * count, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
   const int knobs = env_int("RSP_KNOBS", 0);
   if (e == cudaSuccess) e = cudaMalloc(&s->plans, static_cast<size_t>(count) * grid * rsp::kPlanBytes);
@@ -1050,6 +1056,7 @@ rsp_status rsp_stack_create_ex(const rsp_linear* const* layers, uint32_t count, 
     p.deterministic = det ? 1 : 0;
     p.knobs = knobs;
     p.plans = s->plans;
+    p.ctl = s->ctl;
     bind_workspace(&p, s->ws, wl);
     s->params = p;
     s->es = h0->es;
@@ -1103,6 +1110,7 @@ void rsp_stack_destroy(rsp_stack* s) {
   cudaFree(s->ws);
   cudaFree(s->descs);
   cudaFree(s->plans);
+  cudaFree(s->ctl);
   delete s;
 }
 

@@ -34,6 +34,12 @@ struct LinDesc {
   int dep0, ndep;  // kLinWaitPrev: wait for linears [dep0, dep0 + ndep) (the previous group) to complete
 };
 
+// What every CTA needs of every linear to walk the stack without touching its
+// full descriptor: membership, dependencies, counter slot (shared memory).
+struct LinCtl {
+  int flags, dep0, ndep, cta0, grid, slot, pad0, pad1;
+};
+
 // Parameters of one launch of the stack kernel (rsp_kernels.cu).
 struct StackParams {
   const LinDesc* descs;  // device array of `count` descriptors (null: use `one`)
@@ -52,6 +58,7 @@ struct StackParams {
   int knobs;                       // experiment switches (env RSP_KNOBS): 1 no W prefetch, 2 no A/B prefetch
   long long* trace;                // debug: [grid][16] phase timestamps of the last linear (null in production)
   const void* plans;               // [count][grid] per-CTA plans (plan_kernel), or null: computed in the kernel
+  const LinCtl* ctl;               // [count] control table, or null (single linear: built from `one`)
 };
 
 // Workspace byte layout for `slots` linears; t_part/y_part sized for the
@@ -73,7 +80,7 @@ struct WsLayout {
 // Shared-memory bytes of the stack kernel for these maxima (without / with
 // the operand buffers).
 size_t stack_smem_bytes(int n_max, bool x_bf16, int cap_w, int cap_u, int cap_a, int abuf_bytes = 0,
-                        int bbuf_bytes = 0);
+                        int bbuf_bytes = 0, int count = 1);
 
 cudaError_t stack_set_smem(size_t smem);
 // Fill a stack's plan table (count x grid entries of kPlanBytes) from its device descriptors.

@@ -54,12 +54,13 @@ constexpr int kRedFloats = 4096;    // 16 KB cross-group reduction scratch
 // level-1 histogram is dead once the cut is known, so the cross-group
 // reduction scratch reuses it.
 struct SmemLayout {
-  uint32_t off_h1, off_cand, off_h2, off_misc, off_red, off_w, off_u, off_a, off_x, off_abuf, off_bbuf, off_h16, total;
+  uint32_t off_h1, off_cand, off_h2, off_misc, off_red, off_w, off_u, off_a, off_x, off_abuf, off_bbuf, off_h16, off_ctl,
+      total;
 
   __host__ __device__ static uint32_t up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
 
   __host__ __device__ static SmemLayout make(int n, bool x_bf16, int cap_w, int cap_u, int cap_a, int abuf = 0,
-                                             int bbuf = 0) {
+                                             int bbuf = 0, int count = 1) {
     SmemLayout L;
     uint32_t o = 0;
     L.off_h1 = o;
@@ -85,6 +86,8 @@ struct SmemLayout {
     o = up(o + static_cast<uint32_t>(bbuf), 16);
     L.off_h16 = o;  // bf16 activations: 15-bit key histogram
     o += 4u * kH16Words;
+    L.off_ctl = o;  // control table of the launch's linears
+    o += static_cast<uint32_t>(sizeof(LinCtl)) * static_cast<uint32_t>(count);
     L.total = up(o, 128);
     return L;
   }
@@ -762,7 +765,8 @@ __device__ __forceinline__ void run_linear(const StackParams& P, const LinDesc& 
 template <typename WT, bool XBF>
 __global__ void __launch_bounds__(kThreads, 1) stack_kernel(const StackParams P) {
   extern __shared__ __align__(16) uint8_t smem[];
-  const SmemLayout L = SmemLayout::make(P.n_max, XBF, P.cap_w, P.cap_u, P.cap_a, P.abuf_bytes, P.bbuf_bytes);
+  const SmemLayout L =
+      SmemLayout::make(P.n_max, XBF, P.cap_w, P.cap_u, P.cap_a, P.abuf_bytes, P.bbuf_bytes, P.count);
   const uint32_t sb = smem_base_pinned(smem);  // shared-window base: every access below is LDS/STS
   Ctx C;
   C.S.xs = sb + L.off_x;
@@ -789,18 +793,45 @@ __global__ void __launch_bounds__(kThreads, 1) stack_kernel(const StackParams P)
   C.S.zero = C.zero;
   const int tid = threadIdx.x, b = blockIdx.x, NB = gridDim.x;
 
-  // x-independent work first: overlaps the previous launch under PDL
-  const LinDesc d0 = P.descs ? P.descs[0] : P.one;
-  uint32_t parity = 0;
-  bool pre = !(P.knobs & 6) && preload_operands<WT>(d0, b, C);
-  const uint8_t* plans = static_cast<const uint8_t*>(P.plans);
-  if (plans) {  // plan of linear 0 from the table
-    if (tid < 6)
-      sts4(plan_slot(C.S, 0) + 16u * tid,
-           __ldg(reinterpret_cast<const uint4*>(plans + static_cast<size_t>(b) * kPlanBytes) + tid));
-  } else {
-    fill_plan<WT>(P, d0, b, C, plan_slot(C.S, 0));
+  // x-independent work first: overlaps the previous launch under PDL.
+  // Control table -> shared memory; this CTA's first member linear's
+  // descriptor and plan -> slot 0.
+  const uint32_t ctl_s = sb + L.off_ctl;
+  static_assert(sizeof(LinCtl) == 32, "control entry");
+  if (P.ctl) {
+    for (int i = tid; i < 2 * P.count; i += kThreads)
+      sts4(ctl_s + 16u * i, __ldg(reinterpret_cast<const uint4*>(P.ctl) + i));
+  } else if (tid == 0) {
+    sts4(ctl_s, make_uint4(static_cast<uint32_t>(P.one.flags), 0u, 0u, static_cast<uint32_t>(P.one.cta0)));
+    sts4(ctl_s + 16u, make_uint4(static_cast<uint32_t>(P.one.grid), static_cast<uint32_t>(P.one.slot), 0u, 0u));
   }
+  __syncthreads();
+  auto ctl_get = [&](int l) {
+    const uint4 u0 = lds4(ctl_s + 32u * l), u1 = lds4(ctl_s + 32u * l + 16u);
+    return LinCtl{static_cast<int>(u0.x), static_cast<int>(u0.y), static_cast<int>(u0.z), static_cast<int>(u0.w),
+                  static_cast<int>(u1.x), static_cast<int>(u1.y), 0, 0};
+  };
+  auto is_member = [&](const LinCtl& c) { return b >= c.cta0 && b < c.cta0 + c.grid; };
+  auto next_member = [&](int l) {  // first member linear after l (P.count: none)
+    int m = l + 1;
+    while (m < P.count && !is_member(ctl_get(m))) ++m;
+    return m;
+  };
+  const uint8_t* plans = static_cast<const uint8_t*>(P.plans);
+  const int m0 = is_member(ctl_get(0)) ? 0 : next_member(0);
+  LinDesc dm = P.one;
+  if (m0 < P.count) {
+    if (P.descs) dm = P.descs[m0];
+    if (plans) {
+      if (tid < 6)
+        sts4(plan_slot(C.S, 0) + 16u * tid,
+             __ldg(reinterpret_cast<const uint4*>(plans + (static_cast<size_t>(m0) * NB + b) * kPlanBytes) + tid));
+    } else {
+      fill_plan<WT>(P, dm, b, C, plan_slot(C.S, 0));
+    }
+  }
+  uint32_t parity = 0;
+  bool pre = m0 < P.count && !(P.knobs & 6) && preload_operands<WT>(dm, b, C);
   sel_clear(C.S);
   if (P.pdl) {
     griddep_wait();
@@ -809,65 +840,70 @@ __global__ void __launch_bounds__(kThreads, 1) stack_kernel(const StackParams P)
   if (tid == 0) C.S.set_m(M_GEN, ld_relaxed_gpu(P.hdr));  // launch epoch (stable during the launch)
   __syncthreads();
   C.epoch = C.S.m(M_GEN);
-  prep_linear<WT, XBF>(P, d0, b, C);
+  if (m0 < P.count) prep_linear<WT, XBF>(P, dm, b, C);
 
-  LinDesc d = d0;
+  int mc = 0;        // member linears run so far (shared slot parity)
+  int mnext = m0;    // this CTA's next member linear
   for (int l = 0; l < P.count; ++l) {
     // debug trace of (linear l, CTA b): [0] globaltimer at iteration start,
     // [13] globaltimer after the dependency wait, [1..12] clock64 phases
     long long* tr = P.trace ? P.trace + (static_cast<size_t>(l) * NB + b) * 16 : nullptr;
     if (tr && tid == 0) tr[0] = gtimer();
-    // Linear l+1's descriptor and this CTA's plan of it -> shared slots
-    // (cp.async, land while linear l runs): the tail between two linears
-    // does no global round trip (it is on the critical path of the slowest CTA).
-    if (plans && l + 1 < P.count && tid < 12) {
-      if (tid < 6)
-        cp_async16_s(desc_slot(C.S, l + 1) + 16u * tid, reinterpret_cast<const uint4*>(P.descs + l + 1) + tid);
-      else
-        cp_async16_s(plan_slot(C.S, l + 1) + 16u * (tid - 6),
-                     reinterpret_cast<const uint4*>(plans + (static_cast<size_t>(l + 1) * NB + b) * kPlanBytes) +
-                         (tid - 6));
-      cp_async_commit();
-    }
-    if (d.flags & kLinWaitPrev) {
+    const LinCtl cl = ctl_get(l);
+    if (cl.flags & kLinWaitPrev) {
       // x of this group is the output of the previous group: every member
       // CTA of each of its linears must have issued its y contributions
       // (every CTA waits here, members of this group's later linears too)
       if (tid == 0) {
-        for (int j = d.dep0; j < d.dep0 + d.ndep; ++j) {
-          const LinDesc* q = P.descs + j;
-          spin_until_count(slot_of(P, q->slot), static_cast<unsigned>(q->grid));
+        for (int j = cl.dep0; j < cl.dep0 + cl.ndep; ++j) {
+          const LinCtl cj = ctl_get(j);
+          spin_until_count(slot_of(P, cj.slot), static_cast<unsigned>(cj.grid));
         }
       }
       __syncthreads();
     }
     if (tr && tid == 0) tr[13] = gtimer();
+    if (l != mnext) continue;  // not a member: nothing else to do (no global round trip)
+    // The next member linear's descriptor and plan -> the other shared slot
+    // (cp.async, land while this linear runs): the tail between two member
+    // linears makes no global round trip (it is on the slowest CTA's path).
+    const int mn = next_member(l);
+    if (plans && mn < P.count && tid < 12) {
+      if (tid < 6)
+        cp_async16_s(desc_slot(C.S, mc + 1) + 16u * tid, reinterpret_cast<const uint4*>(P.descs + mn) + tid);
+      else
+        cp_async16_s(plan_slot(C.S, mc + 1) + 16u * (tid - 6),
+                     reinterpret_cast<const uint4*>(plans + (static_cast<size_t>(mn) * NB + b) * kPlanBytes) +
+                         (tid - 6));
+      cp_async_commit();
+    }
     if (P.knobs & 4) {  // preload at the linear's start: fills the HBM-idle selection window
       __syncthreads();  // previous linear's reads of the operand buffer are complete
-      pre = preload_operands<WT>(d, b, C);
+      pre = preload_operands<WT>(dm, b, C);
     }
-    const bool member = b >= d.cta0 && b < d.cta0 + d.grid;
-    if (member) run_linear<WT, XBF>(P, d, C, tr, pre, parity, plan_slot(C.S, l));
+    run_linear<WT, XBF>(P, dm, C, tr, pre, parity, plan_slot(C.S, mc));
     if (pre) parity ^= 1u;
     cp_async_wait_all();  // this thread's staged copies have landed
     __syncthreads();      // this CTA's y contributions are issued; shared memory is free
-    if (member && tid == 0) red_release_add(slot_of(P, d.slot), 1u);
-    if (l + 1 < P.count) {
+    if (tid == 0) red_release_add(slot_of(P, dm.slot), 1u);
+    ++mc;
+    mnext = mn;
+    if (mn < P.count) {
       if (plans) {
         union {
           LinDesc dd;
           uint4 q[6];
         } u;
 #pragma unroll
-        for (int i = 0; i < 6; ++i) u.q[i] = lds4(desc_slot(C.S, l + 1) + 16u * i);
-        d = u.dd;
+        for (int i = 0; i < 6; ++i) u.q[i] = lds4(desc_slot(C.S, mc) + 16u * i);
+        dm = u.dd;
       } else {
-        d = P.descs[l + 1];
-        fill_plan<WT>(P, d, b, C, plan_slot(C.S, l + 1));
+        dm = P.descs[mn];
+        fill_plan<WT>(P, dm, b, C, plan_slot(C.S, mc));
       }
       // next linear's operands towards shared memory while this one drains (opt-in)
-      pre = !(P.knobs & 6) && preload_operands<WT>(d, b, C);
-      prep_linear<WT, XBF>(P, d, b, C);
+      pre = !(P.knobs & 6) && preload_operands<WT>(dm, b, C);
+      prep_linear<WT, XBF>(P, dm, b, C);
     }
     if (tr && tid == 0) tr[14] = gtimer();
   }
@@ -878,7 +914,7 @@ __global__ void __launch_bounds__(kThreads, 1) stack_kernel(const StackParams P)
   __syncthreads();
   if (C.S.m(M_LAST)) {
     for (int l = 0; l < P.count; ++l) {
-      const int sl = P.descs ? P.descs[l].slot : P.one.slot;
+      const int sl = ctl_get(l).slot;
       if (tid < 2) slot_of(P, sl)[tid] = 0u;
     }
     __threadfence();
@@ -900,8 +936,9 @@ cudaError_t launch_plans(const LinDesc* descs, int count, int grid, int knobs, i
   return cudaGetLastError();
 }
 
-size_t stack_smem_bytes(int n_max, bool x_bf16, int cap_w, int cap_u, int cap_a, int abuf_bytes, int bbuf_bytes) {
-  return SmemLayout::make(n_max, x_bf16, cap_w, cap_u, cap_a, abuf_bytes, bbuf_bytes).total;
+size_t stack_smem_bytes(int n_max, bool x_bf16, int cap_w, int cap_u, int cap_a, int abuf_bytes, int bbuf_bytes,
+                        int count) {
+  return SmemLayout::make(n_max, x_bf16, cap_w, cap_u, cap_a, abuf_bytes, bbuf_bytes, count).total;
 }
 
 cudaError_t stack_set_smem(size_t smem) {
