@@ -86,6 +86,11 @@ bool env_flag(const char* name, bool dflt) {
   return !(v[0] == '0' || v[0] == 'n' || v[0] == 'N' || v[0] == 'f' || v[0] == 'F');
 }
 
+double env_double(const char* name, double dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::atof(v) : dflt;
+}
+
 int env_int(const char* name, int dflt) {
   const char* v = std::getenv(name);
   return (v && *v) ? std::atoi(v) : dflt;
@@ -974,9 +979,13 @@ rsp_status rsp_stack_create_ex(const rsp_linear* const* layers, uint32_t count, 
       const rsp_linear* h = layers[i];
       const uint32_t kk = dense ? h->m_in : h->k;
       const bool lr = !dense && h->rank > 0 && kk < h->m_in;
+      // stage-1 rows stream at roughly half the W rate (short gathered rows,
+      // few in flight), so they weigh more in the CTA split of a group
+      const double bw = env_double("RSP_BWEIGHT", 1.0);
       bytes[i - g0] = static_cast<double>(h->es) *
                       (static_cast<double>(kk) * h->m_pad +
-                       (lr ? static_cast<double>(h->m_in - kk) * h->r_pad + static_cast<double>(h->rank) * h->m_pad : 0.0));
+                       (lr ? bw * static_cast<double>(h->m_in - kk) * h->r_pad + static_cast<double>(h->rank) * h->m_pad
+                           : 0.0));
       tot += bytes[i - g0];
     }
     int cta0 = 0;
