@@ -131,19 +131,51 @@ struct NoSide {
   __device__ __forceinline__ void operator()() const {}
 };
 
+// The first batch of a gathered-row stream, issued ahead of time (its
+// loads fly while the CTA does other work; stream_list consumes it).
+constexpr int kUPre = 8;  // rows of the early batch (registers live across the t hand-off)
+struct FirstBatch {
+  uint2 e[kUPre];
+  uint4 u[kUPre];
+};
+
+__device__ __forceinline__ void issue_first(FirstBatch& f, uint32_t list, int first, int count, int stride,
+                                            bool lane_ok, const uint8_t* base, uint32_t row_bytes, uint64_t pol) {
+  if (lane_ok && first < count) {
+#pragma unroll
+    for (int q = 0; q < kUPre; ++q)
+      f.e[q] = lds2(list + 8u * static_cast<uint32_t>(min(first + q * stride, count - 1)));
+#pragma unroll
+    for (int q = 0; q < kUPre; ++q) f.u[q] = ldg_stream_ef(base + static_cast<size_t>(f.e[q].x) * row_bytes, pol);
+  }
+}
+
 // `side` (run once by every lane) is extra issue-only work -- e.g. cp.async
 // copies -- placed after the first batch's loads, where the warp would
 // otherwise stall on them.
 template <typename WT, class Side = NoSide>
 __device__ __forceinline__ Acc stream_list(uint32_t list, int first, int count, int stride, bool lane_ok,
                                            const uint8_t* base, uint32_t row_bytes, uint64_t pol, uint32_t zero,
-                                           Side&& side = Side()) {
+                                           Side&& side = Side(), const FirstBatch* pre = nullptr) {
   float acc[Vec<WT>::kElems];
 #pragma unroll
   for (int e = 0; e < Vec<WT>::kElems; ++e) acc[e] = 0.f;
   bool side_done = false;
   if (lane_ok) {
-    for (int i0 = first; i0 < count; i0 += stride * kU) {
+    int i0 = first;
+    if (pre && first < count) {  // the batch issued ahead of time (issue_first), peeled
+      side();
+      side_done = true;
+      uint32_t t = 0;
+#pragma unroll
+      for (int q = 0; q < kUPre; ++q) t ^= pre->u[q].x;
+      const float dep = __uint_as_float(t & zero);
+#pragma unroll
+      for (int q = 0; q < kUPre; ++q)
+        Vec<WT>::fma(acc, pre->u[q], (first + q * stride < count ? __uint_as_float(pre->e[q].y) : 0.f) + dep);
+      i0 += stride * kUPre;
+    }
+    for (; i0 < count; i0 += stride * kU) {
       uint2 e[kU];
 #pragma unroll
       for (int q = 0; q < kU; ++q) e[q] = lds2(list + 8u * static_cast<uint32_t>(min(i0 + q * stride, count - 1)));
@@ -575,6 +607,8 @@ __device__ __forceinline__ void run_linear(const StackParams& P, const LinDesc& 
     if (preloaded) mbar_wait_s(C.bar, parity);  // the operand bulk copies have landed
     RSP_TRACE(10);
   }
+  FirstBatch wfirst;
+  bool wpre = false;
   if (spec) {
     if (warp < WS) {
       const int v1 = warp * 32 + lane;
@@ -602,6 +636,11 @@ __device__ __forceinline__ void run_linear(const StackParams& P, const LinDesc& 
     const Acc a1 = os.b_smem ? stream_list_smem<WT>(C.list_u, g1, nU, G1, ok, C.obuf + v1 * 16u, uc0, rowB)
                              : stream_list<WT>(C.list_u, g1, nU, G1, ok, Bt + v1 * 16, rowB, C.pol, C.zero);
     RSP_TRACE(11);
+    // the first batch of this warp's W rows flies during the t hand-off
+    if (!(P.knobs & 1024)) {
+      issue_first(wfirst, C.list_w, g2, nW, G2, ok2, Wt + static_cast<size_t>(col0) * ES + v * 16, rowW, C.pol);
+      wpre = true;
+    }
     if (ok) sts_acc<VE>(C.red + 4u * (g1 * d.r_pad + v1 * VE), a1);
     __syncthreads();
     for (int c = tid; c < d.r_pad; c += kThreads) {
@@ -622,7 +661,7 @@ __device__ __forceinline__ void run_linear(const StackParams& P, const LinDesc& 
 
   // W rows of S (HBM); the t barrier completes meanwhile
   Acc acc = stream_list<WT>(C.list_w, g2, nW, G2, ok2, Wt + static_cast<size_t>(col0) * ES + v * 16, rowW, C.pol,
-                            C.zero, a_copy);
+                            C.zero, a_copy, wpre ? &wfirst : nullptr);
   RSP_TRACE(6);
 
   // ---- 5. stage 2: A_r^T rows [alo, ahi), all warps (tile mapping gA/vA;
