@@ -1047,7 +1047,10 @@ rsp_status rsp_stack_create_ex(const rsp_linear* const* layers, uint32_t count, 
   const int knobs = env_int("RSP_KNOBS", 0);
   if (e == cudaSuccess) e = cudaMalloc(&s->plans, static_cast<size_t>(count) * grid * rsp::kPlanBytes);
   if (e == cudaSuccess)
-    e = rsp::launch_plans(s->descs, static_cast<int>(count), grid, knobs, abuf, h0->es, s->plans, cs);
+    e = rsp::launch_plans(s->descs, static_cast<int>(count), grid, knobs, abuf,
+                          rsp::stack_acopy_bytes(n_max, xdt == RSP_BF16, cap_w, cap_u, cap_a, abuf, bbuf,
+                                                 static_cast<int>(count)),
+                          h0->es, s->plans, cs);
   if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
   if (e == cudaSuccess) e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
   if (e == cudaSuccess) {

@@ -84,8 +84,11 @@ size_t stack_smem_bytes(int n_max, bool x_bf16, int cap_w, int cap_u, int cap_a,
 
 cudaError_t stack_set_smem(size_t smem);
 // Fill a stack's plan table (count x grid entries of kPlanBytes) from its device descriptors.
-cudaError_t launch_plans(const LinDesc* descs, int count, int grid, int knobs, int obuf_bytes, int elem_bytes,
-                         void* out, cudaStream_t stream);
+cudaError_t launch_plans(const LinDesc* descs, int count, int grid, int knobs, int obuf_bytes, int acap,
+                         int elem_bytes, void* out, cudaStream_t stream);
+// Bytes of the stack kernel's dead x + histogram area (A_r^T row copies).
+int stack_acopy_bytes(int n_max, bool x_bf16, int cap_w, int cap_u, int cap_a, int abuf_bytes, int bbuf_bytes,
+                      int count);
 cudaError_t launch_stack(const StackParams& p, int elem_bytes, bool x_bf16, int grid, size_t smem,
                          cudaStream_t stream, bool pdl);
 
