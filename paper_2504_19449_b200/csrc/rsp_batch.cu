@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // Kernel 2: the batched forward of one linear.
 // ---------------------------------------------------------------------------
 struct BatchSmem {
-  uint32_t cuts, xs, xu, lw, lu, misc, tiles, tco, red, total;
+  uint32_t cuts, xs, xu, lw, lu, msk, misc, tiles, tco, red, total;
   __host__ __device__ static uint32_t up(uint32_t v) { return (v + 15u) / 16u * 16u; }
   __host__ __device__ static BatchSmem make(const BatchParams& P) {
     BatchSmem L;
@@ -158,6 +158,8 @@ struct BatchSmem {
     o = up(o + 8u * P.range_max);
     L.lu = o;  // {channel, token mask} of the complements in the stage-1 slice
     o = up(o + 8u * P.slice_max);
+    L.msk = o;  // token masks of one range (list building scratch)
+    o = up(o + 4u * static_cast<uint32_t>((P.range_max > P.slice_max ? P.range_max : P.slice_max) + 64));
     L.tiles = o;  // per warp: one 16 x 64 bf16 step tile
     o += static_cast<uint32_t>(kWarps) * kStage * 128u;
     L.tco = o;  // t of the CTA's A rows: [hi/lo][B][na] bf16
@@ -277,9 +279,12 @@ __global__ void __launch_bounds__(kThreads, 1) batch_forward_kernel(const BatchP
       return m & ((1u << hi_off) - 1u) & ~((1u << lo_off) - 1u);
     };
     uint32_t cnt = 0;
-    for (int c = ch0; c < ch1; ++c) {
+    for (int c = ch0; c < ch1; ++c) {  // pass 1: masks -> scratch, counts
       uint32_t t0, t1;
-      cnt += __popc(members(lo2 + 64 * c + 2 * lane, t0, t1));
+      const int j2 = lo2 + 64 * c + 2 * lane;
+      const uint32_t m = members(j2, t0, t1);
+      cnt += __popc(m);
+      sts2(sb + L.msk + 4u * static_cast<uint32_t>(j2 - lo2), t0 | (m << 30), t1);
     }
     cnt = __reduce_add_sync(0xffffffffu, cnt);
     if (lane == 0) S.set_m(slot + warp, cnt);
@@ -292,10 +297,10 @@ __global__ void __launch_bounds__(kThreads, 1) batch_forward_kernel(const BatchP
       tot += v;
     }
     const uint32_t lt = lanemask_lt();
-    for (int c = ch0; c < ch1; ++c) {
+    for (int c = ch0; c < ch1; ++c) {  // pass 2: from the scratch
       const int j2 = lo2 + 64 * c + 2 * lane;
-      uint32_t t0, t1;
-      const uint32_t m = members(j2, t0, t1);
+      const uint2 tt = lds2(sb + L.msk + 4u * static_cast<uint32_t>(j2 - lo2));
+      const uint32_t m = tt.x >> 30, t0 = tt.x & 0x3fffffffu, t1 = tt.y;
       const uint32_t bal0 = __ballot_sync(0xffffffffu, m & 1u), bal1 = __ballot_sync(0xffffffffu, (m >> 1) & 1u);
       const uint32_t pre = off + __popc(bal0 & lt) + __popc(bal1 & lt);
       sts2_pred(m & 1u, list + 8u * pre, static_cast<uint32_t>(j2), t0);
@@ -323,9 +328,10 @@ __global__ void __launch_bounds__(kThreads, 1) batch_forward_kernel(const BatchP
         const bool ok = e < cnt;
         const uint2 ent = lds2(list + 8u * static_cast<uint32_t>(ok ? e : 0));
         const int jj = static_cast<int>(ent.x) - jbase;
-        const uint32_t v0 = ((ent.y >> g) & 1u) && ok && g < B ? lds_u16(xr + 2u * (g * xstride + jj)) : 0u;
-        const uint32_t v1 =
-            ((ent.y >> (g + 8)) & 1u) && ok && g + 8 < B ? lds_u16(xr + 2u * ((g + 8) * xstride + jj)) : 0u;
+        // unconditional loads (clamped token rows), masked values: no branches
+        const uint32_t m0 = ok ? (ent.y >> g) & 1u : 0u, m1 = ok ? (ent.y >> (g + 8)) & 1u : 0u;
+        const uint32_t v0 = lds_u16(xr + 2u * (min(g, B - 1) * xstride + jj)) & (0u - m0);
+        const uint32_t v1 = lds_u16(xr + 2u * (min(g + 8, B - 1) * xstride + jj)) & (0u - m1);
         if (q == 0) {
           lo[h][0] = v0;
           lo[h][1] = v1;
@@ -496,7 +502,8 @@ __global__ void __launch_bounds__(kThreads, 1) batch_forward_kernel(const BatchP
 #pragma unroll
                   for (int q = 0; q < 2; ++q) {
                     const int c = cb + 2 * t4 + 8 * h + q, m = g + 8 * tk;
-                    v[h][tk][q] = (c < na && m < B) ? lds_u16(tc + 2u * (m * P.na_max + c)) : 0u;
+                    v[h][tk][q] = lds_u16(tc + 2u * (min(m, B - 1) * P.na_max + min(c, na - 1))) &
+                                  (0u - static_cast<uint32_t>((c < na) & (m < B)));
                   }
               uint32_t* o = part_ ? a2 : a;
               o[0] = pack_bf16(v[0][0][0], v[0][0][1]);
