@@ -31,7 +31,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     deps = [os.path.join(CSRC, f) for f in SOURCES + sorted(headers)]
     deps.append(os.path.join(ROOT, "include", "rsparse_b200.h"))
     if force or _stale(LIB, deps):
-        cmd = [NVCC, *ARCH, *FLAGS, *[os.path.join(CSRC, f) for f in SOURCES], "-o", LIB]
+        extra = os.environ.get("RSP_NVCC_EXTRA", "").split()  # experiments, e.g. -DRSP_LDG=1
+        cmd = [NVCC, *ARCH, *FLAGS, *extra, *[os.path.join(CSRC, f) for f in SOURCES], "-o", LIB]
         out = subprocess.run(cmd, capture_output=True, text=True)
         if out.returncode != 0:
             raise RuntimeError("nvcc failed:\n" + out.stdout + out.stderr)

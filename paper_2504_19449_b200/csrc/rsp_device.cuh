@@ -369,11 +369,24 @@ __device__ __forceinline__ void reg_fence(uint4& u) {
 }
 
 // Streamed-once weights: no L1 allocation, first in line for L2 eviction.
+#ifndef RSP_LDG
+#define RSP_LDG 0
+#endif
 __device__ __forceinline__ uint4 ldg_stream_ef(const void* p, uint64_t pol) {
   uint4 u;
+#if RSP_LDG == 1
+  asm volatile("ld.global.cg.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w)
+               : "l"(p), "l"(pol));
+#elif RSP_LDG == 2
+  asm volatile("ld.global.nc.L1::evict_first.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w)
+               : "l"(p), "l"(pol));
+#else
   asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
                : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w)
                : "l"(p), "l"(pol));
+#endif
   return u;
 }
 
