@@ -191,7 +191,7 @@ rsp_status make_plan(const rsp_linear& L, const DevProps& dp, LaunchPlan* out, i
     return fail(RSP_E_UNSUPPORTED, "rank %u too large (B_r^T rows limited to 4 KB, r_pad <= %u)", L.rank,
                 rsp::kTAccCap);
   const int sms = std::max(1, budget > 0 ? std::min(budget, dp.sms) : dp.sms);  // CTAs this linear may use
-  const int ks_cap = std::max(1, env_int("RSP_MAX_KSPLITS", 32));
+  const int ks_cap = std::max(1, env_int("RSP_MAX_KSPLITS", 40));
   int best_nt = 1, best_ks = 1;
   double best = 1e30;
   // with a low-rank term, prefer tiles of at most 4 warp columns: that leaves
