@@ -181,7 +181,7 @@ void operand_buffers(int avail, int need_a, int need_b, int* abuf, int* bbuf) {
 // the next linear's CTAs under PDL).  A column tile is C2 whole 512-byte warp
 // columns of a row (C2 in {1,2,4,8,16}); per-CTA time ~ k*C2/(16*k_splits),
 // and the split-K combine costs k_splits*m float reductions, so the cheapest
-// C2/k_splits wins with k_splits <= 32.
+// C2/k_splits wins with k_splits <= 40 (RSP_MAX_KSPLITS).
 rsp_status make_plan(const rsp_linear& L, const DevProps& dp, LaunchPlan* out, int budget = 0) {
   LaunchPlan p;
   const uint32_t n = L.m_in;
