@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
+    ap.add_argument("--force-sharded", action="store_true",
+                    help="use the row-sharded + all-gather path even on one rank (exercises it on 1 GPU)")
     return ap.parse_args()
 
 
@@ -248,8 +250,12 @@ def run_ours(args):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
-    if world > 1:
+    if world > 1 or args.force_sharded:
         import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=dev)
     import paper_2504_19449_b200 as rsp
     from paper_2504_19449_b200 import workloads as wl
@@ -273,7 +279,8 @@ def run_ours(args):
     ys = [y_dev[yoffs[i]:yoffs[i + 1]] for i in range(len(layers))]
     stream = torch.cuda.Stream(device=dev)
 
-    if world == 1:
+    sharded = world > 1 or args.force_sharded
+    if not sharded:
         # one persistent launch per token; q/k/v and gate/up overlap (shared input)
         st = rsp.Stack(layers, xs, ys, wait_prev=wait)
         launch = lambda: st.launch(stream)  # noqa: E731
@@ -334,16 +341,17 @@ def run_ours(args):
                                "50% model-level sparsity (rho~U(0.3,0.7), C=0.5), bf16 W/x, fp32 accum; "
                                "q/k/v and gate/up share one input (decoder-layer dataflow)",
                    "global_batch": 1, "layers": args.layers, "linears": len(layers),
-                   "parallelism": f"row-shard{world}" + ("+allgather" if world > 1 else ""),
+                   "parallelism": f"row-shard{world}" + ("+allgather" if sharded else ""),
                    "l2": "no flush: 16 GB resident operands >> 126 MB L2",
                    "step_ms_p10_p50_p90": [float(np.percentile(per, q)) for q in (10, 50, 90)]},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": load_traffic(),
+                     "frac": achieved / hbm_peak, "traffic": None if sharded else load_traffic(),
                      "peak_kind": peak_kind, "algorithmic_bytes_per_step": bytes_step,
-                     "kernel": "stack_kernel<bf16,bf16> (1 persistent launch/step, 224 linears)"},
+                     "kernel": ("stack_kernel<bf16,bf16> (1 launch per linear, + NCCL all-gather of y)" if sharded
+                                else "stack_kernel<bf16,bf16> (1 persistent launch/step, 224 linears)")},
         "e2e": {"value": e2e_ms * 1e3, "unit": "us/token", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
-        "gpu_launches": args.steps * (1 if world == 1 else len(layers)),
+        "gpu_launches": args.steps * (len(layers) if sharded else 1),
         "clocks": clocks.summary(),
     }
     out.update(extras)
@@ -356,7 +364,7 @@ def run_ours(args):
                                if k in ("value", "unit", "cores", "kind", "sample")}
     if rank == 0:
         print(json.dumps(out), flush=True)
-    if world > 1:
+    if sharded:
         import torch.distributed as dist
         dist.barrier()
         dist.destroy_process_group()

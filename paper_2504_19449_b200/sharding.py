@@ -19,6 +19,7 @@ of this host logic).  Compute is librsparse_b200.so.
 """
 from __future__ import annotations
 
+import os
 from typing import List, Optional, Sequence, Tuple
 
 from .layer import DecomposedLayer, SparsityPlan, shard_rows
@@ -101,13 +102,28 @@ class ShardedLinear:
         self.row_begin, self.row_end = self.layer.row_begin, self.layer.row_end
         self.in_place = even_shards(self.m_out, self.world)
 
+    @classmethod
+    def from_layer(cls, layer: DecomposedLayer, group=None) -> "ShardedLinear":
+        """Wrap an existing shard (a DecomposedLayer created with
+        shard_rank/shard_count of this group) without re-uploading weights."""
+        self = cls.__new__(cls)
+        self.group = group
+        self.rank, self.world = _group_info(group)
+        self.layer = layer
+        self.m_in, self.m_out = layer.m_in, layer.m_out
+        self.row_begin, self.row_end = layer.row_begin, layer.row_end
+        self.in_place = even_shards(self.m_out, self.world)
+        return self
+
     def forward(self, x, out=None, workspace=None, stream=None):
         if out is None:
             out = torch.empty(self.m_out, dtype=torch.float32, device=x.device)
         if self.in_place and x.dim() == 1:
             mine = out[self.row_begin:self.row_end]
             self.layer.forward(x, out=mine, workspace=workspace, stream=stream)
-            if self.world > 1:
+            # (RSP_FORCE_GATHER=1 runs the collective on a single rank too: exercises
+            # the NCCL-in-graph path on one GPU)
+            if self.world > 1 or (os.environ.get("RSP_FORCE_GATHER") == "1" and dist.is_initialized()):
                 dist.all_gather_into_tensor(out, mine, group=self.group)
             return out
         y_local = self.layer.forward(x, workspace=workspace, stream=stream)
@@ -123,8 +139,9 @@ class ShardedStack:
     captured once into a CUDA graph; one replay = one token through the stack.
     ``xs[i]`` / ``ys[i]`` (full-length fp32) are bound at capture time."""
 
-    def __init__(self, linears: Sequence[ShardedLinear], xs, ys, stream=None):
-        self.linears = list(linears)
+    def __init__(self, linears: Sequence[ShardedLinear], xs, ys, stream=None, group=None):
+        # DecomposedLayer shards (built with shard_rank/shard_count) are wrapped
+        self.linears = [l if isinstance(l, ShardedLinear) else ShardedLinear.from_layer(l, group) for l in linears]
         self.xs, self.ys = list(xs), list(ys)
         self.stream = stream or torch.cuda.Stream()
         # one workspace per linear: the fused kernel's grid barrier words are
