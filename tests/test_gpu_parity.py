@@ -414,3 +414,22 @@ def test_batched_forward_repeatable_and_host(cuda):
     assert maxrel(y2, y1) <= 1e-6
     for t in range(8):
         assert maxrel(y1[t], layer.forward(X[t]).cpu().numpy()) <= TOL_BATCH
+
+
+def test_sharded_bench_path_one_rank(cuda, tmp_path):
+    """bench.py's N > 1 code path (row-sharded linears + NCCL all-gather of y,
+    captured in one graph) run on a single rank with the collective forced on:
+    the driver's multi-GPU runs use this path."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, RSP_FORCE_GATHER="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+           "--master-addr", "127.0.0.1", "--master-port", "29517", os.path.join(root, "bench.py"), "--gpus", "1",
+           "--layers", "1", "--steps", "2", "--warmup", "1", "--force-sharded", "--no-cpu", "--no-dense"]
+    out = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["value"] > 0 and "allgather" in line["config"]["parallelism"]
