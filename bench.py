@@ -287,8 +287,11 @@ def run_ours(args):
     else:
         # row-sharded linears, each followed by one in-place NCCL all-gather
         # of y (paper_2504_19449_b200/sharding.py), captured as one graph
-        from paper_2504_19449_b200.sharding import ShardedStack
-        st = ShardedStack(layers, xs, ys, stream=stream)
+        from paper_2504_19449_b200.sharding import ShardedGroupStack, ShardedStack, even_shards
+        if all(even_shards(l.m_out, world) for l in layers) and not os.environ.get("RSP_PER_LINEAR_SHARDS"):
+            st = ShardedGroupStack(layers, xs, ys, gid, stream=stream)  # one stack launch per input group
+        else:
+            st = ShardedStack(layers, xs, ys, stream=stream)
         launch = st.launch
 
     def barrier():
@@ -342,16 +345,17 @@ def run_ours(args):
                                "q/k/v and gate/up share one input (decoder-layer dataflow)",
                    "global_batch": 1, "layers": args.layers, "linears": len(layers),
                    "parallelism": f"row-shard{world}" + ("+allgather" if sharded else ""),
+                   "sharded_graph": (getattr(st, "graph", None) is not None) if sharded else None,
                    "l2": "no flush: 16 GB resident operands >> 126 MB L2",
                    "step_ms_p10_p50_p90": [float(np.percentile(per, q)) for q in (10, 50, 90)]},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": None if sharded else load_traffic(),
                      "peak_kind": peak_kind, "algorithmic_bytes_per_step": bytes_step,
-                     "kernel": ("stack_kernel<bf16,bf16> (1 launch per linear, + NCCL all-gather of y)" if sharded
+                     "kernel": ("stack_kernel<bf16,bf16> (1 launch per input group, + NCCL all-gather of y)" if sharded
                                 else "stack_kernel<bf16,bf16> (1 persistent launch/step, 224 linears)")},
         "e2e": {"value": e2e_ms * 1e3, "unit": "us/token", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
-        "gpu_launches": args.steps * (len(layers) if sharded else 1),
+        "gpu_launches": args.steps * (max(gid) + 1 if sharded else 1),
         "clocks": clocks.summary(),
     }
     out.update(extras)

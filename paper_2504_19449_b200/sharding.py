@@ -160,3 +160,61 @@ class ShardedStack:
 
     def launch(self):
         self.graph.replay()
+
+
+class ShardedGroupStack:
+    """The row-sharded stack with one persistent stack-kernel launch per input
+    group (q/k/v, o, gate/up, down) instead of one launch per linear: each
+    group's shards run side by side (layer.Stack), then one in-place NCCL
+    all-gather per linear assembles the full y on every rank.  All of it is
+    captured into one CUDA graph when the runtime allows a graph launch
+    inside a capture, else replayed eagerly.  Needs even shards (every
+    BASELINE shape at N <= 8); `ys[i]` are the full-length outputs."""
+
+    def __init__(self, layers: Sequence[DecomposedLayer], xs, ys, gid: Sequence[int], stream=None, group=None):
+        from .layer import Stack
+        self.rank, self.world = _group_info(group)
+        self.group = group
+        self.stream = stream or torch.cuda.Stream()
+        self.layers, self.xs, self.ys = list(layers), list(xs), list(ys)
+        for l in self.layers:
+            if not even_shards(l.m_out, self.world):
+                raise ValueError("ShardedGroupStack needs even row shards")
+        self.groups = []
+        for g in sorted(set(gid)):
+            idx = [i for i in range(len(self.layers)) if gid[i] == g]
+            locs = [self.ys[i][self.layers[i].row_begin:self.layers[i].row_end] for i in idx]
+            st = Stack([self.layers[i] for i in idx], [self.xs[i] for i in idx], locs,
+                       wait_prev=[False] * len(idx))
+            self.groups.append((st, idx, locs))
+        self.force = os.environ.get("RSP_FORCE_GATHER") == "1" and dist.is_initialized()
+        self.graph = None
+        with torch.cuda.stream(self.stream):
+            self._run()  # warm NCCL communicators outside capture
+            torch.cuda.synchronize()
+            try:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=self.stream):
+                    self._run()
+                self.graph = g
+            except RuntimeError:
+                torch.cuda.synchronize()
+                self.graph = None
+
+    def _run(self):
+        for st, idx, locs in self.groups:
+            st.launch(self.stream)
+            if self.world > 1 or self.force:
+                for i, loc in zip(idx, locs):
+                    dist.all_gather_into_tensor(self.ys[i], loc, group=self.group)
+
+    def launch(self):
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            with torch.cuda.stream(self.stream):
+                self._run()
+
+    def close(self):
+        for st, _, _ in self.groups:
+            st.close()
