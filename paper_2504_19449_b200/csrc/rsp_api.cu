@@ -628,7 +628,7 @@ bool batch_plan(const rsp_linear* h, int B, const DevProps& dp, BatchParams* out
     p.na_max = (p.r + ks - 1) / ks + 1;
     if (2 * B * p.range_max > 96 * 1024) continue;
     if (rsp::batch_smem_bytes(p) > static_cast<size_t>(dp.smem_optin)) continue;
-    if (!found || p.grid > best.grid) {
+    if (!found || p.grid >= best.grid) {  // ties: the wider column tile (cw = 8 stages whole rows)
       best = p;
       found = true;
     }

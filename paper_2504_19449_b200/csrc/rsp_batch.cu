@@ -41,6 +41,7 @@ namespace {
 constexpr int kColsPerWarp = 64;  // 8 n-blocks of the m16n8k16 product
 constexpr int kStage = 16;        // rows per mma step (K)
 constexpr int kDepth = 4;         // steps in flight per warp
+constexpr int kRing = 4;          // CTA-cooperative stages (cw == 8)
 
 __device__ __forceinline__ int bpart(int total, int i, int parts) {
   return static_cast<int>(static_cast<uint32_t>(total) * static_cast<uint32_t>(i) / static_cast<uint32_t>(parts));
@@ -102,6 +103,32 @@ __device__ __forceinline__ void mma_step(Frag& D, const StepLoad& s, uint32_t ti
   __syncwarp();  // the tile is rewritten by the next step
 }
 
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Products of one cooperative ring stage (16 rows x 1 KB, 16-byte chunk c of
+// row kk at (c & ~7) | ((c ^ kk) & 7)): warp cw takes chunks 8 cw .. 8 cw + 7.
+template <bool kTwo>
+__device__ __forceinline__ void mma_ring(Frag& D, uint32_t stage, const uint32_t (&a)[4], const uint32_t* a2, int cw,
+                                         int lane) {
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const int kk = (lane & 7) + 8 * ((lane >> 3) & 1), cc = 8 * cw + 2 * p + (lane >> 4);
+    const int pos = (cc & ~7) | ((cc ^ kk) & 7);
+    uint32_t r0, r1, r2, r3;
+    ldsm_x4_trans(stage + static_cast<uint32_t>(kk * 64 + pos) * 16u, r0, r1, r2, r3);
+    mma_bf16(D.d[2 * p], a, r0, r1);
+    mma_bf16(D.d[2 * p + 1], a, r2, r3);
+    if constexpr (kTwo) {
+      const uint32_t b4[4] = {a2[0], a2[1], a2[2], a2[3]};
+      mma_bf16(D.d[2 * p], b4, r0, r1);
+      mma_bf16(D.d[2 * p + 1], b4, r2, r3);
+    }
+  }
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -141,7 +168,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // Kernel 2: the batched forward of one linear.
 // ---------------------------------------------------------------------------
 struct BatchSmem {
-  uint32_t cuts, xs, xu, lw, lu, msk, misc, tiles, tco, red, total;
+  uint32_t cuts, xs, xu, lw, lu, msk, misc, tiles, ring, tco, red, total;
   __host__ __device__ static uint32_t up(uint32_t v) { return (v + 15u) / 16u * 16u; }
   __host__ __device__ static BatchSmem make(const BatchParams& P) {
     BatchSmem L;
@@ -162,6 +189,8 @@ struct BatchSmem {
     o = up(o + 4u * static_cast<uint32_t>((P.range_max > P.slice_max ? P.range_max : P.slice_max) + 64));
     L.tiles = o;  // per warp: one 16 x 64 bf16 step tile
     o += static_cast<uint32_t>(kWarps) * kStage * 128u;
+    L.ring = o;  // cw == 8: CTA-cooperative ring of kRing 16-row x 1 KB stages
+    o += P.cw == 8 ? static_cast<uint32_t>(kRing) * kStage * 1024u : 0u;
     L.tco = o;  // t of the CTA's A rows: [hi/lo][B][na] bf16
     o = up(o + 4u * P.B * P.na_max);
     L.red = o;  // cross-group reduction [RG][16][64 CW] fp32
@@ -387,6 +416,36 @@ __global__ void __launch_bounds__(kThreads, 1) batch_forward_kernel(const BatchP
     }
   };
   auto nothing = [](int) {};
+  // cw == 8: all warps share each step's 16 rows x 1 KB (the CTA's whole
+  // column tile), staged by cp.async in a kRing-deep ring -- every row tile is
+  // fetched as one contiguous 1 KB run by the CTA at once.
+  auto coop_steps = [&](auto two, Frag& D, int nsteps, auto&& rowseg, int vbytes, auto&& coef_of) {
+    constexpr bool kTwo = decltype(two)::value;
+    auto issue = [&](int st) {
+      if (st < nsteps) {
+        const uint32_t stage = sb + L.ring + static_cast<uint32_t>(st % kRing) * kStage * 1024u;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int id = tid + kThreads * q, kk = id >> 6, c = id & 63;
+          const uint8_t* src = static_cast<const uint8_t*>(rowseg(st, kk)) + 16 * (c * 16 < vbytes ? c : 0);
+          cp_async16_s_ef(stage + static_cast<uint32_t>(kk * 64 + ((c & ~7) | ((c ^ kk) & 7))) * 16u, src, pol);
+        }
+      }
+      cp_async_commit();
+    };
+#pragma unroll
+    for (int q = 0; q < kRing - 1; ++q) issue(q);
+    for (int st = 0; st < nsteps; ++st) {
+      cp_async_wait_group<kRing - 2>();
+      __syncthreads();
+      uint32_t a[4], a2[4];
+      coef_of(st, a, a2);
+      mma_ring<kTwo>(D, sb + L.ring + static_cast<uint32_t>(st % kRing) * kStage * 1024u, a, a2, cw, lane);
+      __syncthreads();  // the stage is refilled below
+      issue(st + kRing - 1);
+    }
+    cp_async_wait_group<0>();
+  };
 
   const __nv_bfloat16* Wt = static_cast<const __nv_bfloat16*>(P.Wt);
   const __nv_bfloat16* At = static_cast<const __nv_bfloat16*>(P.At);
@@ -446,7 +505,20 @@ __global__ void __launch_bounds__(kThreads, 1) batch_forward_kernel(const BatchP
     const int vch = max(0, min(8, (P.m_pad - colw) / 8));
     const int mine = nW > rg ? (nW - rg + RG - 1) / RG : 0;  // entries rg, rg + RG, ...
     const int nsteps = (mine + kStage - 1) / kStage;
-    if (vch > 0)
+    const int tcol0 = ct * kColsPerWarp * CW;
+    if (CW == 8)
+      coop_steps(
+          std::false_type{}, D, nsteps,
+          [&](int st, int kk) {
+            const int e = min(st * kStage + kk, nW - 1);
+            const uint32_t j = lds(sb + L.lw + 8u * static_cast<uint32_t>(e));
+            return static_cast<const void*>(Wt + static_cast<size_t>(j) * P.m_pad + tcol0);
+          },
+          min(1024, 2 * (P.m_pad - tcol0)),
+          [&](int st, uint32_t(&a)[4], uint32_t(&)[4]) {
+            frag_list(sb + L.lw, st * kStage, 1, nW, sb + L.xs, P.range_max, wb0, a);
+          });
+    else if (vch > 0)
       run_steps(
           std::false_type{}, D, nsteps,
           [&](int st, int kk) {
@@ -481,8 +553,39 @@ __global__ void __launch_bounds__(kThreads, 1) batch_forward_kernel(const BatchP
     const int vch = max(0, min(8, (P.m_pad - colw) / 8));
     const int steps_all = (na + kStage - 1) / kStage;
     const int mine = steps_all > rg ? (steps_all - rg + RG - 1) / RG : 0;  // steps rg, rg + RG, ...
-    if (vch > 0) {  // hi and lo coefficients on the same staged rows
-      const uint32_t th = sb + L.tco, tl = sb + L.tco + 2u * static_cast<uint32_t>(B * P.na_max);
+    const uint32_t th = sb + L.tco, tl = sb + L.tco + 2u * static_cast<uint32_t>(B * P.na_max);
+    auto coef2 = [&](int cb, uint32_t(&a)[4], uint32_t(&a2)[4]) {
+#pragma unroll
+      for (int part_ = 0; part_ < 2; ++part_) {
+        const uint32_t tc = part_ ? tl : th;
+        uint32_t v[2][2][2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int tk = 0; tk < 2; ++tk)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const int c = cb + 2 * t4 + 8 * h + q, m = g + 8 * tk;
+              v[h][tk][q] = lds_u16(tc + 2u * (min(m, B - 1) * P.na_max + min(c, na - 1))) &
+                            (0u - static_cast<uint32_t>((c < na) & (m < B)));
+            }
+        uint32_t* o = part_ ? a2 : a;
+        o[0] = pack_bf16(v[0][0][0], v[0][0][1]);
+        o[1] = pack_bf16(v[0][1][0], v[0][1][1]);
+        o[2] = pack_bf16(v[1][0][0], v[1][0][1]);
+        o[3] = pack_bf16(v[1][1][0], v[1][1][1]);
+      }
+    };
+    if (CW == 8) {
+      const int tcol0 = ct * kColsPerWarp * CW;
+      coop_steps(
+          std::true_type{}, D, steps_all,
+          [&](int st, int kk) {
+            const int c = min(st * kStage + kk, na - 1);
+            return static_cast<const void*>(At + static_cast<size_t>(alo + c) * P.m_pad + tcol0);
+          },
+          min(1024, 2 * (P.m_pad - tcol0)), [&](int st, uint32_t(&a)[4], uint32_t(&a2)[4]) { coef2(st * kStage, a, a2); });
+    } else if (vch > 0) {  // hi and lo coefficients on the same staged rows
       run_steps(
           std::true_type{}, D, mine,
           [&](int st, int kk) {
