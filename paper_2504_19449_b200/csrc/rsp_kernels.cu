@@ -953,9 +953,9 @@ __global__ void __launch_bounds__(kThreads, 1) stack_kernel(const StackParams P)
   if (tid == 0) C.S.set_m(M_LAST, atom_add_acq_rel_gpu(P.hdr + 1, 1u) == static_cast<unsigned>(NB - 1));
   __syncthreads();
   if (C.S.m(M_LAST)) {
-    for (int l = 0; l < P.count; ++l) {
-      const int sl = ctl_get(l).slot;
-      if (tid < 2) slot_of(P, sl)[tid] = 0u;
+    for (int i = tid; i < 2 * P.count; i += kThreads) {  // all slots at once (on the path to the next launch)
+      const int l = i >> 1;
+      slot_of(P, ctl_get(l).slot)[i & 1] = 0u;
     }
     __threadfence();
     __syncthreads();
