@@ -82,6 +82,21 @@ def main():
             if col.size:
                 ph.append(f"{lab}={np.median(col) / args.mhz:.2f}")
         print(f"{name.split('.', 1)[1]:17s} {g:4d} {start:6.2f} {waitd:6.2f} {end:6.2f} {wall:6.2f} | " + " ".join(ph))
+    # finish spread: absolute time each CTA issued its last y reduction
+    # (dependency-wait stamp + run-relative yred clock), and when the next
+    # group's CTAs saw their dependency satisfied
+    print("linear            finish median/p90/max (us from launch start) | next waitd min/median")
+    for i, (name, m, n, s, r) in enumerate(plans):
+        part = t[i, :, 1] > 0
+        fin = (t[i, part, 13] - t0) / 1e3 + t[i, part, 9] / args.mhz
+        nxt = ""
+        for j in range(i + 1, len(plans)):
+            pj = t[j, :, 1] > 0
+            if pj.any():
+                w = (t[j, pj, 13] - t0) / 1e3
+                nxt = f"{name.split('.', 1)[1]} -> {plans[j][0].split('.', 1)[1]}: {w.min():6.2f} / {np.median(w):6.2f}"
+                break
+        print(f"{name.split('.', 1)[1]:17s} {np.median(fin):6.2f} / {np.percentile(fin, 90):6.2f} / {fin.max():6.2f} | {nxt}")
     for i in range(min(7, len(plans))):
         print(f"stragglers of linear {i} ({plans[i][0]}):")
         stragglers(t, i, args.mhz)
