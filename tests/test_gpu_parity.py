@@ -312,9 +312,11 @@ def test_io_cost_gpu(golden, cuda):
 
 
 @pytest.mark.parametrize("grouped", [False, True])
-def test_stack_graph_matches_individual_forwards(cuda, grouped):
+@pytest.mark.parametrize("dtypes", [("bf16", "bf16"), ("f32", "f32"), ("bf16", "f32")])
+def test_stack_graph_matches_individual_forwards(coracle, cuda, grouped, dtypes):
     # one persistent launch over a decoder layer's 7 linears; grouped: q/k/v
     # and gate/up share one input and overlap (wait_prev False)
+    wdt, xdt = dtypes
     rng = np.random.default_rng(9)
     layers, xs = [], []
     plans = [(f"layers.0.{name}", m, n, 0.0, 64) for (name, m, n) in wl.LLAMA2_7B]
@@ -325,10 +327,12 @@ def test_stack_graph_matches_individual_forwards(cuda, grouped):
         r = 64
         a = torch.randn(m, r, device=cuda) * 0.1
         b = torch.randn(r, n, device=cuda) * 0.1
-        layers.append(rsp.DecomposedLayer(w, a, b, rsp.SparsityPlan(float(rng.uniform(0.15, 0.35)), r)))
+        layers.append(rsp.DecomposedLayer(w, a, b, rsp.SparsityPlan(float(rng.uniform(0.15, 0.35)), r),
+                                          weight_dtype=wdt))
         key = gid[i] if grouped else i
         if key not in xg:
-            xg[key] = torch.from_numpy(wl.heavy_tailed_x(n, rng)).to(cuda).to(torch.bfloat16)
+            xt = torch.from_numpy(wl.heavy_tailed_x(n, rng)).to(cuda)
+            xg[key] = xt.to(torch.bfloat16) if xdt == "bf16" else xt
         xs.append(xg[key])
     ys = [torch.empty(l.m_out, device=cuda) for l in layers]
     st = rsp.Stack(layers, xs, ys, wait_prev=wait if grouped else None)
@@ -337,6 +341,10 @@ def test_stack_graph_matches_individual_forwards(cuda, grouped):
     torch.cuda.synchronize()
     for l, x, y in zip(layers, xs, ys):
         assert maxrel(y.cpu().numpy(), l.forward(x).cpu().numpy()) <= 1e-6
+    # and the stack output itself against the reference semantics (oracle on the device values)
+    for i in (3, 6):
+        yo, _, _ = oracle_on_device_values(coracle, layers[i], xs[i])
+        assert maxrel(ys[i].cpu().numpy(), yo) <= TOL_EXACT_INPUTS, (i, maxrel(ys[i].cpu().numpy(), yo))
     # dense stack == dense forward of each layer
     yd = [torch.empty(l.m_out, device=cuda) for l in layers]
     sd = rsp.Stack(layers, xs, yd, dense=True, wait_prev=wait if grouped else None)
