@@ -580,6 +580,7 @@ __device__ __forceinline__ void run_linear(const StackParams& P, const LinDesc& 
         [&](int i, int j) { sts2(C.list_u + 8u * i, static_cast<uint32_t>(j), sel_bits<XBF>(S, j)); }, &nW, &nU);
   }
   RSP_TRACE(4);
+  if (trace && tid == 0) trace[15] = nW | (static_cast<long long>(nU) << 32);  // debug: this CTA's row counts
   const bool acp = (cp.flags & kPlanACp) != 0;
   // A_r^T tile rows [0, na_s) -> the histogram area (row-major, tw units per
   // row), issued by each warp inside its W stream (side job)

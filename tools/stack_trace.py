@@ -109,10 +109,15 @@ def stragglers(t, i, mhz, top=6):
     end = t[i, idx, 14]
     order = idx[np.argsort(end)[::-1][:top]]
     med = {ev: np.median(t[i, idx, ev]) / mhz for ev in PH}
-    print(f"  median: " + " ".join(f"{PH[ev]}={med[ev]:.2f}" for ev in PH))
+    nw = t[i, idx, 15] & 0xffffffff
+    nu = t[i, idx, 15] >> 32
+    print(f"  median: nW={np.median(nw):.0f} (min {nw.min()}, max {nw.max()}) nU={np.median(nu):.0f} (max {nu.max()}) | "
+          + " ".join(f"{PH[ev]}={med[ev]:.2f}" for ev in PH))
+    fin = t[i, idx, 9]
+    print(f"  corr(finish, nW) = {np.corrcoef(fin, nw)[0, 1]:.2f}  corr(finish, nU) = {np.corrcoef(fin, nu)[0, 1]:.2f}")
     t0 = t[i, idx, 0].min()
     for c in order:
-        print(f"  cta {c:3d} end={(t[i, c, 14] - t0) / 1e3:6.2f} start={(t[i, c, 0] - t0) / 1e3:5.2f} waitd={(t[i, c, 13] - t0) / 1e3:5.2f} | "
+        print(f"  cta {c:3d} nW={t[i, c, 15] & 0xffffffff} nU={t[i, c, 15] >> 32} end={(t[i, c, 14] - t0) / 1e3:6.2f} start={(t[i, c, 0] - t0) / 1e3:5.2f} waitd={(t[i, c, 13] - t0) / 1e3:5.2f} | "
               + " ".join(f"{PH[ev]}={t[i, c, ev] / mhz:.2f}" for ev in PH))
 
 
