@@ -441,3 +441,27 @@ def test_sharded_bench_path_one_rank(cuda, tmp_path):
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
     assert line["value"] > 0 and "allgather" in line["config"]["parallelism"]
+
+
+def test_error_monotonic_in_s_and_r_full_size(cuda):
+    """test_layer.cpp:217-251 at a BASELINE shape on the device: the error
+    against the dense layer falls as more channels are kept (s up) and as the
+    low-rank term grows (r up); s = 1 is the dense layer."""
+    c = wl.config1_layer("o_proj", 4096, 4096, device="cuda")
+    w = c["w"]
+    x = c["x"]
+    dense = (w.double() @ x.double()).cpu().numpy()
+    u, sig, vt = torch.linalg.svd(w.double(), full_matrices=False)
+
+    def err(s, r):
+        a = (u[:, :r] * sig[:r].sqrt()).float()
+        b = (sig[:r].sqrt()[:, None] * vt[:r]).float()
+        layer = rsp.DecomposedLayer(w, a if r else None, b if r else None, rsp.SparsityPlan(s, r),
+                                    weight_dtype="f32")
+        return l2rel(layer.forward(x).cpu().numpy(), dense)
+
+    es = [err(s, 64) for s in (0.1, 0.3, 0.5, 0.8)]
+    assert all(es[i + 1] < es[i] for i in range(len(es) - 1)), es
+    er = [err(0.3, r) for r in (0, 32, 128, 256)]
+    assert all(er[i + 1] < er[i] for i in range(len(er) - 1)), er
+    assert err(1.0, 0) < 1e-6
