@@ -1,6 +1,8 @@
 // rsp_kernels.cu -- sm_100a kernels of the R-Sparse linear operator.
 //
-// The hot path is ONE kernel per linear (linear_kernel):
+// The hot path is ONE persistent kernel per decode token (stack_kernel): it
+// runs every linear of the stack in order; a single forward is a stack of one.
+// Per linear:
 //
 //   y = W[:, S] x_S  +  A_r (B_r[:, S^c] x_{S^c})        (layer.cpp:95-123)
 //
@@ -12,30 +14,28 @@
 //
 // Every term is a gathered-row AXPY over contiguous rows, streamed with
 // 16-byte coalesced loads straight into registers: a warp covers a 512-byte
-// segment of one row per load (32 lanes x 16 B) and keeps U rows in flight
+// segment of one row per load (32 lanes x 16 B) and keeps kU rows in flight
 // (tools/gather_probe.cu: LDG.128 gathers stream as fast as a flat read;
 // 1-D TMA bulk copies of 0.5-4 KB row segments are 1.3-4x slower).
 //
-// Decode is a chain of dependent linears, each only 2-8 us of HBM time, so the
-// kernel is shaped around hiding the fixed per-linear latency (x load,
-// selection, grid barrier, split-K combine; tools/overhead_probe.cu):
-//   * two CTAs fit per SM (256 threads, <= 128 registers, < 110 KB shared memory), and each
-//     CTA releases its dependents (griddepcontrol.launch_dependents) right
-//     after it has waited for its own predecessor, so linear i+1's CTAs sit
-//     next to linear i's on every SM;
-//   * before waiting, a CTA pulls the operands that do not depend on x --
-//     its A_r^T tile rows and its slice of B_r^T -- into L2 (evict_last), so
-//     that traffic fills the previous linear's latency bubbles and stages 1
-//     and 2 later read from L2;
-//   * after the wait: x -> shared memory, the exact top-k cut (rsp_select.cuh),
-//     the CTA's row lists, stage 1 (its channel slice of S^c, partial t into
-//     a global accumulator), arrive on a grid barrier, stream its W rows,
-//     wait on the barrier (long complete), stage 2 on its A_r^T rows, combine.
-// Grid = col_tiles x k_splits CTAs (<= #SMs).  A CTA owns a column tile of
-// whole 512-byte warp columns and a contiguous channel range of W.
-// Split-K partials of y are combined with vector float reductions at L2
-// (fast) or written and summed in a fixed order by the last CTA of each
-// column tile (deterministic mode, bit-reproducible).
+// Decode is a chain of dependent linears, each only 2-8 us of HBM time, so
+// the kernel is shaped around the fixed per-step latency:
+//   * grid = #SMs, one CTA per SM for the whole token; linears reading the
+//     same input (q/k/v, gate/up) run side by side on disjoint CTA partitions;
+//     a group waits on per-linear arrival counters of the previous group;
+//   * per-CTA plans come from a table built once per stack; the next member
+//     linear's descriptor and plan are staged into shared memory by cp.async
+//     while the current one runs (no global round trip between linears);
+//   * after the wait: x -> shared memory + 15-bit key histogram, the exact
+//     top-k cut (rsp_select.cuh), the CTA's row lists, stage 1 (its channel
+//     slice of S^c, partial t reduced at L2), release-arrive on the t barrier
+//     (the first W batch already in flight), the W rows (each warp also
+//     copying A_r^T rows into the dead x + histogram area), acquire-wait on
+//     the barrier, stage 2, combine.
+// A CTA owns a column tile of whole 512-byte warp columns and a contiguous
+// channel range of W.  Split-K partials of y are combined with vector float
+// reductions at L2 (fast) or written and summed in a fixed order by the last
+// CTA of each column tile (deterministic mode, bit-reproducible).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
