@@ -15,7 +15,7 @@ LIB = os.path.join(PKG, "librsparse_b200.so")
 SOURCES = ["rsp_kernels.cu", "rsp_batch.cu", "rsp_api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+FLAGS = ["-O3", "-lineinfo", "--diag-error", "20011,20014", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
          "-Xptxas", "-v", f"-I{os.path.join(ROOT, 'include')}"]
 
 

@@ -622,6 +622,7 @@ bool batch_plan(const rsp_linear* h, int B, const DevProps& dp, BatchParams* out
     p.B = B;
     p.cw = cw;
     p.ks = ks;
+    p.tc = cw == 8 && env_int("RSP_BATCH_TC", 0);
     p.grid = tiles * ks;
     p.range_max = ((n + ks - 1) / ks + 16 + 7) / 8 * 8;  // 8-aligned rows around [wc0, wc1)
     p.slice_max = ((n + p.grid - 1) / p.grid + 16 + 7) / 8 * 8;
@@ -665,7 +666,11 @@ rsp_status rsp_linear_forward(const rsp_linear* h, const void* x, rsp_dtype xdt,
     bp.t_acc = reinterpret_cast<float*>(area + 512);
     bp.trace = env_int("RSP_BATCH_TRACE", 0);
     const cudaStream_t cs = static_cast<cudaStream_t>(stream);
-    if (bp.ks > 1) RSP_CUDA(cudaMemsetAsync(y, 0, sizeof(float) * h->m * batch, cs));
+    const bool has_lr = bp.r > 0 && bp.k < bp.n;
+    bp.zero_y = bp.ks > 1 && has_lr;  // zeroed inside, ahead of the t barrier
+    bp.pdl = env_int("RSP_BATCH_PDL", 1);
+    bp.zero = 0u;
+    if (bp.ks > 1 && !has_lr) RSP_CUDA(cudaMemsetAsync(y, 0, sizeof(float) * h->m * batch, cs));
     cudaError_t e = rsp::launch_batch(bp, true, cs);
     if (e != cudaSuccess) return fail(RSP_E_CUDA, "batched forward launch: %s", cudaGetErrorString(e));
     return RSP_OK;

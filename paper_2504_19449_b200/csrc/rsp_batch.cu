@@ -24,6 +24,7 @@
 //                         CTA per SM): lists of U and of each token's
 //                         complement, stage 1 into an L2 t accumulator, a
 //                         counting barrier, W rows, stage 2, combine.
+#include <algorithm>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -42,6 +43,7 @@ constexpr int kColsPerWarp = 64;  // 8 n-blocks of the m16n8k16 product
 constexpr int kStage = 16;        // rows per mma step (K)
 constexpr int kDepth = 4;         // steps in flight per warp
 constexpr int kRing = 4;          // CTA-cooperative stages (cw == 8)
+constexpr int kRingT = 8;         // tcgen05 ring stages (refill lags the MMAs by two steps)
 
 __device__ __forceinline__ int bpart(int total, int i, int parts) {
   return static_cast<int>(static_cast<uint32_t>(total) * static_cast<uint32_t>(i) / static_cast<uint32_t>(parts));
@@ -103,6 +105,32 @@ __device__ __forceinline__ void mma_step(Frag& D, const StepLoad& s, uint32_t ti
   __syncwarp();  // the tile is rewritten by the next step
 }
 
+// ---- tcgen05 (5th-generation tensor cores, accumulators in TMEM) ----
+// Shared-memory matrix descriptor, no swizzle ("interleave"): core matrices
+// of 8 rows x 16 bytes, LBO / SBO the byte strides between core matrices
+// along the leading (K) / strided dimension (cute UMMA::SmemDescriptor,
+// version 1 for sm_100).
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return static_cast<uint64_t>((saddr >> 4) & 0x3fffu) | (static_cast<uint64_t>((lbo >> 4) & 0x3fffu) << 16) |
+         (static_cast<uint64_t>((sbo >> 4) & 0x3fffu) << 32) | (1ull << 46);
+}
+// kind::f16 instruction descriptor: D f32, A and B bf16, A MN-major, B K-major, M = 128, N = 16.
+constexpr uint32_t kIdescM128N16 = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | ((16u >> 3) << 17) |
+                                   ((128u >> 4) << 24);
+
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(kIdescM128N16), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit(uint32_t mbar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
 template <int N>
 __device__ __forceinline__ void cp_async_wait_group() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
@@ -132,43 +160,10 @@ __device__ __forceinline__ void mma_ring(Frag& D, uint32_t stage, const uint32_t
 }  // namespace
 
 // ---------------------------------------------------------------------------
-// Kernel 1: token blockIdx.x's exact cut.
-// ---------------------------------------------------------------------------
-template <bool XBF>
-__global__ void __launch_bounds__(kThreads, 1)
-    batch_cut_kernel(const void* x, int n, int k, int2* cuts, uint32_t zero) {
-  extern __shared__ __align__(16) uint8_t smem_bc[];
-  const uint32_t sb = smem_base_pinned(smem_bc);
-  SelArea S;
-  S.h1 = sb;
-  S.cand = S.h1 + 4u * kBins;
-  S.h2a = S.cand + 4u * kCandWords;
-  S.h2b = S.h2a + 4u * 256;
-  S.misc = S.h2b + 4u * 256;
-  S.h16 = S.misc + 4u * kMiscWords;
-  S.xs = S.h16 + 4u * kH16Words;
-  S.zero = zero;
-  const uint8_t* xb = static_cast<const uint8_t*>(x) + static_cast<size_t>(blockIdx.x) * n * (XBF ? 2 : 4);
-  Cut cut;
-  if constexpr (XBF) {
-    sel_clear16(S);
-    __syncthreads();
-    sel_load16(xb, n, S);
-    cut = sel_cut16(n, k, S);
-  } else {
-    sel_clear(S);
-    __syncthreads();
-    sel_load<false>(xb, n, S, true);
-    cut = sel_cut<false>(n, k, S);
-  }
-  if (threadIdx.x == 0) cuts[blockIdx.x] = make_int2(static_cast<int>(cut.T), cut.jlim);
-}
-
-// ---------------------------------------------------------------------------
-// Kernel 2: the batched forward of one linear.
+// The batched forward of one linear.
 // ---------------------------------------------------------------------------
 struct BatchSmem {
-  uint32_t cuts, xs, xu, lw, lu, msk, misc, tiles, ring, tco, red, total;
+  uint32_t cuts, xs, xu, lw, lu, msk, misc, tiles, ring, btile, mbar, tco, red, total;
   __host__ __device__ static uint32_t up(uint32_t v) { return (v + 15u) / 16u * 16u; }
   __host__ __device__ static BatchSmem make(const BatchParams& P) {
     BatchSmem L;
@@ -190,12 +185,17 @@ struct BatchSmem {
     L.tiles = o;  // per warp: one 16 x 64 bf16 step tile
     o += static_cast<uint32_t>(kWarps) * kStage * 128u;
     L.ring = o;  // cw == 8: CTA-cooperative ring of kRing 16-row x 1 KB stages
-    o += P.cw == 8 ? static_cast<uint32_t>(kRing) * kStage * 1024u : 0u;
+    const uint32_t nring = P.cw == 8 ? static_cast<uint32_t>(P.tc ? kRingT : kRing) : 0u;
+    o += nring * kStage * 1024u;
+    L.btile = o;  // tcgen05: per ring slot, the B operands (coefficients, hi and lo) 2 x 512 B
+    o += P.tc ? nring * 1024u : 0u;
+    L.mbar = o;   // tcgen05: per ring slot, the MMA-completion mbarrier; then the TMEM address
+    o += 8u * kRingT + 16u;
     L.tco = o;  // t of the CTA's A rows: [hi/lo][B][na] bf16
     o = up(o + 4u * P.B * P.na_max);
     L.red = o;  // cross-group reduction [RG][16][64 CW] fp32
     o += 4u * 16u * static_cast<uint32_t>(kWarps) * kColsPerWarp;
-    L.total = o;
+    L.total = o;  // (CTAs b < B also run a cut from L.lw on: batch_smem_bytes)
     return L;
   }
 };
@@ -220,22 +220,45 @@ __global__ void __launch_bounds__(kThreads, 1) batch_forward_kernel(const BatchP
   const int bid = blockIdx.x, NB = gridDim.x, KS = P.ks, B = P.B;
   const int ct = bid / KS, ks = bid - ct * KS;
   const int CW = P.cw, RG = kWarps / CW, cw = warp % CW, rg = warp / CW;
-  const int wc0 = bpart(P.n, ks, KS), wc1 = bpart(P.n, ks + 1, KS), rw = wc1 - wc0;
-  const int uc0 = bpart(P.n, bid, NB), uc1 = bpart(P.n, bid + 1, NB), ru = uc1 - uc0;
+  const int wc0 = bpart(P.n, ks, KS), wc1 = bpart(P.n, ks + 1, KS);
+  const int uc0 = bpart(P.n, bid, NB), uc1 = bpart(P.n, bid + 1, NB);
   const bool has_lr = P.r > 0 && P.k < P.n;
   const int alo = has_lr ? bpart(P.r, ks, KS) : 0, ahi = has_lr ? bpart(P.r, ks + 1, KS) : 0, na = ahi - alo;
   const int colw = ct * kColsPerWarp * CW + cw * kColsPerWarp;  // this warp's first output column
   const uint32_t tile = sb + L.tiles + static_cast<uint32_t>(warp) * kStage * 128u;
   const uint64_t pol = l2_evict_first_policy();
 
+  // ---- CTA b < B computes token b's exact cut (the batch-1 selector) in the
+  // memory past the activation slabs, published to the grid through ctr[2] ----
+  SelArea C;
+  C.h1 = sb + L.lw;
+  C.cand = C.h1 + 4u * kBins;
+  C.h2a = C.cand + 4u * kCandWords;
+  C.h2b = C.h2a + 4u * 256;
+  C.misc = C.h2b + 4u * 256;
+  C.h16 = C.misc + 4u * kMiscWords;
+  C.xs = C.h16 + 4u * kH16Words;
+  C.zero = P.zero;
+  if (bid < B) sel_clear16(C);  // x-independent: overlaps the previous launch under PDL
+  if (P.pdl) {
+    griddep_wait();  // the previous launch's y (our x) and workspace are complete
+    griddep_launch_dependents();
+  }
+  if (bid < B) {
+    __syncthreads();  // the cleared histogram
+    sel_load16(static_cast<const uint8_t*>(P.x) + static_cast<size_t>(bid) * P.n * 2, P.n, C);
+    const Cut cut = sel_cut16(P.n, P.k, C);
+    if (tid == 0) {
+      P.cuts[bid] = make_int2(static_cast<int>(cut.T), cut.jlim);
+      red_release_add(P.ctr + 2, 1u);
+    }
+  }
+  BT_STAMP(0);
+
   SelArea S{};  // compact2 scratch (misc counters)
   S.misc = sb + L.misc;
 
-  // ---- cuts and the activations of the CTA's channel ranges ----
-  if (tid < B) {
-    const int2 c = P.cuts[tid];
-    sts2(sb + L.cuts + 8u * tid, static_cast<uint32_t>(c.x), static_cast<uint32_t>(c.y));
-  }
+  // ---- the activations of the CTA's channel ranges, then the cuts ----
   // Activations of the CTA's channel ranges, all tokens, in shared memory:
   // rows start at the 8-aligned channels wb0 / ub0 (16-byte vectors).
   const int wb0 = wc0 & ~7, ub0 = uc0 & ~7;
@@ -267,8 +290,32 @@ __global__ void __launch_bounds__(kThreads, 1) batch_forward_kernel(const BatchP
                      "h"(x16[static_cast<size_t>(b) * P.n + ub0 + jj]) : "memory");
     }
   }
+  if (tid == 0) spin_until_count(P.ctr + 2, static_cast<unsigned>(B));
+  __syncthreads();
+  if (tid < B) {
+    const int2 c = __ldcg(P.cuts + tid);
+    sts2(sb + L.cuts + 8u * tid, static_cast<uint32_t>(c.x), static_cast<uint32_t>(c.y));
+  }
   __syncthreads();
   BT_STAMP(1);
+  // (after the cut: its scratch overlaps the ring, the mbarriers and the TMEM slot)
+  const bool tc = P.tc && CW == 8;  // W and stage-2 products on tcgen05 (TMEM accumulators)
+  uint32_t tmem = 0;
+  if (tc) {
+    if (warp == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(sb + L.mbar + 8u * kRingT)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 0) {
+      for (int q = 0; q < kRingT; ++q) mbar_init_s(sb + L.mbar + 8u * q, 1);
+      fence_mbar_init();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    tmem = lds(sb + L.mbar + 8u * kRingT);
+  }
   const uint32_t all = (1u << B) - 1u;
   // Token masks of channels j2, j2 + 1 (j2 even): bit b = channel in S_b
   // (packed-pair key tests against each token's cut).
@@ -447,6 +494,74 @@ __global__ void __launch_bounds__(kThreads, 1) batch_forward_kernel(const BatchP
     cp_async_wait_group<0>();
   };
 
+  // tcgen05 version of coop_steps: the ring stage in the MN-major interleave
+  // layout (chunk c of row kk: core matrix (c, kk / 8) at (2 c + kk / 8) x 128 B),
+  // the step's coefficients as a K-major 16 x 16 B operand, one thread issuing
+  // four M = 128 MMAs per step into the TMEM accumulator (column block q of the
+  // 512-column tile at TMEM columns 16 q), a commit per step to the slot's
+  // mbarrier (the slot is refilled once its MMAs have read it).
+  int gstep = 0;            // ring steps issued so far (slot = gstep % kRingT, parity = gstep / kRingT)
+  uint32_t tc_acc = 0;      // the accumulator holds data
+  auto tc_steps = [&](auto two, int nsteps, auto&& rowseg, int vbytes, auto&& coefB) {
+    constexpr bool kTwo = decltype(two)::value;
+    const int g0 = gstep;
+    auto issue = [&](int st) {
+      if (st < nsteps) {
+        const uint32_t stage = sb + L.ring + static_cast<uint32_t>((g0 + st) % kRingT) * kStage * 1024u;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int id = tid + kThreads * q, kk = id >> 6, c = id & 63;
+          const uint8_t* src = static_cast<const uint8_t*>(rowseg(st, kk)) + 16 * (c * 16 < vbytes ? c : 0);
+          cp_async16_s_ef(stage + static_cast<uint32_t>((2 * c + (kk >> 3)) * 128 + (kk & 7) * 16), src, pol);
+        }
+      }
+      cp_async_commit();
+    };
+    auto wait_slot = [&](int gs) {  // MMAs of global step gs have completed
+      mbar_wait_s(sb + L.mbar + 8u * static_cast<uint32_t>(gs % kRingT), static_cast<uint32_t>((gs / kRingT) & 1));
+    };
+    constexpr int kLook = kRingT - 2;  // steps in flight ahead of the MMAs
+#pragma unroll
+    for (int q = 0; q < kLook; ++q) issue(q);
+    for (int st = 0; st < nsteps; ++st) {
+      const int gs = g0 + st, slot = gs % kRingT;
+      cp_async_wait_group<kLook - 1>();
+      // coefficients (B operand, K-major interleave: (n, k) at ((n/8) 2 + k/8) 128 + (n%8) 16 + (k%8) 2)
+      const uint32_t bt = sb + L.btile + static_cast<uint32_t>(slot) * 1024u;
+      {
+        const int n = tid >> 4, k = tid & 15;
+        const uint32_t off = static_cast<uint32_t>(((n >> 3) * 2 + (k >> 3)) * 128 + (n & 7) * 16 + (k & 7) * 2);
+        asm volatile("st.shared.u16 [%0], %1;" ::"r"(bt + off), "h"(static_cast<unsigned short>(coefB(st, 0, n, k)))
+                     : "memory");
+        if constexpr (kTwo)
+          asm volatile("st.shared.u16 [%0], %1;" ::"r"(bt + 512u + off),
+                       "h"(static_cast<unsigned short>(coefB(st, 1, n, k)))
+                       : "memory");
+      }
+      fence_proxy_async_smem();  // this thread's cp.async data and coefficients -> the async proxy
+      __syncthreads();
+      if (tid == 0) {
+        tc_fence_after();
+        const uint32_t stage = sb + L.ring + static_cast<uint32_t>(slot) * kStage * 1024u;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint64_t ad = umma_desc(stage + 4096u * q, 128u, 256u);
+          tc_mma(tmem + 16u * q, ad, umma_desc(bt, 128u, 256u), tc_acc);
+          if constexpr (kTwo) tc_mma(tmem + 16u * q, ad, umma_desc(bt + 512u, 128u, 256u), 1u);
+        }
+        tc_commit(sb + L.mbar + 8u * static_cast<uint32_t>(slot));
+      }
+      tc_acc = 1u;
+      // refill the slot of step gs - 2 once its MMAs are done (long since, normally)
+      if (st >= 2) wait_slot(gs - 2);
+      issue(st + kLook);
+    }
+    if (nsteps > 1) wait_slot(g0 + nsteps - 2);
+    if (nsteps > 0) wait_slot(g0 + nsteps - 1);
+    cp_async_wait_group<0>();
+    gstep = g0 + nsteps;
+  };
+
   const __nv_bfloat16* Wt = static_cast<const __nv_bfloat16*>(P.Wt);
   const __nv_bfloat16* At = static_cast<const __nv_bfloat16*>(P.At);
   const __nv_bfloat16* Bt = static_cast<const __nv_bfloat16*>(P.Bt);
@@ -493,6 +608,11 @@ __global__ void __launch_bounds__(kThreads, 1) batch_forward_kernel(const BatchP
           }
         });
   }
+  if (P.zero_y) {  // this CTA's share of y, published by the arrival below (the combine waits for it)
+    const int nv = B * P.m;
+    const int v0 = bpart(nv, bid, NB), v1 = bpart(nv, bid + 1, NB);
+    for (int i = v0 + tid; i < v1; i += kThreads) P.y[i] = 0.f;
+  }
   __syncthreads();
   BT_STAMP(3);
   if (tid == 0) red_release_add(P.ctr, 1u);
@@ -506,7 +626,23 @@ __global__ void __launch_bounds__(kThreads, 1) batch_forward_kernel(const BatchP
     const int mine = nW > rg ? (nW - rg + RG - 1) / RG : 0;  // entries rg, rg + RG, ...
     const int nsteps = (mine + kStage - 1) / kStage;
     const int tcol0 = ct * kColsPerWarp * CW;
-    if (CW == 8)
+    if (tc)
+      tc_steps(
+          std::false_type{}, nsteps,
+          [&](int st, int kk) {
+            const int e = min(st * kStage + kk, nW - 1);
+            const uint32_t j = lds(sb + L.lw + 8u * static_cast<uint32_t>(e));
+            return static_cast<const void*>(Wt + static_cast<size_t>(j) * P.m_pad + tcol0);
+          },
+          min(1024, 2 * (P.m_pad - tcol0)),
+          [&](int st, int, int n, int k) -> uint32_t {
+            const int e = st * kStage + k;
+            if (e >= nW || n >= B) return 0u;
+            const uint2 ent = lds2(sb + L.lw + 8u * static_cast<uint32_t>(e));
+            return ((ent.y >> n) & 1u) ? lds_u16(sb + L.xs + 2u * (n * P.range_max + (static_cast<int>(ent.x) - wb0)))
+                                       : 0u;
+          });
+    else if (CW == 8)
       coop_steps(
           std::false_type{}, D, nsteps,
           [&](int st, int kk) {
@@ -576,7 +712,21 @@ __global__ void __launch_bounds__(kThreads, 1) batch_forward_kernel(const BatchP
         o[3] = pack_bf16(v[1][1][0], v[1][1][1]);
       }
     };
-    if (CW == 8) {
+    if (tc) {
+      const int tcol0 = ct * kColsPerWarp * CW;
+      tc_steps(
+          std::true_type{}, steps_all,
+          [&](int st, int kk) {
+            const int c = min(st * kStage + kk, na - 1);
+            return static_cast<const void*>(At + static_cast<size_t>(alo + c) * P.m_pad + tcol0);
+          },
+          min(1024, 2 * (P.m_pad - tcol0)),
+          [&](int st, int part_, int n, int k) -> uint32_t {
+            const int c = st * kStage + k;
+            if (c >= na || n >= B) return 0u;
+            return lds_u16((part_ ? tl : th) + 2u * (n * P.na_max + c));
+          });
+    } else if (CW == 8) {
       const int tcol0 = ct * kColsPerWarp * CW;
       coop_steps(
           std::true_type{}, D, steps_all,
@@ -623,13 +773,36 @@ __global__ void __launch_bounds__(kThreads, 1) batch_forward_kernel(const BatchP
   // ---- combine the row groups, then y (split-K reductions at L2) ----
   const uint32_t red = sb + L.red;
   const int tcols = kColsPerWarp * CW;
+  if (tc) {
+    // TMEM lane m of column block q = output column 128 q + m, column n = token n
+    if (warp < 4) {
+      tc_fence_after();
 #pragma unroll
-  for (int nb = 0; nb < 8; ++nb) {
-    const int c = cw * kColsPerWarp + 8 * nb + 2 * t4;
-    sts2(red + 4u * ((rg * 16 + g) * tcols + c), __float_as_uint(D.d[nb][0]), __float_as_uint(D.d[nb][1]));
-    sts2(red + 4u * ((rg * 16 + g + 8) * tcols + c), __float_as_uint(D.d[nb][2]), __float_as_uint(D.d[nb][3]));
+      for (int q = 0; q < 4; ++q) {
+        uint32_t r[16];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+            "%14, %15}, [%16];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+            : "r"(tmem + (static_cast<uint32_t>(32 * warp) << 16) + 16u * q));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        const int c = 128 * q + 32 * warp + lane;
+#pragma unroll
+        for (int n = 0; n < 16; ++n) sts(red + 4u * (n * tcols + c), tc_acc ? r[n] : 0u);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int nb = 0; nb < 8; ++nb) {
+      const int c = cw * kColsPerWarp + 8 * nb + 2 * t4;
+      sts2(red + 4u * ((rg * 16 + g) * tcols + c), __float_as_uint(D.d[nb][0]), __float_as_uint(D.d[nb][1]));
+      sts2(red + 4u * ((rg * 16 + g + 8) * tcols + c), __float_as_uint(D.d[nb][2]), __float_as_uint(D.d[nb][3]));
+    }
   }
+  tc_fence_before();
   __syncthreads();
+  if (tc && warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem) : "memory");
   const int col0 = ct * tcols;
   const bool vec = (P.m & 3) == 0;
   for (int i = tid; i < B * (tcols / 4); i += kThreads) {  // 4 consecutive columns per thread
@@ -671,11 +844,15 @@ __global__ void __launch_bounds__(kThreads, 1) batch_forward_kernel(const BatchP
     if (tid == 0) {
       P.ctr[0] = 0u;
       P.ctr[1] = 0u;
+      P.ctr[2] = 0u;
     }
   }
 }
 
-size_t batch_smem_bytes(const BatchParams& p) { return BatchSmem::make(p).total; }
+size_t batch_smem_bytes(const BatchParams& p) {
+  const BatchSmem L = BatchSmem::make(p);
+  return std::max<size_t>(L.total, L.lw + select_smem_bytes(p.n, true));
+}
 
 cudaError_t batch_trace_copy(long long* host, int count) {
   return cudaMemcpyFromSymbol(host, g_batch_trace, sizeof(long long) * static_cast<size_t>(count) * 16);
@@ -683,18 +860,21 @@ cudaError_t batch_trace_copy(long long* host, int count) {
 
 cudaError_t launch_batch(const BatchParams& p, bool x_bf16, cudaStream_t stream) {
   if (!x_bf16) return cudaErrorInvalidValue;
-  const size_t cut_smem = select_smem_bytes(p.n, true);
-  cudaError_t e = cudaFuncSetAttribute(batch_cut_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(cut_smem));
-  if (e != cudaSuccess) return e;
-  batch_cut_kernel<true><<<p.B, kThreads, cut_smem, stream>>>(p.x, p.n, p.k, p.cuts, 0u);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
   const size_t smem = batch_smem_bytes(p);
-  e = cudaFuncSetAttribute(batch_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  cudaError_t e = cudaFuncSetAttribute(batch_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  batch_forward_kernel<<<p.grid, kThreads, smem, stream>>>(p);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = p.pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, batch_forward_kernel, p);
 }
 
 }  // namespace rsp

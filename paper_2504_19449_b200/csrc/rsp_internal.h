@@ -99,14 +99,18 @@ struct BatchParams {
   const void* At;   // bf16 [r][m_pad]
   const void* Bt;   // bf16 [n][r_pad]
   const void* x;    // bf16 [B][n]
-  float* y;         // fp32 [B][m]  (zero on entry when ks > 1)
+  float* y;         // fp32 [B][m]  (zero on entry when ks > 1 and !zero_y)
   int2* cuts;       // [B] per-token cuts (workspace)
   float* t_acc;     // [B][r_pad] (workspace; zero on entry, left zero)
-  unsigned* ctr;    // [0] t arrivals, [1] CTAs done (workspace; zero on entry, left zero)
+  unsigned* ctr;    // [0] t arrivals, [1] CTAs done, [2] cuts published (workspace; zero on entry, left zero)
   int n, m, m_pad, r, r_pad, k, B;
   int cw, ks, grid;  // 64 x cw output columns per CTA, ks channel splits, grid = tiles x ks
   int range_max, slice_max, na_max;  // shared-memory carve-up
   int trace;                         // debug: per-CTA phase clocks into g_batch_trace
+  int tc;                            // W / stage-2 products on tcgen05 (cw == 8)
+  int zero_y;                        // the kernel zeroes y before the t barrier (ks > 1, low-rank term)
+  int pdl;                           // launched with programmatic stream serialization
+  unsigned zero;                     // 0, opaque to the compiler (selector load batching)
 };
 cudaError_t batch_trace_copy(long long* host, int count);
 constexpr size_t kBatchWsBytes(int r_pad) { return 512 + static_cast<size_t>(kBatchMax) * r_pad * 4; }

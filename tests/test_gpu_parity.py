@@ -410,6 +410,27 @@ def test_batched_forward_matches_per_token_oracle(coracle, cuda, shape, batch):
         assert maxrel(Y[t], one) <= TOL_BATCH, (t, maxrel(Y[t], one))
 
 
+@pytest.mark.parametrize("shape", [(11008, 4096, 0.27, 687), (4096, 11008, 0.19, 933), (1000, 700, 0.3, 40)])
+@pytest.mark.parametrize("batch", [3, 16])
+def test_batched_tcgen05_variant_matches_oracle(coracle, cuda, monkeypatch, shape, batch):
+    """RSP_BATCH_TC=1: the cooperative ring's products on tcgen05 (TMEM
+    accumulators, one issuing thread, mbarrier-tracked ring slots) instead of
+    warp-level mma.sync -- same per-token semantics and tolerance."""
+    monkeypatch.setenv("RSP_BATCH_TC", "1")
+    m, n, s, r = shape
+    rng = np.random.default_rng(m + 3 * n + batch)
+    w = torch.from_numpy(rng.standard_normal((m, n)).astype(np.float32) * 0.02)
+    a = torch.from_numpy(rng.standard_normal((m, r)).astype(np.float32) * 0.05)
+    b = torch.from_numpy(rng.standard_normal((r, n)).astype(np.float32) * 0.05)
+    layer = rsp.DecomposedLayer(w.to(cuda), a.to(cuda), b.to(cuda), rsp.SparsityPlan(s, r), weight_dtype="bf16")
+    X = torch.stack([torch.from_numpy(wl.heavy_tailed_x(n, rng)) for _ in range(batch)]).to(cuda).to(torch.bfloat16)
+    Y = layer.forward(X).cpu().numpy()
+    W, A, Bm = layer.export()
+    for t in range(batch):
+        want = coracle.forward(np.ascontiguousarray(W.T), A, Bm, layer.plan.keep_fraction, as_seen(X[t]))
+        assert maxrel(Y[t], want) <= TOL_BATCH, (t, maxrel(Y[t], want))
+
+
 def test_batched_forward_repeatable_and_host(cuda):
     """Back-to-back batched launches reuse the workspace (counters and the t
     accumulator are left zero); the host-buffer entry point takes the same path."""

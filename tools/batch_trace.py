@@ -20,7 +20,7 @@ ap.add_argument("--mhz", type=float, default=1965.0)
 a = ap.parse_args()
 dev = torch.device("cuda:0")
 rng = np.random.default_rng(3)
-PH = ["", "stage-x", "lists", "stage1", "arrive", "Wrows", "tbar", "stage2", "combine"]
+PH = ["cut", "stage-x", "lists", "stage1", "arrive", "Wrows", "tbar", "stage2", "combine"]
 for name, m, n, s, r in [("q", 4096, 4096, 0.2, 610), ("gate", 11008, 4096, 0.27, 687), ("down", 4096, 11008, 0.19, 933)]:
     layer = rsp.DecomposedLayer(torch.randn(m, n, device=dev, dtype=torch.bfloat16) * 0.02,
                                 torch.randn(m, r, device=dev, dtype=torch.bfloat16) * 0.05,
@@ -39,4 +39,4 @@ for name, m, n, s, r in [("q", 4096, 4096, 0.2, 610), ("gate", 11008, 4096, 0.27
         t = t[used] / a.mhz
         med = np.median(t, axis=0)
         mx = t.max(axis=0)
-        print(f"{name} B={B} ctas={used.sum()}: " + " ".join(f"{PH[i]}={med[i]:.2f}/{mx[i]:.2f}" for i in range(1, 9)))
+        print(f"{name} B={B} ctas={used.sum()}: " + " ".join(f"{PH[i]}={med[i]:.2f}/{mx[i]:.2f}" for i in range(0, 9)))
