@@ -618,12 +618,15 @@ __device__ __forceinline__ void run_linear(const StackParams& P, const LinDesc& 
       RSP_TRACE(11);
       if (v1 < vb) sts_acc<VE>(C.red + 4u * (v1 * VE), a1);
       named_bar_sync(1, WS * 32);
-      for (int c = tid; c < d.r_pad; c += WS * 32) {
-        const float sum = ldsf(C.red + 4u * c);
-        if (det)
-          P.t_part[static_cast<size_t>(c) * P.nb_pad + b] = sum;
-        else if (sum != 0.f)
-          red_add_f32(t_cur + c, sum);
+      if (det) {
+        for (int c = tid; c < d.r_pad; c += WS * 32) P.t_part[static_cast<size_t>(c) * P.nb_pad + b] = ldsf(C.red + 4u * c);
+      } else {
+        for (int c = 4 * tid; c < d.r_pad; c += 4 * WS * 32) {  // 4 columns per L2 reduction
+          const uint4 u = lds4(C.red + 4u * c);
+          if ((u.x | u.y | u.z | u.w) & 0x7fffffffu)
+            red_add_v4(t_cur + c, __uint_as_float(u.x), __uint_as_float(u.y), __uint_as_float(u.z),
+                       __uint_as_float(u.w));
+        }
       }
       named_bar_sync(1, WS * 32);  // the group's t contributions are issued
       if (tid == 0) red_release_add(slot + 1, 1u);
@@ -644,13 +647,24 @@ __device__ __forceinline__ void run_linear(const StackParams& P, const LinDesc& 
     }
     if (ok) sts_acc<VE>(C.red + 4u * (g1 * d.r_pad + v1 * VE), a1);
     __syncthreads();
-    for (int c = tid; c < d.r_pad; c += kThreads) {
-      float sum = 0.f;
-      for (int g = 0; g < G1; ++g) sum += ldsf(C.red + 4u * (g * d.r_pad + c));
-      if (det)
+    if (det) {
+      for (int c = tid; c < d.r_pad; c += kThreads) {
+        float sum = 0.f;
+        for (int g = 0; g < G1; ++g) sum += ldsf(C.red + 4u * (g * d.r_pad + c));
         P.t_part[static_cast<size_t>(c) * P.nb_pad + b] = sum;
-      else if (sum != 0.f)
-        red_add_f32(t_cur + c, sum);
+      }
+    } else {
+      for (int c = 4 * tid; c < d.r_pad; c += 4 * kThreads) {  // 4 columns per L2 reduction (r_pad % 4 == 0)
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+        for (int g = 0; g < G1; ++g) {
+          const uint4 u = lds4(C.red + 4u * (g * d.r_pad + c));
+          s0 += __uint_as_float(u.x);
+          s1 += __uint_as_float(u.y);
+          s2 += __uint_as_float(u.z);
+          s3 += __uint_as_float(u.w);
+        }
+        if (s0 != 0.f || s1 != 0.f || s2 != 0.f || s3 != 0.f) red_add_v4(t_cur + c, s0, s1, s2, s3);
+      }
     }
     RSP_TRACE(12);
     __syncthreads();  // this CTA's t contributions are issued; `red` is free again
