@@ -240,6 +240,9 @@ __global__ void __launch_bounds__(kThreads, 1) batch_forward_kernel(const BatchP
   C.xs = C.h16 + 4u * kH16Words;
   C.zero = P.zero;
   if (bid < B) sel_clear16(C);  // x-independent: overlaps the previous launch under PDL
+  if (tid == 0 && has_lr && uc1 > uc0)  // the stage-1 slice of B_r^T (contiguous) towards L2 meanwhile
+    prefetch_l2_bulk(static_cast<const uint8_t*>(P.Bt) + static_cast<size_t>(uc0) * P.r_pad * 2,
+                     static_cast<uint32_t>(uc1 - uc0) * static_cast<uint32_t>(P.r_pad) * 2u);
   if (P.pdl) {
     griddep_wait();  // the previous launch's y (our x) and workspace are complete
     griddep_launch_dependents();
