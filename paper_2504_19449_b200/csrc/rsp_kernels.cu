@@ -491,12 +491,19 @@ __device__ __forceinline__ void prep_linear(const StackParams& P, const LinDesc&
     // the CTA's B_r^T channel slice (contiguous, x-independent) towards L2 while
     // the dependency and the selection run: stage 1's rows are a subset of it.
     // Measured -2% per token (2316 -> 2270 us); the same for the A_r^T row
-    // segments (one prefetch per row) costs +5%: its issue stalls the warp.
+    // segments costs +5% (one prefetch per row: its issue stalls the warp) and
+    // +1.8% as one contiguous block per split shared by the column tiles.
     const int u0 = static_cast<int>(lds(plan_addr + 8u)), u1 = static_cast<int>(lds(plan_addr + 12u));
     const uint32_t rowB = static_cast<uint32_t>(d.r_pad) * static_cast<uint32_t>(sizeof(WT));
     if (u1 > u0)
       prefetch_l2_bulk(static_cast<const uint8_t*>(d.Bt) + static_cast<size_t>(u0) * rowB,
                        static_cast<uint32_t>(u1 - u0) * rowB);
+  }
+  if (!(P.knobs & 16384) && tid == 32 && (reinterpret_cast<uintptr_t>(d.x) & 15u) == 0) {
+    // x (contiguous) towards L2 before its producer is done (harmless: L2 is the
+    // coherence point its reductions land in); measured -0.7% (2270 -> 2255 us)
+    const uint32_t xb = static_cast<uint32_t>(d.n) * (XBF ? 2u : 4u);
+    prefetch_l2_bulk(d.x, (xb + 15u) & ~15u);
   }
   const bool det = P.deterministic != 0;
   const int KS = d.k_splits;
