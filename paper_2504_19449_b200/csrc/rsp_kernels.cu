@@ -153,14 +153,18 @@ __device__ __forceinline__ void issue_first(FirstBatch& f, uint32_t list, int fi
 // `side` (run once by every lane) is extra issue-only work -- e.g. cp.async
 // copies -- placed after the first batch's loads, where the warp would
 // otherwise stall on them.
-template <typename WT, class Side = NoSide>
+// `probe` (run once by every lane) is issued right after the last batch's
+// loads -- e.g. an early acquire load of a barrier counter whose round trip
+// then overlaps the batch.
+template <typename WT, class Side = NoSide, class Probe = NoSide>
 __device__ __forceinline__ Acc stream_list(uint32_t list, int first, int count, int stride, bool lane_ok,
                                            const uint8_t* base, uint32_t row_bytes, uint64_t pol, uint32_t zero,
-                                           Side&& side = Side(), const FirstBatch* pre = nullptr) {
+                                           Side&& side = Side(), const FirstBatch* pre = nullptr,
+                                           Probe&& probe = Probe()) {
   float acc[Vec<WT>::kElems];
 #pragma unroll
   for (int e = 0; e < Vec<WT>::kElems; ++e) acc[e] = 0.f;
-  bool side_done = false;
+  bool side_done = false, probed = false;
   if (lane_ok) {
     int i0 = first;
     if (pre && first < count) {  // the batch issued ahead of time (issue_first), peeled
@@ -186,6 +190,10 @@ __device__ __forceinline__ Acc stream_list(uint32_t list, int first, int count, 
         side();
         side_done = true;
       }
+      if (i0 + stride * kU >= count) {
+        probe();
+        probed = true;
+      }
       const float dep = batch_dep(u, zero);
 #pragma unroll
       for (int q = 0; q < kU; ++q)
@@ -193,6 +201,7 @@ __device__ __forceinline__ Acc stream_list(uint32_t list, int first, int count, 
     }
   }
   if (!side_done) side();
+  if (!probed) probe();
   Acc r;
 #pragma unroll
   for (int e = 0; e < 8; ++e) r.v[e] = e < Vec<WT>::kElems ? acc[e] : 0.f;
@@ -694,8 +703,13 @@ __device__ __forceinline__ void run_linear(const StackParams& P, const LinDesc& 
   RSP_TRACE(5);
 
   // W rows of S (HBM); the t barrier completes meanwhile
+  unsigned tprobe = 0u;  // the t barrier's count, loaded early (thread 0) so its round trip overlaps W
+  const bool early = use_bar && !(P.knobs & 32768);
+  auto probe = [&]() {
+    if (early && tid == 0) tprobe = ld_acquire_gpu(slot + 1);
+  };
   Acc acc = stream_list<WT>(C.list_w, g2, nW, G2, ok2, Wt + static_cast<size_t>(col0) * ES + v * 16, rowW, C.pol,
-                            C.zero, a_copy, wpre ? &wfirst : nullptr);
+                            C.zero, a_copy, wpre ? &wfirst : nullptr, probe);
   RSP_TRACE(6);
 
   // ---- 5. stage 2: A_r^T rows [alo, ahi), all warps (tile mapping gA/vA;
@@ -716,7 +730,7 @@ __device__ __forceinline__ void run_linear(const StackParams& P, const LinDesc& 
     }
   }
   if (use_bar) {
-    if (tid == 0) spin_until_count(slot + 1, static_cast<unsigned>(NB));
+    if (tid == 0 && tprobe < static_cast<unsigned>(NB)) spin_until_count(slot + 1, static_cast<unsigned>(NB));
     __syncthreads();
   }
   RSP_TRACE(7);
