@@ -974,10 +974,12 @@ rsp_status rsp_stack_create_ex(const rsp_linear* const* layers, uint32_t count, 
   // its share of the group's bytes.  Deterministic mode shares one
   // partial-sum scratch, so there every linear waits for the previous one.
   std::vector<LaunchPlan> plans(count);
+  std::vector<uint32_t> gstart(count);  // first linear of each linear's group
   uint32_t pg0 = 0, pg1 = 0;  // the previous group
   for (uint32_t g0 = 0; g0 < count;) {
     uint32_t g1 = g0 + 1;
     while (g1 < count && !det && wait_prev && !wait_prev[g1]) ++g1;
+    for (uint32_t i = g0; i < g1; ++i) gstart[i] = g0;
     double tot = 0.0;
     std::vector<double> bytes(g1 - g0);
     for (uint32_t i = g0; i < g1; ++i) {
@@ -1043,13 +1045,17 @@ rsp_status rsp_stack_create_ex(const rsp_linear* const* layers, uint32_t count, 
   if (e == cudaSuccess) e = cudaMemset(s->ws, 0, wl.bytes);
   if (e == cudaSuccess) e = cudaMalloc(&s->descs, sizeof(LinDesc) * count);
   if (e == cudaSuccess) e = cudaMemcpy(s->descs, descs.data(), sizeof(LinDesc) * count, cudaMemcpyHostToDevice);
+  // Completion arrivals go to one counter per group (the slot of its first
+  // linear): a dependent group polls one counter, not one per linear (each
+  // poll is an L2 round trip).  RSP_KNOBS & 65536: one counter per linear.
+  const int knobs = env_int("RSP_KNOBS", 0);
   std::vector<rsp::LinCtl> ctl(count);
   for (uint32_t i = 0; i < count; ++i)
-    ctl[i] = rsp::LinCtl{descs[i].flags, descs[i].dep0, descs[i].ndep, descs[i].cta0, descs[i].grid, descs[i].slot, 0, 0};
+    ctl[i] = rsp::LinCtl{descs[i].flags, descs[i].dep0, descs[i].ndep, descs[i].cta0, descs[i].grid, descs[i].slot,
+                         (knobs & 65536) ? descs[i].slot : descs[gstart[i]].slot, 0};
   if (e == cudaSuccess) e = cudaMalloc(&s->ctl, sizeof(rsp::LinCtl) * count);
   if (e == cudaSuccess) e = cudaMemcpy(s->ctl, ctl.data(), sizeof(rsp::LinCtl) * count, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
-  const int knobs = env_int("RSP_KNOBS", 0);
   if (e == cudaSuccess) e = cudaMalloc(&s->plans, static_cast<size_t>(count) * grid * rsp::kPlanBytes);
   if (e == cudaSuccess)
     e = rsp::launch_plans(s->descs, static_cast<int>(count), grid, knobs, abuf,

@@ -37,7 +37,9 @@ struct LinDesc {
 // What every CTA needs of every linear to walk the stack without touching its
 // full descriptor: membership, dependencies, counter slot (shared memory).
 struct LinCtl {
-  int flags, dep0, ndep, cta0, grid, slot, pad0, pad1;
+  int flags, dep0, ndep, cta0, grid, slot;
+  int aslot;  // slot whose word 0 counts this linear's completed CTAs (shared by its group)
+  int pad1;
 };
 
 // Parameters of one launch of the stack kernel (rsp_kernels.cu).

@@ -891,13 +891,14 @@ __global__ void __launch_bounds__(kThreads, 1) stack_kernel(const StackParams P)
       sts4(ctl_s + 16u * i, __ldg(reinterpret_cast<const uint4*>(P.ctl) + i));
   } else if (tid == 0) {
     sts4(ctl_s, make_uint4(static_cast<uint32_t>(P.one.flags), 0u, 0u, static_cast<uint32_t>(P.one.cta0)));
-    sts4(ctl_s + 16u, make_uint4(static_cast<uint32_t>(P.one.grid), static_cast<uint32_t>(P.one.slot), 0u, 0u));
+    sts4(ctl_s + 16u, make_uint4(static_cast<uint32_t>(P.one.grid), static_cast<uint32_t>(P.one.slot),
+                                 static_cast<uint32_t>(P.one.slot), 0u));
   }
   __syncthreads();
   auto ctl_get = [&](int l) {
     const uint4 u0 = lds4(ctl_s + 32u * l), u1 = lds4(ctl_s + 32u * l + 16u);
     return LinCtl{static_cast<int>(u0.x), static_cast<int>(u0.y), static_cast<int>(u0.z), static_cast<int>(u0.w),
-                  static_cast<int>(u1.x), static_cast<int>(u1.y), 0, 0};
+                  static_cast<int>(u1.x), static_cast<int>(u1.y), static_cast<int>(u1.z), 0};
   };
   auto is_member = [&](const LinCtl& c) { return b >= c.cta0 && b < c.cta0 + c.grid; };
   auto next_member = [&](int l) {  // first member linear after l (P.count: none)
@@ -943,9 +944,18 @@ __global__ void __launch_bounds__(kThreads, 1) stack_kernel(const StackParams P)
       // CTA of each of its linears must have issued its y contributions
       // (every CTA waits here, members of this group's later linears too)
       if (tid == 0) {
-        for (int j = cl.dep0; j < cl.dep0 + cl.ndep; ++j) {
+        // consecutive dependencies sharing an arrival counter: one poll for their summed grids
+        for (int j = cl.dep0, je = cl.dep0 + cl.ndep; j < je;) {
           const LinCtl cj = ctl_get(j);
-          spin_until_count(slot_of(P, cj.slot), static_cast<unsigned>(cj.grid));
+          unsigned target = static_cast<unsigned>(cj.grid);
+          int j2 = j + 1;
+          for (; j2 < je; ++j2) {
+            const LinCtl ck = ctl_get(j2);
+            if (ck.aslot != cj.aslot) break;
+            target += static_cast<unsigned>(ck.grid);
+          }
+          spin_until_count(slot_of(P, cj.aslot), target);
+          j = j2;
         }
       }
       __syncthreads();
@@ -973,7 +983,7 @@ __global__ void __launch_bounds__(kThreads, 1) stack_kernel(const StackParams P)
     if (pre) parity ^= 1u;
     cp_async_wait_all();  // this thread's staged copies have landed
     __syncthreads();      // this CTA's y contributions are issued; shared memory is free
-    if (tid == 0) red_release_add(slot_of(P, dm.slot), 1u);
+    if (tid == 0) red_release_add(slot_of(P, cl.aslot), 1u);
     ++mc;
     mnext = mn;
     if (mn < P.count) {
