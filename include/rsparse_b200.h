@@ -264,6 +264,27 @@ rsp_status rsp_debug_stack_trace(rsp_stack* s, int64_t* trace_dev, uint32_t* gri
  * 5 W rows, 6 t barrier, 7 stage 2, 8 combine). */
 rsp_status rsp_debug_batch_trace(int64_t* host, uint32_t ctas);
 
+/* -- offline factor build, fp64 device buffers ------------------ */
+/* Replaces rsparse::aggregate_scores (scores.cpp:52-62, over score_single_token,
+ * scores.cpp:15-29): scores[i][j] = (1/T) sum_t |sigma_i x_tj Vt_ij| for tokens
+ * x[T][n], sigma[k], vt[k][n]; the token sum in the reference's pairwise tree,
+ * bit-identical.  T == 0 -> RSP_E_USAGE ("requires at least one token"). */
+rsp_status rsp_aggregate_scores(const double* tokens, uint32_t T, uint32_t n, const double* sigma,
+                                const double* vt, uint32_t k, double* scores, void* stream);
+/* Replaces rsparse::select_components (scores.cpp:73-85): the r components of
+ * largest score row mass (ties to the lower index), ascending, into comps[r]
+ * (device); mass[k] (device) receives the row masses.  r > k -> RSP_E_USAGE. */
+rsp_status rsp_select_components(const double* scores, uint32_t k, uint32_t n, uint32_t r, uint32_t* comps,
+                                 double* mass, void* stream);
+/* The factor split of rsparse::decompose_with_svd (layer.cpp:58-66):
+ * a_r[m][r] = U[:, comps] sqrt(sigma[comps]), b_r[r][n] = sqrt(sigma[comps]) Vt[comps, :]
+ * (U is m x ucols row-major, Vt is (>= max comps + 1) x n). */
+rsp_status rsp_split_factors(const double* u, uint32_t m, uint32_t ucols, const double* sigma, const double* vt,
+                             uint32_t n, const uint32_t* comps, uint32_t r, double* a_r, double* b_r, void* stream);
+/* Records a layer's selected components (the decompose_with_svd output kept
+ * by DecomposedLayer::selected_components; written to RSPL files). */
+rsp_status rsp_linear_set_components(rsp_linear* h, const uint32_t* comps, uint32_t r);
+
 /* -- device helpers ------------------------------------------------------------- */
 int rsp_device_sm_count(int device);
 

@@ -253,6 +253,14 @@ class RefOracle(_Lib):
         L.rspr_write_layer.restype = ct.c_int
         L.rspr_read_layer.argtypes = [ct.c_char_p, _u64p, _dp, _dp, _dp, _i64p, _dp]
         L.rspr_read_layer.restype = ct.c_int
+        L.rspr_aggregate_scores.argtypes = [_dp, ct.c_size_t, ct.c_size_t, _dp, _dp, ct.c_size_t,
+                                            ct.c_uint, _dp]
+        L.rspr_aggregate_scores.restype = ct.c_int
+        L.rspr_select_components.argtypes = [_dp, ct.c_size_t, ct.c_size_t, ct.c_size_t, _i64p]
+        L.rspr_select_components.restype = ct.c_int
+        L.rspr_decompose_with_svd.argtypes = [_dp, ct.c_size_t, ct.c_size_t, ct.c_double, ct.c_size_t,
+                                              _dp, ct.c_size_t, _dp, _dp, _dp, _dp, _dp, _i64p]
+        L.rspr_decompose_with_svd.restype = ct.c_int
 
     class Layer:
         """An owned reference DecomposedLayer."""
@@ -315,6 +323,38 @@ class RefOracle(_Lib):
                                                comps.ctypes.data_as(_i64p)), "decompose")
         return (a[: m * rank].reshape(m, rank).copy(), b[: rank * n].reshape(rank, n).copy(),
                 comps[:rank].copy())
+
+    def aggregate_scores(self, tokens, sigma, vt, workers: int = 1) -> np.ndarray:
+        """aggregate_scores (scores.cpp:52-62): tokens [T, n], sigma [kc], vt [kc, n] -> [kc, n]."""
+        tokens, sigma, vt = _as_f64(tokens), _as_f64(sigma), _as_f64(vt)
+        T, n = tokens.shape
+        kc = sigma.shape[0]
+        out = np.empty(kc * n, dtype=np.float64)
+        _raise(self.lib.rspr_aggregate_scores(_d(tokens), T, n, _d(sigma), _d(vt), kc, workers, _d(out)),
+               "aggregate_scores")
+        return out.reshape(kc, n)
+
+    def select_components(self, scores, r: int) -> np.ndarray:
+        """select_components (scores.cpp:73-85) -> ascending component indices."""
+        scores = _as_f64(scores)
+        kc, n = scores.shape
+        comps = np.empty(max(r, 1), dtype=np.int64)
+        _raise(self.lib.rspr_select_components(_d(scores), kc, n, r, comps.ctypes.data_as(_i64p)),
+               "select_components")
+        return comps[:r].copy()
+
+    def decompose_with_svd(self, w, keep_fraction: float, rank: int, scores, u, sigma, vt):
+        """decompose_with_svd (layer.cpp:35-68) -> a_r, b_r, comps."""
+        w, scores, u, sigma, vt = (_as_f64(a) for a in (w, scores, u, sigma, vt))
+        m, n = w.shape
+        kc = sigma.shape[0]
+        a = np.empty(max(m * rank, 1), dtype=np.float64)
+        b = np.empty(max(rank * n, 1), dtype=np.float64)
+        comps = np.empty(max(rank, 1), dtype=np.int64)
+        _raise(self.lib.rspr_decompose_with_svd(_d(w), m, n, keep_fraction, rank, _d(scores), kc, _d(u), _d(sigma),
+                                                _d(vt), _d(a), _d(b), comps.ctypes.data_as(_i64p)),
+               "decompose_with_svd")
+        return (a[: m * rank].reshape(m, rank).copy(), b[: rank * n].reshape(rank, n).copy(), comps[:rank].copy())
 
     def write_layer(self, path: str, w_cols, a_r, b_r, keep_fraction: float, comps=None) -> None:
         """write_decomposed_layer (layer.cpp:243-267) of the layer built from these arrays."""

@@ -207,6 +207,47 @@ int rspr_decompose_uniform(const double* w, size_t m_out, size_t m_in, double ke
   })
 }
 
+// scores.cpp:52-62 (aggregate_scores over score_single_token): tokens[T][n],
+// sigma[kc], vt[kc][n] -> scores[kc][n].  num_workers > 1 exercises the
+// reference's threaded tree (same result by construction).
+int rspr_aggregate_scores(const double* tokens, size_t T, size_t n, const double* sigma, const double* vt,
+                          size_t kc, unsigned num_workers, double* scores) {
+  GUARD({
+    std::vector<std::vector<double>> tok(T);
+    for (size_t t = 0; t < T; ++t) tok[t].assign(tokens + t * n, tokens + (t + 1) * n);
+    SvdResult svd{Matrix(1, kc), std::vector<double>(sigma, sigma + kc),
+                  Matrix(kc, n, std::vector<double>(vt, vt + kc * n))};
+    const ScoreMatrix sc = aggregate_scores(tok, svd, "", num_workers);
+    std::memcpy(scores, sc.values.data(), kc * n * sizeof(double));
+  })
+}
+
+// scores.cpp:73-85 (select_components): scores[kc][n] -> comps[r] ascending
+int rspr_select_components(const double* scores, size_t kc, size_t n, size_t r, int64_t* comps) {
+  GUARD({
+    const ScoreMatrix sc{Matrix(kc, n, std::vector<double>(scores, scores + kc * n)), 1, ""};
+    const std::vector<size_t> c = select_components(sc, r);
+    for (size_t i = 0; i < c.size(); ++i) comps[i] = static_cast<int64_t>(c[i]);
+  })
+}
+
+// layer.cpp:35-68 (decompose_with_svd) with caller-supplied scores and SVD:
+// w[m][n], scores[kc][n], u[m][kc], sigma[kc], vt[kc][n] -> a_r[m][r], b_r[r][n], comps[r]
+int rspr_decompose_with_svd(const double* w, size_t m_out, size_t m_in, double keep_fraction, size_t rank,
+                            const double* scores, size_t kc, const double* u, const double* sigma,
+                            const double* vt, double* a_r, double* b_r, int64_t* comps) {
+  GUARD({
+    Matrix W(m_out, m_in, std::vector<double>(w, w + m_out * m_in));
+    const ScoreMatrix sc{Matrix(kc, m_in, std::vector<double>(scores, scores + kc * m_in)), 1, ""};
+    SvdResult svd{Matrix(m_out, kc, std::vector<double>(u, u + m_out * kc)), std::vector<double>(sigma, sigma + kc),
+                  Matrix(kc, m_in, std::vector<double>(vt, vt + kc * m_in))};
+    const DecomposedLayer L = decompose_with_svd(W, SparsityPlan{keep_fraction, rank}, sc, svd);
+    std::memcpy(a_r, L.a_r.data(), m_out * rank * sizeof(double));
+    std::memcpy(b_r, L.b_r.data(), rank * m_in * sizeof(double));
+    for (size_t c = 0; c < rank; ++c) comps[c] = static_cast<int64_t>(L.selected_components[c]);
+  })
+}
+
 // layer.cpp:161-210 (the reference's own fp32 timing harness)
 int rspr_bench_matvec(size_t m_in, size_t m_out, double s, size_t reps, uint64_t seed,
                       double* dense_ns, double* gather_ns, uint64_t* dense_bytes,

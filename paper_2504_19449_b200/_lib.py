@@ -25,6 +25,7 @@ EXPORTS = [
     "rsp_top_k_by_magnitude", "rsp_threshold_sparsify", "rsp_stack_create", "rsp_stack_create_ex",
     "rsp_stack_launch", "rsp_stack_destroy", "rsp_device_sm_count", "rsp_debug_forward_trace",
     "rsp_debug_stack_trace", "rsp_debug_batch_trace", "rsp_rspl_read", "rsp_linear_load_rspl", "rsp_linear_save_rspl", "rsp_linear_components",
+    "rsp_aggregate_scores", "rsp_select_components", "rsp_split_factors", "rsp_linear_set_components",
 ]
 
 
@@ -139,6 +140,10 @@ def lib() -> ct.CDLL:
         "rsp_linear_load_rspl": (ct.c_int, [ct.c_char_p, ct.POINTER(LinearDesc), ct.POINTER(vp)]),
         "rsp_linear_save_rspl": (ct.c_int, [vp, ct.c_char_p]),
         "rsp_linear_components": (ct.c_int, [vp, ct.POINTER(u32)]),
+        "rsp_aggregate_scores": (ct.c_int, [vp, u32, u32, vp, vp, u32, vp, vp]),
+        "rsp_select_components": (ct.c_int, [vp, u32, u32, u32, vp, vp, vp]),
+        "rsp_split_factors": (ct.c_int, [vp, u32, u32, vp, vp, u32, vp, u32, vp, vp, vp]),
+        "rsp_linear_set_components": (ct.c_int, [vp, ct.POINTER(u32), u32]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -12,7 +12,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.environ.get("RSP_LIB") or os.path.join(PKG, "librsparse_b200.so")  # RSP_LIB: debug override (A/B of builds)
-SOURCES = ["rsp_kernels.cu", "rsp_batch.cu", "rsp_api.cu"]
+SOURCES = ["rsp_kernels.cu", "rsp_batch.cu", "rsp_offline.cu", "rsp_api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "--diag-error", "20011,20014", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",

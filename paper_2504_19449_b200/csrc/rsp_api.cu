@@ -846,6 +846,41 @@ rsp_status rsp_linear_components(const rsp_linear* h, uint32_t* comps) {
   return RSP_OK;
 }
 
+rsp_status rsp_linear_set_components(rsp_linear* h, const uint32_t* comps, uint32_t r) {
+  if (!h || (r && !comps)) return fail(RSP_E_USAGE, "null handle or buffer");
+  if (r != h->rank) return fail(RSP_E_USAGE, "%u components for a rank-%u layer", r, h->rank);
+  h->comps.assign(comps, comps + r);
+  return RSP_OK;
+}
+
+rsp_status rsp_aggregate_scores(const double* tokens, uint32_t T, uint32_t n, const double* sigma,
+                                const double* vt, uint32_t k, double* scores, void* stream) {
+  if (T == 0) return fail(RSP_E_USAGE, "aggregate_scores requires at least one token");  // scores.cpp:55
+  if (n == 0 || k == 0) return RSP_OK;
+  if (!tokens || !sigma || !vt || !scores) return fail(RSP_E_USAGE, "null buffer");
+  const cudaError_t e = rsp::launch_scores(tokens, T, n, sigma, vt, k, scores, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? RSP_OK : fail(RSP_E_CUDA, "aggregate_scores: %s", cudaGetErrorString(e));
+}
+
+rsp_status rsp_select_components(const double* scores, uint32_t k, uint32_t n, uint32_t r, uint32_t* comps,
+                                 double* mass, void* stream) {
+  if (r > k)  // scores.cpp:74-77
+    return fail(RSP_E_USAGE, "select_components: r=%u exceeds component count %u", r, k);
+  if (k == 0) return RSP_OK;
+  if (!scores || !mass || (r && !comps)) return fail(RSP_E_USAGE, "null buffer");
+  const cudaError_t e = rsp::launch_select_components(scores, k, n, r, comps, mass, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? RSP_OK : fail(RSP_E_CUDA, "select_components: %s", cudaGetErrorString(e));
+}
+
+rsp_status rsp_split_factors(const double* u, uint32_t m, uint32_t ucols, const double* sigma, const double* vt,
+                             uint32_t n, const uint32_t* comps, uint32_t r, double* a_r, double* b_r, void* stream) {
+  if (r == 0) return RSP_OK;
+  if (!u || !sigma || !vt || !comps || !a_r || !b_r) return fail(RSP_E_USAGE, "null buffer");
+  const cudaError_t e =
+      rsp::launch_split_factors(u, m, ucols, sigma, vt, n, comps, r, a_r, b_r, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? RSP_OK : fail(RSP_E_CUDA, "split_factors: %s", cudaGetErrorString(e));
+}
+
 rsp_status rsp_top_k_by_magnitude(const void* x, rsp_dtype xdt, uint32_t n, uint32_t k,
                                   int32_t* kept, int32_t* rest, void* stream) {
   if (k > n)  // matrix.cpp:101-104

@@ -115,6 +115,15 @@ struct BatchParams {
   unsigned zero;                     // 0, opaque to the compiler (selector load batching)
 };
 cudaError_t batch_trace_copy(long long* host, int count);
+
+// Offline factor build (rsp_offline.cu), fp64.
+cudaError_t launch_scores(const double* x, uint32_t T, uint32_t n, const double* sigma, const double* vt, uint32_t k,
+                          double* out, cudaStream_t s);
+cudaError_t launch_select_components(const double* scores, uint32_t k, uint32_t n, uint32_t r, uint32_t* comps,
+                                     double* mass, cudaStream_t s);
+cudaError_t launch_split_factors(const double* u, uint32_t m, uint32_t ucols, const double* sigma, const double* vt,
+                                 uint32_t n, const uint32_t* comps, uint32_t r, double* a_r, double* b_r,
+                                 cudaStream_t s);
 constexpr size_t kBatchWsBytes(int r_pad) { return 512 + static_cast<size_t>(kBatchMax) * r_pad * 4; }
 size_t batch_smem_bytes(const BatchParams& p);
 cudaError_t launch_batch(const BatchParams& p, bool x_bf16, cudaStream_t stream);
