@@ -253,6 +253,8 @@ class RefOracle(_Lib):
         L.rspr_write_layer.restype = ct.c_int
         L.rspr_read_layer.argtypes = [ct.c_char_p, _u64p, _dp, _dp, _dp, _i64p, _dp]
         L.rspr_read_layer.restype = ct.c_int
+        L.rspr_mlp_forward.argtypes = [ct.c_void_p, ct.c_void_p, ct.c_void_p, _dp, ct.c_size_t, _dp]
+        L.rspr_mlp_forward.restype = ct.c_int
         L.rspr_aggregate_scores.argtypes = [_dp, ct.c_size_t, ct.c_size_t, _dp, _dp, ct.c_size_t,
                                             ct.c_uint, _dp]
         L.rspr_aggregate_scores.restype = ct.c_int
@@ -323,6 +325,13 @@ class RefOracle(_Lib):
                                                comps.ctypes.data_as(_i64p)), "decompose")
         return (a[: m * rank].reshape(m, rank).copy(), b[: rank * n].reshape(rank, n).copy(),
                 comps[:rank].copy())
+
+    def mlp_forward(self, up: "RefOracle.Layer", gate: "RefOracle.Layer", down: "RefOracle.Layer", x) -> np.ndarray:
+        """mlp_forward (model.cpp:115-127): down(up(x) * silu(gate(x)))."""
+        x = _as_f64(x)
+        out = np.empty(x.shape[0], dtype=np.float64)
+        _raise(self.lib.rspr_mlp_forward(up.h, gate.h, down.h, _d(x), x.shape[0], _d(out)), "mlp_forward")
+        return out
 
     def aggregate_scores(self, tokens, sigma, vt, workers: int = 1) -> np.ndarray:
         """aggregate_scores (scores.cpp:52-62): tokens [T, n], sigma [kc], vt [kc, n] -> [kc, n]."""

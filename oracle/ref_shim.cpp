@@ -20,6 +20,7 @@
 #include "rsparse/errors.hpp"
 #include "rsparse/layer.hpp"
 #include "rsparse/matrix.hpp"
+#include "rsparse/model.hpp"
 #include "rsparse/rng.hpp"
 #include "rsparse/scores.hpp"
 #include "rsparse/search.hpp"
@@ -245,6 +246,20 @@ int rspr_decompose_with_svd(const double* w, size_t m_out, size_t m_in, double k
     std::memcpy(a_r, L.a_r.data(), m_out * rank * sizeof(double));
     std::memcpy(b_r, L.b_r.data(), rank * m_in * sizeof(double));
     for (size_t c = 0; c < rank; ++c) comps[c] = static_cast<int64_t>(L.selected_components[c]);
+  })
+}
+
+// model.cpp:115-127 (mlp_forward) over three reference layers made by
+// rspr_layer_create: x[n] -> out[n]; hidden width h = up's m_out.
+int rspr_mlp_forward(const void* up, const void* gate, const void* down, const double* x, size_t n, double* out) {
+  GUARD({
+    const auto* U = static_cast<const DecomposedLayer*>(up);
+    BlockWeights b;
+    b.w_up = Matrix(U->m_out, n);
+    const std::vector<double> y = mlp_forward(std::span<const double>(x, n), b, U,
+                                              static_cast<const DecomposedLayer*>(gate),
+                                              static_cast<const DecomposedLayer*>(down));
+    std::memcpy(out, y.data(), y.size() * sizeof(double));
   })
 }
 
