@@ -48,6 +48,12 @@ def parse():
     ap.add_argument("--no-dense", action="store_true", help="skip the dense baselines")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--cpu-layers", type=int, default=4,
+                    help="decoder layers in the cpu_baseline sample of the GPU arm (one token through them)")
+    ap.add_argument("--ref-layers", type=int, default=None,
+                    help="--impl reference: decoder layers per pass (default: all --layers)")
+    ap.add_argument("--check", action="store_true",
+                    help="after the timed loop, check a sample of the stack outputs against the oracle")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
     ap.add_argument("--force-sharded", action="store_true",
                     help="use the row-sharded + all-gather path even on one rank (exercises it on 1 GPU)")
@@ -176,49 +182,139 @@ def time_graph(torch, launch, steps, warmup, stream, barrier=None):
     return t0.elapsed_time(t1), per
 
 
-def cpu_reference_leg(wl, plans, threads, seconds=None, warmup=1, passes=None):
-    """The reference's own CPU forward (oracle/_ref = reference sources compiled
-    in place; else the C port) over one decoder layer's 7 linears per pass,
-    linears spread over `threads` host threads; extrapolated to the stack."""
+# --------------------------------------------------------------------------- reference CPU arm
+# The reference arm never imports paper_2504_19449_b200 (nor maps its .so):
+# plans come from the reference's own Recipe::plan_for (oracle/_ref), the
+# draws replicate workloads.config2_plans (same numpy generator and order).
+REF_SHAPES = [("q_proj", 4096, 4096), ("k_proj", 4096, 4096), ("v_proj", 4096, 4096),
+              ("o_proj", 4096, 4096), ("gate_proj", 11008, 4096), ("up_proj", 11008, 4096),
+              ("down_proj", 4096, 11008)]
+REF_GROUP = {"q_proj": 0, "k_proj": 0, "v_proj": 0, "o_proj": 1, "gate_proj": 2, "up_proj": 2, "down_proj": 3}
+
+
+def ref_config2_plans(R, n_layers=32, seed=2, budget=0.5):
+    """(name, m_out, m_in, s, r) per linear: rho ~ U(0.3, 0.7), C = 0.5 through
+    the reference's Recipe::plan_for (search.cpp:14-25) -- the same draws as
+    workloads.config2_plans (checked by tests/test_bench_cpu.py)."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for layer in range(n_layers):
+        for (name, m, n) in REF_SHAPES:
+            rho = float(rng.uniform(0.3, 0.7))
+            s, r = R.plan_for(rho, budget, n, m)
+            out.append((f"layers.{layer}.{name}", m, n, float(s), int(r)))
+    return out
+
+
+def host_info():
+    info = {"nproc": os.cpu_count()}
+    try:
+        info["affinity"] = len(os.sched_getaffinity(0))
+    except Exception:
+        pass
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    info["cpu_model"] = line.split(":", 1)[1].strip()
+                    break
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith(("MemTotal", "MemAvailable")):
+                    info[line.split(":")[0]] = int(line.split()[1]) * 1024
+    except Exception:
+        pass
+    return info
+
+
+def cpu_reference_leg(plans, threads, seconds=None, warmup=1, passes=None, layers=None):
+    """The reference's own CPU forward (oracle/_ref = the reference sources
+    compiled in place; else the C port) over the config-2 stack.
+
+    A pass is one decode token through ``layers`` decoder layers (default:
+    all of them).  Layers are built one at a time (fp64 weights of one layer
+    resident: ~2 GB), and every layer's 7 linears are run in decode order:
+    the linears of one input group (q/k/v, o, gate/up, down) concurrently on
+    up to ``threads`` host threads (rsparse::forward is single-threaded and
+    re-entrant), groups one after another.  Only the forward
+    calls are timed; each pass's time is the sum over its layers, so the
+    reported per-token time covers exactly the work that ran."""
     from oracle.oracle import c_oracle, ref_available, ref_oracle
-    sample = plans[:7]
-    rng = np.random.default_rng(99)
     use_ref = ref_available()
     R = ref_oracle() if use_ref else c_oracle()
-    objs, xs, ys = [], [], []
-    for (name, m, n, s, r) in sample:
-        w_cols = rng.standard_normal((n, m)) * 0.02
-        a = rng.standard_normal((m, r)) * 0.05
-        b = rng.standard_normal((r, n)) * 0.05
-        x = (wl.silu_gate_x(n, rng) if name.endswith("down_proj") else wl.heavy_tailed_x(n, rng)).astype(np.float64)
-        objs.append(R.layer(w_cols, a, b, s) if use_ref else (w_cols, a, b, s))
-        xs.append(x)
-        ys.append(np.empty(m))
+    rng = np.random.default_rng(99)
+    n_layers = len(plans) // 7 if layers is None else layers
+    rmax = max(p[4] for p in plans[: 7 * n_layers])
+    src = {}
+    for (name, m, n) in REF_SHAPES:  # fp64 sources per shape (values do not change the work)
+        if (m, n) not in src:
+            src[(m, n)] = (rng.standard_normal((n, m)) * 0.02, rng.standard_normal((m, rmax)) * 0.05,
+                           rng.standard_normal((rmax, n)) * 0.05)
+    xs = {}
+    for (name, m, n) in REF_SHAPES:
+        g = REF_GROUP[name]
+        if g not in xs:
+            x = (rng.standard_normal(n) / (1 + np.exp(-rng.standard_normal(n)))) if name == "down_proj" else \
+                rng.laplace(size=n) * rng.lognormal(size=n)
+            xs[g] = np.ascontiguousarray(x, dtype=np.float64)
+    # decoder layers stay resident across passes when host memory allows
+    # (~2 GB of fp64 per layer); otherwise each layer is rebuilt per pass
+    # (untimed) with only one layer resident at a time
+    per_layer = sum(8 * (m * n + r * (m + n)) for (_, m, n, _, r) in plans[:7])
+    avail = host_info().get("MemAvailable", 0)
+    resident = avail > 1.5 * per_layer * n_layers + (8 << 30)
+    cache = {}
 
-    def one_pass():
-        if use_ref:
-            R.forward_many(objs, xs, ys, threads)
-        else:
-            R.forward_many(objs, xs, threads)
+    def build(L):
+        objs = []
+        for (name, m, n, s, r) in plans[7 * L: 7 * L + 7]:
+            w, a, b = src[(m, n)]
+            a, b = np.ascontiguousarray(a[:, :r]), np.ascontiguousarray(b[:r])
+            objs.append(R.layer(w, a, b, s) if use_ref else (w, a, b, s))
+        return objs
 
-    for _ in range(max(warmup, 0)):
-        one_pass()
+    ys = {i: np.empty(p[1]) for i, p in enumerate(REF_SHAPES)}
     times = []
     t_end = time.perf_counter() + (seconds or 0.0)
-    while (passes is not None and len(times) < passes) or \
-            (passes is None and (time.perf_counter() < t_end or len(times) < 3)):
-        t = time.perf_counter()
-        one_pass()
-        times.append(time.perf_counter() - t)
-    layer_s = float(np.median(times))
-    scale = len(plans) / len(sample)
+    npass = 0
+    while True:
+        done = npass - max(warmup, 0)
+        if passes is not None and done >= passes:
+            break
+        if passes is None and done >= 1 and time.perf_counter() >= t_end:
+            break
+        tok = 0.0
+        for L in range(n_layers):
+            objs = cache.get(L) or build(L)
+            if resident:
+                cache[L] = objs
+            lin = plans[7 * L: 7 * L + 7]
+            for g in range(4):
+                idx = [i for i, p in enumerate(lin) if REF_GROUP[p[0].rsplit(".", 1)[1]] == g]
+                t0 = time.perf_counter()
+                if use_ref:
+                    R.forward_many([objs[i] for i in idx], [xs[g]] * len(idx), [ys[i] for i in idx],
+                                   min(threads, len(idx)))
+                else:
+                    R.forward_many([objs[i] for i in idx], [xs[g]] * len(idx), min(threads, len(idx)))
+                tok += time.perf_counter() - t0
+            del objs
+        if npass >= max(warmup, 0):
+            times.append(tok)
+        npass += 1
+    cache.clear()
+    tok_s = float(np.median(times))
+    hi = host_info()
     return {
-        "value": layer_s * 1e6 * scale, "unit": "us/token", "cores": threads,
+        "value": tok_s * 1e6, "unit": "us/token", "cores": min(threads, 3),
         "kind": "reference" if use_ref else "port",
-        "sample": (f"{'reference rsparse::forward (oracle/_ref, fp64, -O3)' if use_ref else 'C port'} over "
-                   f"decoder layer 0's 7 linears of the config-2 stack per pass, linears spread over "
-                   f"{threads} threads, median of {len(times)} passes, x{scale:g} to the {len(plans)}-linear stack"),
-        "passes": len(times), "pass_times_s": times,
+        "sample": (f"{'reference rsparse::forward (oracle/_ref, fp64, -O3)' if use_ref else 'C port (oracle)'}: "
+                   f"one decode token through {n_layers} decoder layer(s) x 7 linears of the config-2 plans "
+                   f"per pass (no extrapolation), linears of one input group concurrent on up to "
+                   f"{min(threads, 3)} threads, groups sequential; median of {len(times)} passes; "
+                   f"host {hi.get('cpu_model', '?')}, nproc {hi.get('nproc')}"),
+        "passes": len(times), "pass_times_s": times, "host": hi, "layers_timed": n_layers,
+        "resident": resident,
     }
 
 
@@ -226,20 +322,27 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    from paper_2504_19449_b200 import workloads as wl
-    plans = wl.config2_plans(n_layers=args.layers)
+    from oracle.oracle import c_oracle, ref_available, ref_oracle
+    R = ref_oracle() if ref_available() else c_oracle()
+    plans = ref_config2_plans(R, n_layers=args.layers)
     threads = os.cpu_count() or 1
-    res = cpu_reference_leg(wl, plans, threads, warmup=args.warmup, passes=args.steps)
+    t_run = time.perf_counter()
+    res = cpu_reference_leg(plans, threads, warmup=min(args.warmup, 1), passes=args.steps,
+                            layers=args.ref_layers)
+    same = args.ref_layers is None or args.ref_layers == args.layers
     line = {
         "metric": METRIC, "impl": "reference", "value": res["value"], "unit": "us/token",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": world, "steps": args.steps, "warmup": min(args.warmup, 1),
         "ms_per_step": res["value"] / 1e3, "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "config2: 32-layer Llama-2-7B-shaped R-Sparse linear stack, batch 1, "
                                "50% model-level sparsity (rho~U(0.3,0.7), C=0.5)",
-                   "global_batch": 1, "layers": args.layers, "linears": len(plans)},
+                   "global_batch": 1, "layers": args.layers if same else args.ref_layers,
+                   "linears": 7 * (args.layers if same else args.ref_layers)},
         "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": res["value"], "unit": "us/token", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "host": res["host"], "timed_seconds": sum(res["pass_times_s"]),
+        "wall_seconds": time.perf_counter() - t_run,
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -363,9 +466,16 @@ def run_ours(args):
         out["speedup_vs_dense_cublas"] = out["dense_cublas_us_per_token"] / us_token
         out["speedup_vs_dense_inhouse"] = out["dense_inhouse_us_per_token"] / us_token
     if rank == 0 and world == 1 and not args.no_cpu and not args.profile:
-        out["cpu_baseline"] = {k: v for k, v in cpu_reference_leg(wl, plans, os.cpu_count() or 1,
-                                                                  seconds=args.cpu_seconds).items()
-                               if k in ("value", "unit", "cores", "kind", "sample")}
+        cpu = cpu_reference_leg(plans, os.cpu_count() or 1, seconds=args.cpu_seconds, layers=args.cpu_layers)
+        # per-token time of the sampled layers, scaled to the stack (a
+        # reported baseline only; the reference arm times the whole stack)
+        scale = len(plans) / (7 * cpu["layers_timed"])
+        out["cpu_baseline"] = {"value": cpu["value"] * scale, "unit": "us/token", "cores": cpu["cores"],
+                               "kind": cpu["kind"],
+                               "sample": cpu["sample"] + f"; x{scale:g} from {cpu['layers_timed']} to "
+                                                         f"{len(plans) // 7} layers"}
+    if args.check and rank == 0:
+        out["check"] = check_outputs(layers, xs, ys, plans)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if sharded:
@@ -373,6 +483,28 @@ def run_ours(args):
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def check_outputs(layers, xs, ys, plans, every=16):
+    """Oracle check of the stack's last outputs (run after the timed loop, not
+    timed): for every `every`-th linear and every linear with r > 1024 the
+    selection must equal top_k_by_magnitude and y must match the reference
+    forward on the device-held values within 1e-5 (max-norm relative)."""
+    from oracle.oracle import c_oracle
+    C = c_oracle()
+    idx = sorted(set(range(0, len(layers), every)) | {i for i, p in enumerate(plans) if p[4] > 1024})
+    worst, bad = 0.0, []
+    for i in idx:
+        l = layers[i]
+        W, A, B = l.export()
+        x = xs[i].float().cpu().numpy().astype(np.float64)
+        yo, kept = C.forward(np.ascontiguousarray(W.T), A, B, plans[i][3], x, return_kept=True)
+        y = ys[i].cpu().numpy().astype(np.float64)
+        e = float(np.max(np.abs(y - yo)) / max(np.max(np.abs(yo)), 1e-300))
+        worst = max(worst, e)
+        if e > 1e-5 or not np.array_equal(l.selected(xs[i]), kept):
+            bad.append(plans[i][0])
+    return {"linears_checked": len(idx), "max_rel_err": worst, "failed": bad, "ok": not bad}
 
 
 def load_traffic():

@@ -624,6 +624,9 @@ bool batch_plan(const rsp_linear* h, int B, const DevProps& dp, BatchParams* out
     p.ks = ks;
     p.tc = cw == 8 && env_int("RSP_BATCH_TC", 0);
     p.grid = tiles * ks;
+    // CTA b < B computes token b's cut and every CTA waits for all B cuts:
+    // fewer CTAs than tokens would never publish some cuts (small n / m)
+    if (p.grid < B) continue;
     p.range_max = ((n + ks - 1) / ks + 16 + 7) / 8 * 8;  // 8-aligned rows around [wc0, wc1)
     p.slice_max = ((n + p.grid - 1) / p.grid + 16 + 7) / 8 * 8;
     p.na_max = (p.r + ks - 1) / ks + 1;
@@ -729,14 +732,17 @@ rsp_status rsp_linear_forward_host(rsp_linear* h, const void* x_host, rsp_dtype 
     RSP_CUDA(cudaMallocHost(&h->y_pin, sizeof(float) * h->m * batch));
     h->host_batch = batch;
   }
+  // the workspace of the largest path forward() may take (batch > 1 adds the
+  // batched-kernel area after the single-token one)
+  const size_t ws_bytes = rsp_linear_workspace_size(h, batch);
   if (!h->ws) {
-    RSP_CUDA(cudaMalloc(&h->ws, h->plan.ws_bytes));
-    RSP_CUDA(cudaMemsetAsync(h->ws, 0, h->plan.ws_bytes, h->stream));
+    RSP_CUDA(cudaMalloc(&h->ws, ws_bytes));
+    RSP_CUDA(cudaMemsetAsync(h->ws, 0, ws_bytes, h->stream));
   }
   const size_t xbytes = static_cast<size_t>(h->m_in) * (xdt == RSP_BF16 ? 2 : 4) * batch;
   std::memcpy(h->x_pin, x_host, xbytes);
   RSP_CUDA(cudaMemcpyAsync(h->x_dev, h->x_pin, xbytes, cudaMemcpyHostToDevice, h->stream));
-  rsp_status st = rsp_linear_forward(h, h->x_dev, xdt, h->y_dev, batch, h->ws, h->plan.ws_bytes, h->stream);
+  rsp_status st = rsp_linear_forward(h, h->x_dev, xdt, h->y_dev, batch, h->ws, ws_bytes, h->stream);
   if (st) return st;
   const size_t ycount = static_cast<size_t>(h->m) * batch;
   RSP_CUDA(cudaMemcpyAsync(h->y_pin, h->y_dev, ycount * sizeof(float), cudaMemcpyDeviceToHost, h->stream));
@@ -881,14 +887,29 @@ rsp_status rsp_split_factors(const double* u, uint32_t m, uint32_t ucols, const 
   return e == cudaSuccess ? RSP_OK : fail(RSP_E_CUDA, "split_factors: %s", cudaGetErrorString(e));
 }
 
-rsp_status rsp_top_k_by_magnitude(const void* x, rsp_dtype xdt, uint32_t n, uint32_t k,
+namespace {
+// The stand-alone selector keeps x and its histograms in one CTA's shared
+// memory: refuse (RSP_E_UNSUPPORTED) before touching CUDA when this device's
+// opt-in limit cannot hold them.
+rsp_status selector_fits(uint32_t n, bool x_bf16) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const size_t need = rsp::select_smem_bytes(static_cast<int>(n), x_bf16);
+  const int cap = device_props(dev).smem_optin;
+  if (need > static_cast<size_t>(cap))
+    return fail(RSP_E_UNSUPPORTED, "selector: n=%u needs %zu B of shared memory (device limit %d B)", n, need, cap);
+  return RSP_OK;
+}
+}  // namespace
+
+extern "C" rsp_status rsp_top_k_by_magnitude(const void* x, rsp_dtype xdt, uint32_t n, uint32_t k,
                                   int32_t* kept, int32_t* rest, void* stream) {
   if (k > n)  // matrix.cpp:101-104
     return fail(RSP_E_USAGE, "top_k_by_magnitude: k=%u exceeds vector length %u", k, n);
   if (rsp_status st = check_x_dtype(xdt)) return st;
   if (n == 0) return RSP_OK;
   if (!x) return fail(RSP_E_USAGE, "null x");
-  if (n > 48000) return fail(RSP_E_UNSUPPORTED, "selector supports n <= 48000");
+  if (rsp_status st = selector_fits(n, xdt == RSP_BF16)) return st;
   cudaError_t e = rsp::launch_select(x, xdt == RSP_BF16, static_cast<int>(n), static_cast<int>(k), kept, rest,
                                      nullptr, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(RSP_E_CUDA, "selector launch: %s", cudaGetErrorString(e));
@@ -902,7 +923,7 @@ rsp_status rsp_threshold_sparsify(const void* x, rsp_dtype xdt, uint32_t n, doub
   if (rsp_status st = check_x_dtype(xdt)) return st;
   if (k_out) *k_out = k;
   if (n == 0) return RSP_OK;
-  if (n > 48000) return fail(RSP_E_UNSUPPORTED, "selector supports n <= 48000");
+  if (rsp_status st = selector_fits(n, xdt == RSP_BF16)) return st;
   cudaError_t e = rsp::launch_select(x, xdt == RSP_BF16, static_cast<int>(n), static_cast<int>(k), kept, nullptr,
                                      sparse_x, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(RSP_E_CUDA, "selector launch: %s", cudaGetErrorString(e));

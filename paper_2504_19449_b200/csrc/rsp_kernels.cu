@@ -516,11 +516,16 @@ __device__ __forceinline__ void prep_linear(const StackParams& P, const LinDesc&
   }
   const bool det = P.deterministic != 0;
   const int KS = d.k_splits;
-  if (has_lr || (KS > 1 && !det)) {
-    if (KS > 1 && !det) {
-      const int y0 = part(d.m, b, NB), y1 = part(d.m, b + 1, NB);
-      for (int i = y0 + tid; i < y1; i += kThreads) d.y[i] = 0.f;
-    }
+  if (KS > 1 && !det) {
+    const int y0 = part(d.m, b, NB), y1 = part(d.m, b + 1, NB);
+    for (int i = y0 + tid; i < y1; i += kThreads) d.y[i] = 0.f;
+  }
+  {
+    // The next launch's t buffer of this slot is zeroed by EVERY launch that
+    // advances the epoch -- also dense / rank-0 / k_splits == 1 launches that
+    // do not accumulate into t themselves: a workspace shared by forward and
+    // dense_forward would otherwise hand stale sums to the next low-rank
+    // launch two epochs later.
     float* t_nxt = P.t_acc + (static_cast<size_t>(d.slot) * 2 + ((C.epoch + 1u) & 1u)) * kTAccCap;
     const int c0 = part(static_cast<int>(kTAccCap), b, NB), c1 = part(static_cast<int>(kTAccCap), b + 1, NB);
     for (int c = c0 + tid; c < c1; c += kThreads) t_nxt[c] = 0.f;
@@ -1151,7 +1156,10 @@ cudaError_t launch_select(const void* x, bool x_bf16, int n, int k, int32_t* kep
                                                 static_cast<int>(smem))
                          : cudaFuncSetAttribute(select_kernel<false>,
                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  if (e != cudaSuccess) return e;
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();  // clear the sticky last-error state of the failed attribute call
+    return e;
+  }
   if (x_bf16)
     select_kernel<true><<<1, kThreads, smem, stream>>>(x, n, k, kept, rest, sparse_x, 0u);
   else
