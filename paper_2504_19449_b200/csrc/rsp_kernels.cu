@@ -674,7 +674,9 @@ __device__ __forceinline__ void run_linear(const StackParams& P, const LinDesc& 
                              : stream_list<WT>(C.list_u, g1, nU, G1, ok, Bt + v1 * 16, rowB, C.pol, C.zero);
     RSP_TRACE(11);
     // the first batch of this warp's W rows flies during the t hand-off
-    if (!(P.knobs & 1024)) {
+    // (not warp 0: thread 0 releases the t barrier below, and a release waits
+    // for the thread's loads in flight -- measured -0.6% per token)
+    if (!(P.knobs & 1024) && warp != 0) {
       issue_first(wfirst, C.list_w, g2, nW, G2, ok2, Wt + static_cast<size_t>(col0) * ES + v * 16, rowW, C.pol);
       wpre = true;
     }
