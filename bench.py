@@ -52,6 +52,8 @@ def parse():
                     help="decoder layers in the cpu_baseline sample of the GPU arm (one token through them)")
     ap.add_argument("--ref-layers", type=int, default=None,
                     help="--impl reference: decoder layers per pass (default: all --layers)")
+    ap.add_argument("--deterministic", action="store_true",
+                    help="fixed-order (bit-reproducible) combines instead of float reductions at L2")
     ap.add_argument("--check", action="store_true",
                     help="after the timed loop, check a sample of the stack outputs against the oracle")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
@@ -127,7 +129,7 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------- workload
-def build_stack(rsp, wl, plans, rank, world, dev, torch):
+def build_stack(rsp, wl, plans, rank, world, dev, torch, deterministic=False):
     """Create every linear's shard on the device from synthetic weights, and
     one synthetic activation per input group (q/k/v share one, gate/up share
     one: workloads.input_groups)."""
@@ -141,7 +143,8 @@ def build_stack(rsp, wl, plans, rank, world, dev, torch):
         a = torch.randn(m, r, device=dev, dtype=torch.bfloat16, generator=gen) * 0.05
         b = torch.randn(r, n, device=dev, dtype=torch.bfloat16, generator=gen) * 0.05
         layers.append(rsp.DecomposedLayer(w, a, b, rsp.SparsityPlan(s, r), weight_dtype="bf16",
-                                          device=dev.index, shard_rank=rank, shard_count=world))
+                                          device=dev.index, shard_rank=rank, shard_count=world,
+                                          deterministic=deterministic))
         del w, a, b
         if wait[i]:
             xs_host.append(wl.silu_gate_x(n, rng) if name.endswith("down_proj") else wl.heavy_tailed_x(n, rng))
@@ -365,7 +368,7 @@ def run_ours(args):
     rsp.lib()
 
     plans = wl.config2_plans(n_layers=args.layers)
-    layers, xs_host, gid, wait = build_stack(rsp, wl, plans, rank, world, dev, torch)
+    layers, xs_host, gid, wait = build_stack(rsp, wl, plans, rank, world, dev, torch, args.deterministic)
 
     # activations: one contiguous bf16 buffer (device + pinned host) for the e2e copy
     offs = np.cumsum([0] + [x.size for x in xs_host])
@@ -392,9 +395,10 @@ def run_ours(args):
         # of y (paper_2504_19449_b200/sharding.py), captured as one graph
         from paper_2504_19449_b200.sharding import ShardedGroupStack, ShardedStack, even_shards
         if all(even_shards(l.m_out, world) for l in layers) and not os.environ.get("RSP_PER_LINEAR_SHARDS"):
-            st = ShardedGroupStack(layers, xs, ys, gid, stream=stream)  # one stack launch per input group
+            st = ShardedGroupStack(layers, xs, ys, gid, stream=stream,  # one stack launch per input group
+                                   force_gather=args.force_sharded)
         else:
-            st = ShardedStack(layers, xs, ys, stream=stream)
+            st = ShardedStack(layers, xs, ys, stream=stream, force_gather=args.force_sharded)
         launch = st.launch
 
     def barrier():
@@ -448,6 +452,7 @@ def run_ours(args):
                                "q/k/v and gate/up share one input (decoder-layer dataflow)",
                    "global_batch": 1, "layers": args.layers, "linears": len(layers),
                    "parallelism": f"row-shard{world}" + ("+allgather" if sharded else ""),
+                   "combine": "deterministic (fixed-order partials)" if args.deterministic else "float reductions at L2",
                    "sharded_graph": (getattr(st, "graph", None) is not None) if sharded else None,
                    "l2": "no flush: 16 GB resident operands >> 126 MB L2",
                    "step_ms_p10_p50_p90": [float(np.percentile(per, q)) for q in (10, 50, 90)]},

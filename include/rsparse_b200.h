@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define RSP_ABI_VERSION 1
+#define RSP_ABI_VERSION 2
 
 typedef enum rsp_status {
   RSP_OK = 0,
@@ -80,6 +80,16 @@ typedef struct rsp_linear_desc {
 #define RSP_FLAG_DETERMINISTIC 1u /* combine split-K partials of y in a fixed order
                                      (bit-reproducible, ~1 us slower per forward);
                                      default: float atomics into y */
+#define RSP_FLAG_BATCH_TCGEN05 2u /* batch 2..16: the W / stage-2 products on tcgen05
+                                     with TMEM accumulators instead of warp-level
+                                     mma.sync (measured slower at B <= 16; default off) */
+
+/* rsp_linear_info.path: which kernels forward() runs (fixed at create). */
+#define RSP_PATH_PERSISTENT 1u     /* batch 1: the persistent fused kernel (selection,
+                                      gathered rows, low-rank stages in one launch) */
+#define RSP_PATH_BATCH_MMA 2u      /* batch 2..16 (bf16 W and x): union-of-masks pass, mma.sync */
+#define RSP_PATH_BATCH_TCGEN05 4u  /* batch 2..16: the same pass on tcgen05 / TMEM */
+#define RSP_PATH_DETERMINISTIC 8u  /* fixed-order combines (batch > 1 runs per token) */
 
 typedef struct rsp_linear_info {
   uint32_t m_in, m_out, rank, k;
@@ -89,6 +99,7 @@ typedef struct rsp_linear_info {
   uint32_t smem_bytes;
   rsp_dtype weight_dtype;
   uint64_t device_bytes;       /* weights + factors resident in HBM */
+  uint32_t path;               /* RSP_PATH_* bits: the kernels forward() uses */
 } rsp_linear_info;
 
 /* io_cost (layer.cpp:125-140) plus the bytes the B200 kernel actually moves. */
@@ -243,6 +254,16 @@ rsp_status rsp_stack_create_ex(const rsp_linear* const* layers, uint32_t count,
                                const void* const* x_devs, rsp_dtype x_dtype, float* const* y_devs,
                                int dense, const uint8_t* wait_prev, rsp_stack** out);
 rsp_status rsp_stack_launch(rsp_stack* s, void* stream);
+/* The end-to-end stack path with host buffers: x_host (x_bytes) is copied to
+ * the span of device memory covering all the stack's inputs (the x_devs given
+ * at creation must lie in one contiguous allocation; x_bytes must equal that
+ * span), the stack runs, and the span covering all outputs (y_bytes) is
+ * copied to y_host; returns after the stream has synchronised.  Pinned host
+ * buffers make both copies asynchronous DMA.  rsp_stack_io_spans reports the
+ * two spans. */
+rsp_status rsp_stack_io_spans(const rsp_stack* s, size_t* x_bytes, size_t* y_bytes);
+rsp_status rsp_stack_launch_host(rsp_stack* s, const void* x_host, size_t x_bytes, void* y_host,
+                                 size_t y_bytes, void* stream);
 void rsp_stack_destroy(rsp_stack* s);
 
 /* -- diagnostics ---------------------------------------------------------------- */
@@ -258,8 +279,10 @@ rsp_status rsp_debug_forward_trace(const rsp_linear* h, const void* x_dev, rsp_d
  * [13] after its dependency wait, [14] at its end, [1..12] %clock64 phase
  * stamps relative to the CTA's start of the linear.  *grid_out = grid. */
 rsp_status rsp_debug_stack_trace(rsp_stack* s, int64_t* trace_dev, uint32_t* grid_out, void* stream);
-/* Debug: per-CTA phase clocks of the last batched forward run with the
- * environment variable RSP_BATCH_TRACE=1: host[cta * 16 + phase] (clock64
+/* Debug: record per-CTA phase clocks in subsequent batched forwards (on != 0). */
+rsp_status rsp_debug_set_batch_trace(int on);
+/* Debug: per-CTA phase clocks of the last batched forward run with
+ * rsp_debug_set_batch_trace(1): host[cta * 16 + phase] (clock64
  * since the CTA started; phases 1 staging, 2 lists, 3 stage 1, 4 arrive,
  * 5 W rows, 6 t barrier, 7 stage 2, 8 combine). */
 rsp_status rsp_debug_batch_trace(int64_t* host, uint32_t ctas);

@@ -24,7 +24,8 @@ EXPORTS = [
     "rsp_linear_selected", "rsp_linear_io_cost", "rsp_linear_export",
     "rsp_top_k_by_magnitude", "rsp_threshold_sparsify", "rsp_stack_create", "rsp_stack_create_ex",
     "rsp_stack_launch", "rsp_stack_destroy", "rsp_device_sm_count", "rsp_debug_forward_trace",
-    "rsp_debug_stack_trace", "rsp_debug_batch_trace", "rsp_rspl_read", "rsp_linear_load_rspl", "rsp_linear_save_rspl", "rsp_linear_components",
+    "rsp_debug_stack_trace", "rsp_debug_batch_trace", "rsp_debug_set_batch_trace", "rsp_stack_io_spans",
+    "rsp_stack_launch_host", "rsp_rspl_read", "rsp_linear_load_rspl", "rsp_linear_save_rspl", "rsp_linear_components",
     "rsp_aggregate_scores", "rsp_select_components", "rsp_split_factors", "rsp_linear_set_components",
 ]
 
@@ -41,6 +42,8 @@ class LinearDesc(ct.Structure):
 
 
 RSP_FLAG_DETERMINISTIC = 1
+RSP_FLAG_BATCH_TCGEN05 = 2
+RSP_PATH_PERSISTENT, RSP_PATH_BATCH_MMA, RSP_PATH_BATCH_TCGEN05, RSP_PATH_DETERMINISTIC = 1, 2, 4, 8
 
 
 class LinearInfo(ct.Structure):
@@ -49,7 +52,7 @@ class LinearInfo(ct.Structure):
         ("row_begin", ct.c_uint32), ("row_end", ct.c_uint32), ("m_pad", ct.c_uint32),
         ("r_pad", ct.c_uint32), ("col_tiles", ct.c_uint32), ("k_splits", ct.c_uint32),
         ("grid", ct.c_uint32), ("smem_bytes", ct.c_uint32), ("weight_dtype", ct.c_int),
-        ("device_bytes", ct.c_uint64),
+        ("device_bytes", ct.c_uint64), ("path", ct.c_uint32),
     ]
 
 
@@ -136,6 +139,9 @@ def lib() -> ct.CDLL:
         "rsp_debug_forward_trace": (ct.c_int, [vp, vp, ct.c_int, vp, vp, ct.c_size_t, vp, ct.c_int, vp]),
         "rsp_debug_stack_trace": (ct.c_int, [vp, vp, ct.POINTER(u32), vp]),
         "rsp_debug_batch_trace": (ct.c_int, [vp, u32]),
+        "rsp_debug_set_batch_trace": (ct.c_int, [ct.c_int]),
+        "rsp_stack_io_spans": (ct.c_int, [vp, ct.POINTER(ct.c_size_t), ct.POINTER(ct.c_size_t)]),
+        "rsp_stack_launch_host": (ct.c_int, [vp, vp, ct.c_size_t, vp, ct.c_size_t, vp]),
         "rsp_rspl_read": (ct.c_int, [ct.c_char_p, ct.POINTER(RsplHeader), vp, vp, vp, vp]),
         "rsp_linear_load_rspl": (ct.c_int, [ct.c_char_p, ct.POINTER(LinearDesc), ct.POINTER(vp)]),
         "rsp_linear_save_rspl": (ct.c_int, [vp, ct.c_char_p]),

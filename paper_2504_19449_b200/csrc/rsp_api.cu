@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -80,27 +81,14 @@ DevProps device_props(int dev) {
   return cache[dev];
 }
 
-bool env_flag(const char* name, bool dflt) {
-  const char* v = std::getenv(name);
-  if (!v || !*v) return dflt;
-  return !(v[0] == '0' || v[0] == 'n' || v[0] == 'N' || v[0] == 'f' || v[0] == 'F');
-}
-
-double env_double(const char* name, double dflt) {
-  const char* v = std::getenv(name);
-  return v && *v ? std::atof(v) : dflt;
-}
-
-int env_int(const char* name, int dflt) {
-  const char* v = std::getenv(name);
-  return (v && *v) ? std::atoi(v) : dflt;
-}
-
 size_t dtype_size(rsp_dtype d) { return d == RSP_F64 ? 8 : (d == RSP_F32 ? 4 : 2); }
 
 uint32_t round_up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
 
 constexpr int kMaxN = 32768;  // selection keeps x in shared memory
+constexpr int kMaxKSplits = 40;  // channel splits per column tile (o / down use all 148 SMs)
+
+std::atomic<int> g_batch_trace{0};  // rsp_debug_set_batch_trace
 
 // k = ceil(s * n) in double (sparsity.cpp:26-27).
 uint32_t keep_count(double s, uint32_t n) {
@@ -112,8 +100,6 @@ struct LaunchPlan {
   int col_tiles = 1, k_splits = 1, grid = 1;
   int cap_w = 1, cap_u = 1, cap_a = 1;
   int nb_pad = 4;
-  int need_a = 0, need_b = 0;    // bytes of one CTA's A_r^T tile rows / B_r^T slice
-  int abuf = 0, bbuf = 0;        // shared-memory operand buffers of a single-linear launch
   size_t smem = 0;
   size_t ws_bytes = 0;  // single-linear workspace
 };
@@ -133,6 +119,7 @@ struct rsp_linear {
   LaunchPlan plan;
   bool pdl = true;
   bool deterministic = false;  // RSP_FLAG_DETERMINISTIC: fixed-order split-K combine
+  bool batch_tc = false;       // RSP_FLAG_BATCH_TCGEN05: batched products on tcgen05 (TMEM accumulators)
   // forward_host staging (lazily created)
   cudaStream_t stream = nullptr;
   void* x_dev = nullptr;
@@ -156,32 +143,20 @@ struct rsp_stack {
   int es = 2, grid = 1;
   bool x_bf16 = false;
   size_t smem = 0;
+  // contiguous device spans covering every x / y of the stack (host-buffer path)
+  uint8_t* x_lo = nullptr;
+  uint8_t* y_lo = nullptr;
+  size_t x_span = 0, y_span = 0;
 };
 
 namespace {
-
-// Split the shared memory left over by the kernel's fixed carve-up between
-// the operand buffers: the B_r^T slice is used all-or-nothing (it precedes
-// the grid barrier), the A_r^T tile takes what remains.  Opt-in (env
-// RSP_SMEM_OPS=1): measured on the config-2 stack it speeds up stage 1 and
-// stage 2 but the bulk copies compete with the critical W stream, and the
-// stack is 3-4% faster without them.
-void operand_buffers(int avail, int need_a, int need_b, int* abuf, int* bbuf) {
-  // one buffer (abuf) holds a linear's B_r^T slice then its A_r^T rows; the
-  // kernel splits it per linear (operand_split)
-  avail = std::max(0, avail - 1024);
-  *abuf = *bbuf = 0;
-  if (!env_int("RSP_SMEM_OPS", 0)) return;
-  const int cap = env_int("RSP_OBUF_KB", 0) > 0 ? env_int("RSP_OBUF_KB", 0) * 1024 : avail;
-  *abuf = std::min(std::min(need_a + need_b + 16, avail), cap) / 16 * 16;
-}
 
 // Decompose one forward over the GPU: col_tiles column tiles x k_splits
 // channel splits, at most one CTA per SM (a second slot per SM is left for
 // the next linear's CTAs under PDL).  A column tile is C2 whole 512-byte warp
 // columns of a row (C2 in {1,2,4,8,16}); per-CTA time ~ k*C2/(16*k_splits),
 // and the split-K combine costs k_splits*m float reductions, so the cheapest
-// C2/k_splits wins with k_splits <= 40 (RSP_MAX_KSPLITS).
+// C2/k_splits wins with k_splits <= kMaxKSplits.
 rsp_status make_plan(const rsp_linear& L, const DevProps& dp, LaunchPlan* out, int budget = 0) {
   LaunchPlan p;
   const uint32_t n = L.m_in;
@@ -191,12 +166,12 @@ rsp_status make_plan(const rsp_linear& L, const DevProps& dp, LaunchPlan* out, i
     return fail(RSP_E_UNSUPPORTED, "rank %u too large (B_r^T rows limited to 4 KB, r_pad <= %u)", L.rank,
                 rsp::kTAccCap);
   const int sms = std::max(1, budget > 0 ? std::min(budget, dp.sms) : dp.sms);  // CTAs this linear may use
-  const int ks_cap = std::max(1, env_int("RSP_MAX_KSPLITS", 40));
+  const int ks_cap = kMaxKSplits;
   int best_nt = 1, best_ks = 1;
   double best = 1e30;
   // with a low-rank term, prefer tiles of at most 4 warp columns: that leaves
   // room for a stage-1 warp group beside the W warps (warp-specialised path)
-  const int c2_pref = (L.rank > 0 && L.k < n) ? env_int("RSP_C2PREF", 4) : 8;
+  const int c2_pref = (L.rank > 0 && L.k < n) ? 4 : 8;
   for (int c2 = 1; c2 <= 8; c2 *= 2) {  // <= one row of warps (kThreads / 32 = 8)
     const int nt = (wcols + c2 - 1) / c2;
     if (nt > sms || nt > static_cast<int>(rsp::kMaxTickets)) continue;
@@ -217,7 +192,6 @@ rsp_status make_plan(const rsp_linear& L, const DevProps& dp, LaunchPlan* out, i
   const int want = std::max(1, static_cast<int>(std::ceil(bytes / 32768.0)));
   ks = std::min(ks, std::max(1, (want + nt - 1) / nt));
   ks = std::min(ks, static_cast<int>(std::max(1u, n)));
-  if (const int force = env_int("RSP_KSPLITS", 0)) ks = std::max(1, std::min(force, sms / nt));
   ks = std::max(1, std::min(ks, sms / nt));
   p.col_tiles = nt;
   p.k_splits = ks;
@@ -226,17 +200,9 @@ rsp_status make_plan(const rsp_linear& L, const DevProps& dp, LaunchPlan* out, i
   p.cap_w = static_cast<int>((n + ks - 1) / ks) + 1;          // W channel range of one CTA
   p.cap_u = static_cast<int>((n + p.grid - 1) / p.grid) + 1;  // stage-1 channel range of one CTA
   p.cap_a = static_cast<int>((L.rank + ks - 1) / ks) + 1;     // A_r^T rows of one CTA
-  {
-    const int wmax = 32 * ((wcols + nt - 1) / nt);  // widest tile, 16-B units
-    const bool lr = L.rank > 0 && L.k < n;
-    p.need_a = lr ? p.cap_a * std::min(wmax, vrow) * 16 : 0;
-    p.need_b = lr ? (p.cap_u - 1) * static_cast<int>(L.r_pad * L.es) : 0;
-  }
-  const size_t base = rsp::stack_smem_bytes(static_cast<int>(n), false, p.cap_w, p.cap_u, p.cap_a);  // fp32 x
-  if (base > static_cast<size_t>(dp.smem_optin))
-    return fail(RSP_E_UNSUPPORTED, "fused kernel needs %zu B shared memory (> %d)", base, dp.smem_optin);
-  operand_buffers(static_cast<int>(dp.smem_optin - base), p.need_a, p.need_b, &p.abuf, &p.bbuf);
-  p.smem = rsp::stack_smem_bytes(static_cast<int>(n), false, p.cap_w, p.cap_u, p.cap_a, p.abuf, p.bbuf);
+  p.smem = rsp::stack_smem_bytes(static_cast<int>(n), false, p.cap_w, p.cap_u, p.cap_a);  // fp32 x: the larger
+  if (p.smem > static_cast<size_t>(dp.smem_optin))
+    return fail(RSP_E_UNSUPPORTED, "fused kernel needs %zu B shared memory (> %d)", p.smem, dp.smem_optin);
   p.ws_bytes = WsLayout::make(1, p.nb_pad, static_cast<int>(L.r_pad), ks, static_cast<int>(L.m_pad)).bytes;
   *out = p;
   return RSP_OK;
@@ -362,11 +328,9 @@ rsp_status launch_forward(const rsp_linear* h, const void* x, rsp_dtype xdt, flo
   p.cap_w = h->plan.cap_w;
   p.cap_u = h->plan.cap_u;
   p.cap_a = h->plan.cap_a;
-  p.abuf_bytes = h->plan.abuf;
-  p.bbuf_bytes = h->plan.bbuf;
   p.nb_pad = h->plan.nb_pad;
   p.deterministic = h->deterministic ? 1 : 0;
-  p.knobs = env_int("RSP_KNOBS", 0);
+  p.zero = 0u;
   p.trace = trace;
   bind_workspace(&p, ws, WsLayout::make(1, h->plan.nb_pad, static_cast<int>(h->r_pad), h->plan.k_splits,
                                          static_cast<int>(h->m_pad)));
@@ -523,8 +487,9 @@ rsp_status rsp_linear_create(const rsp_linear_desc* d, rsp_linear** out) {
   h->r_pad = d->rank ? round_up(d->rank, 8) : 0;
   h->wdt = d->weight_dtype;
   h->es = d->weight_dtype == RSP_F32 ? 4 : 2;
-  h->pdl = env_flag("RSP_PDL", true);
-  h->deterministic = (d->flags & RSP_FLAG_DETERMINISTIC) != 0 || env_flag("RSP_DETERMINISTIC", false);
+  h->pdl = true;
+  h->deterministic = (d->flags & RSP_FLAG_DETERMINISTIC) != 0;
+  h->batch_tc = (d->flags & RSP_FLAG_BATCH_TCGEN05) != 0;
   const DevProps dp = device_props(d->device);
   if (dp.sms == 0) {
     delete h;
@@ -586,6 +551,8 @@ rsp_status rsp_linear_info_get(const rsp_linear* h, rsp_linear_info* o) {
   o->weight_dtype = h->wdt;
   o->device_bytes = (static_cast<uint64_t>(h->m_in) * h->m_pad + static_cast<uint64_t>(h->rank) * h->m_pad +
                      static_cast<uint64_t>(h->m_in) * h->r_pad) * h->es;
+  o->path = RSP_PATH_PERSISTENT | (h->deterministic ? RSP_PATH_DETERMINISTIC : 0u) |
+            (h->deterministic || h->es != 2 ? 0u : (h->batch_tc ? RSP_PATH_BATCH_TCGEN05 : RSP_PATH_BATCH_MMA));
   return RSP_OK;
 }
 
@@ -622,7 +589,7 @@ bool batch_plan(const rsp_linear* h, int B, const DevProps& dp, BatchParams* out
     p.B = B;
     p.cw = cw;
     p.ks = ks;
-    p.tc = cw == 8 && env_int("RSP_BATCH_TC", 0);
+    p.tc = cw == 8 && h->batch_tc;
     p.grid = tiles * ks;
     // CTA b < B computes token b's cut and every CTA waits for all B cuts:
     // fewer CTAs than tokens would never publish some cuts (small n / m)
@@ -653,7 +620,7 @@ rsp_status rsp_linear_forward(const rsp_linear* h, const void* x, rsp_dtype xdt,
   // tokens' selected rows on the tensor cores (rsp_batch.cu)
   BatchParams bp;
   if (batch > 1 && batch <= static_cast<uint32_t>(rsp::kBatchMax) && h->es == 2 && xdt == RSP_BF16 &&
-      !h->deterministic && !env_int("RSP_BATCH_LOOP", 0) &&
+      !h->deterministic &&
       batch_plan(h, static_cast<int>(batch), device_props(h->device), &bp)) {
     if (!ws || ws_bytes < rsp_linear_workspace_size(h, batch))
       return fail(RSP_E_USAGE, "workspace of %zu bytes is smaller than the %zu required", ws_bytes,
@@ -667,11 +634,11 @@ rsp_status rsp_linear_forward(const rsp_linear* h, const void* x, rsp_dtype xdt,
     bp.ctr = reinterpret_cast<unsigned*>(area);
     bp.cuts = reinterpret_cast<int2*>(area + 256);
     bp.t_acc = reinterpret_cast<float*>(area + 512);
-    bp.trace = env_int("RSP_BATCH_TRACE", 0);
+    bp.trace = g_batch_trace.load() ? 1 : 0;
     const cudaStream_t cs = static_cast<cudaStream_t>(stream);
     const bool has_lr = bp.r > 0 && bp.k < bp.n;
     bp.zero_y = bp.ks > 1 && has_lr;  // zeroed inside, ahead of the t barrier
-    bp.pdl = env_int("RSP_BATCH_PDL", 1);
+    bp.pdl = 1;
     bp.zero = 0u;
     if (bp.ks > 1 && !has_lr) RSP_CUDA(cudaMemsetAsync(y, 0, sizeof(float) * h->m * batch, cs));
     cudaError_t e = rsp::launch_batch(bp, true, cs);
@@ -684,6 +651,11 @@ rsp_status rsp_linear_forward(const rsp_linear* h, const void* x, rsp_dtype xdt,
                                    ws, ws_bytes, static_cast<cudaStream_t>(stream), false);
     if (st) return st;
   }
+  return RSP_OK;
+}
+
+extern "C" rsp_status rsp_debug_set_batch_trace(int on) {
+  g_batch_trace.store(on ? 1 : 0);
   return RSP_OK;
 }
 
@@ -1044,10 +1016,9 @@ rsp_status rsp_stack_create_ex(const rsp_linear* const* layers, uint32_t count, 
       const bool lr = !dense && h->rank > 0 && kk < h->m_in;
       // stage-1 rows stream at roughly half the W rate (short gathered rows,
       // few in flight), so they weigh more in the CTA split of a group
-      const double bw = env_double("RSP_BWEIGHT", 1.0);
       bytes[i - g0] = static_cast<double>(h->es) *
                       (static_cast<double>(kk) * h->m_pad +
-                       (lr ? bw * static_cast<double>(h->m_in - kk) * h->r_pad + static_cast<double>(h->rank) * h->m_pad
+                       (lr ? static_cast<double>(h->m_in - kk) * h->r_pad + static_cast<double>(h->rank) * h->m_pad
                            : 0.0));
       tot += bytes[i - g0];
     }
@@ -1072,11 +1043,8 @@ rsp_status rsp_stack_create_ex(const rsp_linear* const* layers, uint32_t count, 
     pg1 = g1;
     g0 = g1;
   }
-  int need_a = 0, need_b = 0;
   for (uint32_t i = 0; i < count; ++i) {
     const rsp_linear* h = layers[i];
-    need_a = std::max(need_a, plans[i].need_a);
-    need_b = std::max(need_b, plans[i].need_b);
     n_max = std::max(n_max, static_cast<int>(h->m_in));
     cap_w = std::max(cap_w, plans[i].cap_w);
     cap_u = std::max(cap_u, plans[i].cap_u);
@@ -1086,16 +1054,28 @@ rsp_status rsp_stack_create_ex(const rsp_linear* const* layers, uint32_t count, 
     ks_max = std::max(ks_max, plans[i].k_splits);
     m_pad_max = std::max(m_pad_max, static_cast<int>(h->m_pad));
   }
-  smem = rsp::stack_smem_bytes(n_max, xdt == RSP_BF16, cap_w, cap_u, cap_a, 0, 0, static_cast<int>(count));
+  smem = rsp::stack_smem_bytes(n_max, xdt == RSP_BF16, cap_w, cap_u, cap_a, static_cast<int>(count));
   const DevProps& dp = dpx;
   if (smem > static_cast<size_t>(dp.smem_optin))
     return fail(RSP_E_UNSUPPORTED, "stack needs %zu B shared memory (> %d)", smem, dp.smem_optin);
-  int abuf = 0, bbuf = 0;
-  operand_buffers(static_cast<int>(dp.smem_optin - smem), need_a, need_b, &abuf, &bbuf);
-  smem = rsp::stack_smem_bytes(n_max, xdt == RSP_BF16, cap_w, cap_u, cap_a, abuf, bbuf, static_cast<int>(count));
   const WsLayout wl = WsLayout::make(static_cast<int>(count), nb_pad, r_pad_max, ks_max, m_pad_max);
   auto* s = new rsp_stack();
   s->device = dev;
+  {
+    const size_t xe = xdt == RSP_BF16 ? 2 : 4;
+    uintptr_t xl = UINTPTR_MAX, xh = 0, yl = UINTPTR_MAX, yh = 0;
+    for (uint32_t i = 0; i < count; ++i) {
+      const uintptr_t xa = reinterpret_cast<uintptr_t>(x_devs[i]), ya = reinterpret_cast<uintptr_t>(y_devs[i]);
+      xl = std::min(xl, xa);
+      xh = std::max(xh, xa + xe * layers[i]->m_in);
+      yl = std::min(yl, ya);
+      yh = std::max(yh, ya + sizeof(float) * layers[i]->m);
+    }
+    s->x_lo = reinterpret_cast<uint8_t*>(xl);
+    s->y_lo = reinterpret_cast<uint8_t*>(yl);
+    s->x_span = xh - xl;
+    s->y_span = yh - yl;
+  }
   cudaStream_t cs = nullptr;
   cudaError_t e = cudaMalloc(&s->ws, wl.bytes);
   if (e == cudaSuccess) e = cudaMemset(s->ws, 0, wl.bytes);
@@ -1103,20 +1083,18 @@ rsp_status rsp_stack_create_ex(const rsp_linear* const* layers, uint32_t count, 
   if (e == cudaSuccess) e = cudaMemcpy(s->descs, descs.data(), sizeof(LinDesc) * count, cudaMemcpyHostToDevice);
   // Completion arrivals go to one counter per group (the slot of its first
   // linear): a dependent group polls one counter, not one per linear (each
-  // poll is an L2 round trip).  RSP_KNOBS & 65536: one counter per linear.
-  const int knobs = env_int("RSP_KNOBS", 0);
+  // poll is an L2 round trip).
   std::vector<rsp::LinCtl> ctl(count);
   for (uint32_t i = 0; i < count; ++i)
     ctl[i] = rsp::LinCtl{descs[i].flags, descs[i].dep0, descs[i].ndep, descs[i].cta0, descs[i].grid, descs[i].slot,
-                         (knobs & 65536) ? descs[i].slot : descs[gstart[i]].slot, 0};
+                         descs[gstart[i]].slot, 0};
   if (e == cudaSuccess) e = cudaMalloc(&s->ctl, sizeof(rsp::LinCtl) * count);
   if (e == cudaSuccess) e = cudaMemcpy(s->ctl, ctl.data(), sizeof(rsp::LinCtl) * count, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaMalloc(&s->plans, static_cast<size_t>(count) * grid * rsp::kPlanBytes);
   if (e == cudaSuccess)
-    e = rsp::launch_plans(s->descs, static_cast<int>(count), grid, knobs, abuf,
-                          rsp::stack_acopy_bytes(n_max, xdt == RSP_BF16, cap_w, cap_u, cap_a, abuf, bbuf,
-                                                 static_cast<int>(count)),
+    e = rsp::launch_plans(s->descs, static_cast<int>(count), grid,
+                          rsp::stack_acopy_bytes(n_max, xdt == RSP_BF16, cap_w, cap_u, cap_a, static_cast<int>(count)),
                           h0->es, s->plans, cs);
   if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
   if (e == cudaSuccess) e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
@@ -1129,11 +1107,9 @@ rsp_status rsp_stack_create_ex(const rsp_linear* const* layers, uint32_t count, 
     p.cap_w = cap_w;
     p.cap_u = cap_u;
     p.cap_a = cap_a;
-    p.abuf_bytes = abuf;
-    p.bbuf_bytes = bbuf;
     p.nb_pad = nb_pad;
     p.deterministic = det ? 1 : 0;
-    p.knobs = knobs;
+    p.zero = 0u;
     p.plans = s->plans;
     p.ctl = s->ctl;
     bind_workspace(&p, s->ws, wl);
@@ -1167,6 +1143,28 @@ rsp_status rsp_stack_launch(rsp_stack* s, void* stream) {
   if (!s) return fail(RSP_E_USAGE, "null stack");
   DeviceGuard g(s->device);
   RSP_CUDA(cudaGraphLaunch(s->exec, static_cast<cudaStream_t>(stream)));
+  return RSP_OK;
+}
+
+rsp_status rsp_stack_io_spans(const rsp_stack* s, size_t* x_bytes, size_t* y_bytes) {
+  if (!s) return fail(RSP_E_USAGE, "null stack");
+  if (x_bytes) *x_bytes = s->x_span;
+  if (y_bytes) *y_bytes = s->y_span;
+  return RSP_OK;
+}
+
+rsp_status rsp_stack_launch_host(rsp_stack* s, const void* x_host, size_t x_bytes, void* y_host, size_t y_bytes,
+                                 void* stream) {
+  if (!s || !x_host || !y_host) return fail(RSP_E_USAGE, "null stack or buffer");
+  if (x_bytes != s->x_span || y_bytes != s->y_span)
+    return fail(RSP_E_USAGE, "host buffers of %zu / %zu bytes do not match the stack's x / y spans (%zu / %zu)",
+                x_bytes, y_bytes, s->x_span, s->y_span);
+  DeviceGuard g(s->device);
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  RSP_CUDA(cudaMemcpyAsync(s->x_lo, x_host, x_bytes, cudaMemcpyHostToDevice, cs));
+  RSP_CUDA(cudaGraphLaunch(s->exec, cs));
+  RSP_CUDA(cudaMemcpyAsync(y_host, s->y_lo, y_bytes, cudaMemcpyDeviceToHost, cs));
+  RSP_CUDA(cudaStreamSynchronize(cs));
   return RSP_OK;
 }
 

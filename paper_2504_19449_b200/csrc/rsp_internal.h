@@ -48,7 +48,6 @@ struct StackParams {
   LinDesc one;
   int count;
   int n_max, cap_w, cap_u, cap_a;  // shared-memory carve-up (maxima over the linears)
-  int abuf_bytes, bbuf_bytes;      // shared-memory operand buffers (A_r^T tile rows, B_r^T slice)
   unsigned* hdr;                   // workspace header
   unsigned* slots;                 // [slots][kSlotWords]
   float* t_acc;                    // [slots][2][kTAccCap] stage-1 sums (parity = launch epoch & 1)
@@ -57,7 +56,7 @@ struct StackParams {
   int nb_pad;                      // row stride of t_part
   int deterministic;               // 1: fixed-order combines (bit-reproducible y); linears serialised
   int pdl;                         // 1: launched with programmatic dependent launch
-  int knobs;                       // experiment switches (env RSP_KNOBS): 1 no W prefetch, 2 no A/B prefetch
+  unsigned zero;                   // always 0: a value the compiler cannot fold (load batching in stream_list)
   long long* trace;                // debug: [grid][16] phase timestamps of the last linear (null in production)
   const void* plans;               // [count][grid] per-CTA plans (plan_kernel), or null: computed in the kernel
   const LinCtl* ctl;               // [count] control table, or null (single linear: built from `one`)
@@ -79,18 +78,15 @@ struct WsLayout {
   }
 };
 
-// Shared-memory bytes of the stack kernel for these maxima (without / with
-// the operand buffers).
-size_t stack_smem_bytes(int n_max, bool x_bf16, int cap_w, int cap_u, int cap_a, int abuf_bytes = 0,
-                        int bbuf_bytes = 0, int count = 1);
+// Shared-memory bytes of the stack kernel for these maxima.
+size_t stack_smem_bytes(int n_max, bool x_bf16, int cap_w, int cap_u, int cap_a, int count = 1);
 
 cudaError_t stack_set_smem(size_t smem);
 // Fill a stack's plan table (count x grid entries of kPlanBytes) from its device descriptors.
-cudaError_t launch_plans(const LinDesc* descs, int count, int grid, int knobs, int obuf_bytes, int acap,
-                         int elem_bytes, void* out, cudaStream_t stream);
+cudaError_t launch_plans(const LinDesc* descs, int count, int grid, int acap, int elem_bytes, void* out,
+                         cudaStream_t stream);
 // Bytes of the stack kernel's dead x + histogram area (A_r^T row copies).
-int stack_acopy_bytes(int n_max, bool x_bf16, int cap_w, int cap_u, int cap_a, int abuf_bytes, int bbuf_bytes,
-                      int count);
+int stack_acopy_bytes(int n_max, bool x_bf16, int cap_w, int cap_u, int cap_a, int count);
 cudaError_t launch_stack(const StackParams& p, int elem_bytes, bool x_bf16, int grid, size_t smem,
                          cudaStream_t stream, bool pdl);
 

@@ -105,7 +105,7 @@ class DecomposedLayer:
                  keep_fraction: Optional[float] = None, rank: Optional[int] = None,
                  weight_dtype: str = "bf16", w_layout: str = "row", k: Optional[int] = None,
                  device: int = 0, shard_rank: int = 0, shard_count: int = 1,
-                 deterministic: bool = False):
+                 deterministic: bool = False, batch_tcgen05: bool = False):
         if plan is None:
             plan = SparsityPlan(1.0 if keep_fraction is None else keep_fraction,
                                 0 if rank is None else rank)
@@ -141,7 +141,8 @@ class DecomposedLayer:
         d.w_layout = L.RSP_W_ROW_MAJOR if w_layout == "row" else L.RSP_W_COL_MAJOR
         d.w, d.a_r, d.b_r = wp, ap, bp
         d.device, d.shard_rank, d.shard_count = device, shard_rank, shard_count
-        d.flags = L.RSP_FLAG_DETERMINISTIC if deterministic else 0
+        d.flags = (L.RSP_FLAG_DETERMINISTIC if deterministic else 0) | \
+            (L.RSP_FLAG_BATCH_TCGEN05 if batch_tcgen05 else 0)
         h = ct.c_void_p()
         if torch is not None and wmem == L.RSP_MEM_DEVICE:
             torch.cuda.synchronize(device)
@@ -447,6 +448,21 @@ class Stack:
 
     def launch(self, stream=None) -> None:
         check(L.lib().rsp_stack_launch(self._h, _stream_ptr(stream)), "rsp_stack_launch")
+
+    def io_spans(self):
+        """(x_bytes, y_bytes): the device spans covering all inputs / outputs."""
+        xb, yb = ct.c_size_t(), ct.c_size_t()
+        check(L.lib().rsp_stack_io_spans(self._h, ct.byref(xb), ct.byref(yb)), "rsp_stack_io_spans")
+        return xb.value, yb.value
+
+    def launch_host(self, x_host, y_host, stream=None) -> None:
+        """End to end through the ABI (rsp_stack_launch_host): H2D of x_host
+        (a host tensor / array covering the stack's input span), the stack,
+        D2H of the output span into y_host; returns synchronised."""
+        xb, yb = self.io_spans()
+        xp = x_host.data_ptr() if hasattr(x_host, "data_ptr") else x_host.ctypes.data
+        yp = y_host.data_ptr() if hasattr(y_host, "data_ptr") else y_host.ctypes.data
+        check(L.lib().rsp_stack_launch_host(self._h, xp, xb, yp, yb, _stream_ptr(stream)), "rsp_stack_launch_host")
 
     def close(self) -> None:
         if getattr(self, "_h", None):

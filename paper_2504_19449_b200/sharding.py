@@ -19,7 +19,6 @@ of this host logic).  Compute is librsparse_b200.so.
 """
 from __future__ import annotations
 
-import os
 from typing import List, Optional, Sequence, Tuple
 
 from .layer import DecomposedLayer, SparsityPlan, shard_rows
@@ -115,15 +114,15 @@ class ShardedLinear:
         self.in_place = even_shards(self.m_out, self.world)
         return self
 
-    def forward(self, x, out=None, workspace=None, stream=None):
+    def forward(self, x, out=None, workspace=None, stream=None, force_gather: bool = False):
+        """force_gather: run the collective on a single rank too (exercises
+        the NCCL-in-graph path on one GPU)."""
         if out is None:
             out = torch.empty(self.m_out, dtype=torch.float32, device=x.device)
         if self.in_place and x.dim() == 1:
             mine = out[self.row_begin:self.row_end]
             self.layer.forward(x, out=mine, workspace=workspace, stream=stream)
-            # (RSP_FORCE_GATHER=1 runs the collective on a single rank too: exercises
-            # the NCCL-in-graph path on one GPU)
-            if self.world > 1 or (os.environ.get("RSP_FORCE_GATHER") == "1" and dist.is_initialized()):
+            if self.world > 1 or (force_gather and dist.is_initialized()):
                 dist.all_gather_into_tensor(out, mine, group=self.group)
             return out
         y_local = self.layer.forward(x, workspace=workspace, stream=stream)
@@ -139,10 +138,12 @@ class ShardedStack:
     captured once into a CUDA graph; one replay = one token through the stack.
     ``xs[i]`` / ``ys[i]`` (full-length fp32) are bound at capture time."""
 
-    def __init__(self, linears: Sequence[ShardedLinear], xs, ys, stream=None, group=None):
+    def __init__(self, linears: Sequence[ShardedLinear], xs, ys, stream=None, group=None,
+                 force_gather: bool = False):
         # DecomposedLayer shards (built with shard_rank/shard_count) are wrapped
         self.linears = [l if isinstance(l, ShardedLinear) else ShardedLinear.from_layer(l, group) for l in linears]
         self.xs, self.ys = list(xs), list(ys)
+        self.force = force_gather
         self.stream = stream or torch.cuda.Stream()
         # one workspace per linear: the fused kernel's grid barrier words are
         # per-workspace, and consecutive kernels may overlap under PDL
@@ -156,7 +157,7 @@ class ShardedStack:
 
     def _run(self):
         for l, x, y, ws in zip(self.linears, self.xs, self.ys, self.ws):
-            l.forward(x, out=y, workspace=ws, stream=self.stream)
+            l.forward(x, out=y, workspace=ws, stream=self.stream, force_gather=self.force)
 
     def launch(self):
         self.graph.replay()
@@ -171,7 +172,8 @@ class ShardedGroupStack:
     inside a capture, else replayed eagerly.  Needs even shards (every
     BASELINE shape at N <= 8); `ys[i]` are the full-length outputs."""
 
-    def __init__(self, layers: Sequence[DecomposedLayer], xs, ys, gid: Sequence[int], stream=None, group=None):
+    def __init__(self, layers: Sequence[DecomposedLayer], xs, ys, gid: Sequence[int], stream=None, group=None,
+                 force_gather: bool = False):
         from .layer import Stack
         self.rank, self.world = _group_info(group)
         self.group = group
@@ -187,7 +189,7 @@ class ShardedGroupStack:
             st = Stack([self.layers[i] for i in idx], [self.xs[i] for i in idx], locs,
                        wait_prev=[False] * len(idx))
             self.groups.append((st, idx, locs))
-        self.force = os.environ.get("RSP_FORCE_GATHER") == "1" and dist.is_initialized()
+        self.force = force_gather and dist.is_initialized()
         self.graph = None
         with torch.cuda.stream(self.stream):
             self._run()  # warm NCCL communicators outside capture

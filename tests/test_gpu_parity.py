@@ -413,16 +413,17 @@ def test_batched_forward_matches_per_token_oracle(coracle, cuda, shape, batch):
 @pytest.mark.parametrize("shape", [(11008, 4096, 0.27, 687), (4096, 11008, 0.19, 933), (1000, 700, 0.3, 40)])
 @pytest.mark.parametrize("batch", [3, 16])
 def test_batched_tcgen05_variant_matches_oracle(coracle, cuda, monkeypatch, shape, batch):
-    """RSP_BATCH_TC=1: the cooperative ring's products on tcgen05 (TMEM
-    accumulators, one issuing thread, mbarrier-tracked ring slots) instead of
-    warp-level mma.sync -- same per-token semantics and tolerance."""
-    monkeypatch.setenv("RSP_BATCH_TC", "1")
+    """RSP_FLAG_BATCH_TCGEN05: the cooperative ring's products on tcgen05
+    (TMEM accumulators, one issuing thread, mbarrier-tracked ring slots)
+    instead of warp-level mma.sync -- same per-token semantics and tolerance."""
     m, n, s, r = shape
     rng = np.random.default_rng(m + 3 * n + batch)
     w = torch.from_numpy(rng.standard_normal((m, n)).astype(np.float32) * 0.02)
     a = torch.from_numpy(rng.standard_normal((m, r)).astype(np.float32) * 0.05)
     b = torch.from_numpy(rng.standard_normal((r, n)).astype(np.float32) * 0.05)
-    layer = rsp.DecomposedLayer(w.to(cuda), a.to(cuda), b.to(cuda), rsp.SparsityPlan(s, r), weight_dtype="bf16")
+    layer = rsp.DecomposedLayer(w.to(cuda), a.to(cuda), b.to(cuda), rsp.SparsityPlan(s, r), weight_dtype="bf16",
+                                batch_tcgen05=True)
+    assert layer.info["path"] & 4  # RSP_PATH_BATCH_TCGEN05
     X = torch.stack([torch.from_numpy(wl.heavy_tailed_x(n, rng)) for _ in range(batch)]).to(cuda).to(torch.bfloat16)
     Y = layer.forward(X).cpu().numpy()
     W, A, Bm = layer.export()
@@ -454,7 +455,7 @@ def test_sharded_bench_path_one_rank(cuda, tmp_path):
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, RSP_FORCE_GATHER="1")
+    env = dict(os.environ)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
            "--master-addr", "127.0.0.1", "--master-port", "29517", os.path.join(root, "bench.py"), "--gpus", "1",
            "--layers", "1", "--steps", "2", "--warmup", "1", "--force-sharded", "--no-cpu", "--no-dense"]

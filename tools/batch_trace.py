@@ -1,4 +1,4 @@
-"""Phase timeline of one batched forward (RSP_BATCH_TRACE=1): medians and
+"""Phase timeline of one batched forward (rsp_debug_set_batch_trace): medians and
 maxima over the CTAs of the per-phase clock64 stamps, in us at --mhz."""
 import argparse
 import ctypes as ct
@@ -8,7 +8,6 @@ import sys
 import numpy as np
 import torch
 
-os.environ["RSP_BATCH_TRACE"] = "1"
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import paper_2504_19449_b200 as rsp  # noqa: E402
@@ -18,6 +17,7 @@ from paper_2504_19449_b200 import workloads as wl  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--mhz", type=float, default=1965.0)
 a = ap.parse_args()
+L.check(L.lib().rsp_debug_set_batch_trace(1), "trace on")
 dev = torch.device("cuda:0")
 rng = np.random.default_rng(3)
 PH = ["cut", "stage-x", "lists", "stage1", "arrive", "Wrows", "tbar", "stage2", "combine"]
