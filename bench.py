@@ -425,10 +425,18 @@ def run_ours(args):
     h2d = x_host.numel() * 2
     d2h = y_dev.numel() * 4
 
-    def e2e_step():
-        x_dev.copy_(x_host, non_blocking=True)
-        launch()
-        y_host.copy_(y_dev, non_blocking=True)
+    if not sharded:
+        # through the ABI's host-buffer entry (rsp_stack_launch_host): H2D of
+        # the token's activations, the stack, D2H of every output, synchronised
+        assert st.io_spans() == (x_host.numel() * 2, y_host.numel() * 4)
+
+        def e2e_step():
+            st.launch_host(x_host, y_host, stream)
+    else:
+        def e2e_step():
+            x_dev.copy_(x_host, non_blocking=True)
+            launch()
+            y_host.copy_(y_dev, non_blocking=True)
 
     with torch.cuda.stream(stream):
         e2e_total, _ = time_graph(torch, e2e_step, args.steps, args.warmup, stream, barrier)
@@ -462,7 +470,9 @@ def run_ours(args):
                      "kernel": ("stack_kernel<bf16,bf16> (1 launch per input group, + NCCL all-gather of y)" if sharded
                                 else "stack_kernel<bf16,bf16> (1 persistent launch/step, 224 linears)")},
         "e2e": {"value": e2e_ms * 1e3, "unit": "us/token", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h},
+                "d2h_bytes_per_step": d2h,
+                "path": "rsp_stack_launch_host (C ABI, pinned host buffers, synchronised per token)" if not sharded
+                else "torch pinned copies around the sharded graph"},
         "gpu_launches": args.steps * (max(gid) + 1 if sharded else 1),
         "clocks": clocks.summary(),
     }

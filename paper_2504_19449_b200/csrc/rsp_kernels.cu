@@ -605,9 +605,11 @@ __device__ __forceinline__ void run_linear(const StackParams& P, const LinDesc& 
     if (!det) {
       for (int i = tid; i < na; i += kThreads) stsf(C.coef_a + 4u * i, __ldcg(t_cur + alo + i));
     } else {
-      // 8 lanes per row sum the row's nb_pad partials (float4 loads, fixed order, fixed xor tree)
+      // 8 lanes per row sum the row's partials of THIS linear's NB CTAs
+      // (float4 loads, fixed order, fixed xor tree).  Entries past NB belong
+      // to other linears of a stack (the scratch is shared): masked.
       const int g8 = tid >> 3, l8 = tid & 7, ng8 = kThreads / 8;
-      const int nq = P.nb_pad / 4;
+      const int nq = (NB + 3) / 4;
       for (int cbase = alo; cbase < ahi; cbase += ng8) {  // uniform trip count: shuffles below
         const int c = cbase + g8;
         float sum = 0.f;
@@ -615,7 +617,9 @@ __device__ __forceinline__ void run_linear(const StackParams& P, const LinDesc& 
           const float4* row = reinterpret_cast<const float4*>(P.t_part + static_cast<size_t>(c) * P.nb_pad);
           for (int q = l8; q < nq; q += 8) {
             const float4 u = __ldcg(row + q);
-            sum += (u.x + u.y) + (u.z + u.w);
+            const int e0 = 4 * q;
+            sum += ((e0 < NB ? u.x : 0.f) + (e0 + 1 < NB ? u.y : 0.f)) +
+                   ((e0 + 2 < NB ? u.z : 0.f) + (e0 + 3 < NB ? u.w : 0.f));
           }
         }
         sum += __shfl_xor_sync(0xffffffffu, sum, 4);

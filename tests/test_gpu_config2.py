@@ -49,24 +49,30 @@ def _config2_layers(layer_ids, dev, seed=7):
     return sel, out
 
 
-@pytest.mark.parametrize("layer_ids", [(13,), (26, 30)])
-def test_config2_stack_every_output_vs_oracle(coracle, cuda, layer_ids):
+@pytest.mark.parametrize("layer_ids,deterministic", [((13,), False), ((26, 30), False), ((13,), True)])
+def test_config2_stack_every_output_vs_oracle(coracle, cuda, layer_ids, deterministic):
     plans, built = _config2_layers(layer_ids, cuda)
     assert any(r > 1024 for (*_, r) in plans), "these layers carry the r > 1024 linears"
     gid, wait = wl.input_groups(plans)
     rng = np.random.default_rng(11)
     layers, xs, xg = [], [], {}
     for i, (name, m, n, s, r, w, a, b) in enumerate(built):
-        layers.append(rsp.DecomposedLayer(w, a, b, rsp.SparsityPlan(s, r), weight_dtype="bf16"))
+        layers.append(rsp.DecomposedLayer(w, a, b, rsp.SparsityPlan(s, r), weight_dtype="bf16",
+                                          deterministic=deterministic))
         if gid[i] not in xg:
             x = wl.silu_gate_x(n, rng) if name.endswith("down_proj") else wl.heavy_tailed_x(n, rng)
             xg[gid[i]] = torch.from_numpy(x).to(cuda).to(torch.bfloat16)
         xs.append(xg[gid[i]])
     ys = [torch.full((l.m_out,), float("nan"), device=cuda) for l in layers]
     st = rsp.Stack(layers, xs, ys, wait_prev=wait)
+    outs = []
     for _ in range(3):  # repeated launches reuse the workspace (epoch, counters, t buffers)
         st.launch()
-    torch.cuda.synchronize()
+        torch.cuda.synchronize()
+        outs.append([y.clone() for y in ys])
+    if deterministic:  # fixed-order combines: bit-reproducible, and equal to each layer's own forward
+        assert all(torch.equal(a, b) for o in outs[1:] for a, b in zip(outs[0], o))
+        assert all(torch.equal(y, l.forward(x)) for l, x, y in zip(layers, xs, ys))
     for i, (layer, x, y) in enumerate(zip(layers, xs, ys)):
         name, m, n, s, r, w, a, b = built[i]
         W, A, B = layer.export()
@@ -152,3 +158,36 @@ def test_selector_too_large_is_unsupported(cuda):
     # and the runtime is still healthy
     y = rsp.top_k_by_magnitude(torch.arange(100, dtype=torch.float32, device=cuda), 3)
     assert y.cpu().tolist() == [97, 98, 99]
+
+
+def test_stack_launch_host_matches_device_launch(cuda):
+    """rsp_stack_launch_host (the stack's end-to-end ABI entry): one H2D of
+    the input span, the stack, one D2H of the output span."""
+    rng = np.random.default_rng(8)
+    shapes = [("layers.0.q_proj", 512, 256, 0.3, 32), ("layers.0.k_proj", 256, 256, 0.2, 16),
+              ("layers.0.o_proj", 256, 512, 0.25, 24)]
+    gid, wait = wl.input_groups(shapes)
+    layers = [rsp.DecomposedLayer(torch.randn(m, n, device=cuda) * 0.05, torch.randn(m, r, device=cuda) * 0.1,
+                                  torch.randn(r, n, device=cuda) * 0.1, rsp.SparsityPlan(s, r))
+              for (_, m, n, s, r) in shapes]
+    xin = [wl.heavy_tailed_x(256, rng), wl.heavy_tailed_x(512, rng)]
+    x_host = torch.from_numpy(np.concatenate(xin)).to(torch.bfloat16).pin_memory()
+    x_dev = x_host.to(cuda)
+    xs = [x_dev[:256], x_dev[:256], x_dev[256:]]
+    y_dev = torch.zeros(512 + 256 + 256, device=cuda)
+    ys = [y_dev[:512], y_dev[512:768], y_dev[768:]]
+    st = rsp.Stack(layers, xs, ys, wait_prev=wait)
+    assert st.io_spans() == (x_host.numel() * 2, y_dev.numel() * 4)
+    st.launch()
+    torch.cuda.synchronize()
+    want = y_dev.cpu().clone()
+    y_dev.zero_()
+    x_dev.zero_()  # the host entry must bring the inputs itself
+    y_host = torch.empty(y_dev.numel()).pin_memory()
+    st.launch_host(x_host, y_host)
+    assert torch.allclose(y_host, want, rtol=1e-6, atol=1e-6)
+    with pytest.raises(rsp.UsageError):
+        rsp.lib()  # noqa: B018 (keep the library loaded)
+        import ctypes as ct
+        from paper_2504_19449_b200 import _lib as L
+        L.check(L.lib().rsp_stack_launch_host(st._h, x_host.data_ptr(), 2, y_host.data_ptr(), 4, None))
