@@ -447,6 +447,8 @@ def run_ours(args):
         e2e_ms = float(t.item())
 
     extras = {}
+    if args.check and rank == 0:  # the stack's own outputs, before the dense baselines reuse ys
+        extras["check"] = check_outputs(layers, xs, ys, plans)
     if not args.no_dense and not args.profile and world == 1:
         extras.update(dense_baselines(torch, rsp, layers, xs, ys, stream, args, plans, dev, gid, wait))
 
@@ -489,8 +491,7 @@ def run_ours(args):
                                "kind": cpu["kind"],
                                "sample": cpu["sample"] + f"; x{scale:g} from {cpu['layers_timed']} to "
                                                          f"{len(plans) // 7} layers"}
-    if args.check and rank == 0:
-        out["check"] = check_outputs(layers, xs, ys, plans)
+
     if rank == 0:
         print(json.dumps(out), flush=True)
     if sharded:

@@ -253,6 +253,17 @@ rsp_status rsp_stack_create(const rsp_linear* const* layers, uint32_t count,
 rsp_status rsp_stack_create_ex(const rsp_linear* const* layers, uint32_t count,
                                const void* const* x_devs, rsp_dtype x_dtype, float* const* y_devs,
                                int dense, const uint8_t* wait_prev, rsp_stack** out);
+/* As rsp_stack_create_ex, with an input operator per linear (x_ops may be
+ * NULL = all RSP_XOP_NONE).  RSP_XOP_SILU_GATE: x_devs[i] holds two fp32
+ * vectors [a (m_in) | g (m_in)] -- typically the outputs of a stack's up and
+ * gate linears written side by side -- and the linear's input is
+ * a * silu(g), formed inside the kernel's x load (the gated MLP of
+ * model.cpp:115-127: down_proj reads up * silu(gate)); needs x_dtype F32. */
+#define RSP_XOP_NONE 0u
+#define RSP_XOP_SILU_GATE 1u
+rsp_status rsp_stack_create_ops(const rsp_linear* const* layers, uint32_t count,
+                                const void* const* x_devs, rsp_dtype x_dtype, float* const* y_devs,
+                                int dense, const uint8_t* wait_prev, const uint8_t* x_ops, rsp_stack** out);
 rsp_status rsp_stack_launch(rsp_stack* s, void* stream);
 /* The end-to-end stack path with host buffers: x_host (x_bytes) is copied to
  * the span of device memory covering all the stack's inputs (the x_devs given

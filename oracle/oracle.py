@@ -255,6 +255,16 @@ class RefOracle(_Lib):
         L.rspr_read_layer.restype = ct.c_int
         L.rspr_mlp_forward.argtypes = [ct.c_void_p, ct.c_void_p, ct.c_void_p, _dp, ct.c_size_t, _dp]
         L.rspr_mlp_forward.restype = ct.c_int
+        _ip = ct.POINTER(ct.c_int)
+        _vpp = ct.POINTER(ct.c_void_p)
+        L.rspr_model_write.argtypes = [ct.c_size_t] * 5 + [ct.c_uint64, ct.c_size_t, ct.c_char_p]
+        L.rspr_model_write.restype = ct.c_int
+        L.rspr_model_logits.argtypes = [ct.c_char_p, _ip, ct.c_size_t, _vpp, ct.c_size_t, ct.c_size_t, _dp]
+        L.rspr_model_logits.restype = ct.c_int
+        L.rspr_model_perplexity.argtypes = [ct.c_char_p, _ip, ct.c_size_t, ct.c_size_t, _vpp, ct.c_size_t, _dp]
+        L.rspr_model_perplexity.restype = ct.c_int
+        L.rspr_recipe_loss.argtypes = [ct.c_char_p, _ip, ct.c_size_t, ct.c_size_t, _dp, _dp, ct.c_size_t, _dp, _dp]
+        L.rspr_recipe_loss.restype = ct.c_int
         L.rspr_aggregate_scores.argtypes = [_dp, ct.c_size_t, ct.c_size_t, _dp, _dp, ct.c_size_t,
                                             ct.c_uint, _dp]
         L.rspr_aggregate_scores.restype = ct.c_int
@@ -332,6 +342,47 @@ class RefOracle(_Lib):
         out = np.empty(x.shape[0], dtype=np.float64)
         _raise(self.lib.rspr_mlp_forward(up.h, gate.h, down.h, _d(x), x.shape[0], _d(out)), "mlp_forward")
         return out
+
+    # -- model.cpp / search.cpp (the toy decoder that calls forward) ---------
+    def model_write(self, path: str, num_layers=2, embed=64, hidden=172, heads=4, vocab=256, seed=1,
+                    max_seq=256) -> None:
+        """init_model + write_model (model.cpp:89-113, 767-792)."""
+        _raise(self.lib.rspr_model_write(num_layers, embed, hidden, heads, vocab, seed, max_seq, path.encode()),
+               "model_write")
+
+    @staticmethod
+    def _handles(layers):
+        if layers is None:
+            return None, 0
+        arr = (ct.c_void_p * len(layers))(*[l.h for l in layers])
+        return arr, len(layers)
+
+    def model_logits(self, path: str, tokens, layers=None, decode_start: int = 0, vocab: int = 256) -> np.ndarray:
+        """read_model + model_forward (model.cpp:159-242)."""
+        tok = np.ascontiguousarray(tokens, dtype=np.int32)
+        out = np.empty((tok.size, vocab), dtype=np.float64)
+        hp, nl = self._handles(layers)
+        _raise(self.lib.rspr_model_logits(path.encode(), tok.ctypes.data_as(ct.POINTER(ct.c_int)), tok.size, hp, nl,
+                                          decode_start, _d(out)), "model_forward")
+        return out
+
+    def model_perplexity(self, path: str, tokens, split_point: int, layers=None) -> float:
+        """read_model + perplexity (model.cpp:244-269)."""
+        tok = np.ascontiguousarray(tokens, dtype=np.int32)
+        out = ct.c_double()
+        hp, nl = self._handles(layers)
+        _raise(self.lib.rspr_model_perplexity(path.encode(), tok.ctypes.data_as(ct.POINTER(ct.c_int)), tok.size,
+                                              split_point, hp, nl, ct.byref(out)), "perplexity")
+        return out.value
+
+    def recipe_loss(self, path: str, calib, seq_len: int, rho, budget):
+        """RecipeEvaluator(model, calib, seq_len).loss(Recipe{rho, budget}), dense_loss() (search.cpp:36-105)."""
+        tok = np.ascontiguousarray(calib, dtype=np.int32)
+        r, b = _as_f64(rho), _as_f64(budget)
+        loss, dense = ct.c_double(), ct.c_double()
+        _raise(self.lib.rspr_recipe_loss(path.encode(), tok.ctypes.data_as(ct.POINTER(ct.c_int)), tok.size, seq_len,
+                                         _d(r), _d(b), r.size, ct.byref(loss), ct.byref(dense)), "recipe_loss")
+        return loss.value, dense.value
 
     def aggregate_scores(self, tokens, sigma, vt, workers: int = 1) -> np.ndarray:
         """aggregate_scores (scores.cpp:52-62): tokens [T, n], sigma [kc], vt [kc, n] -> [kc, n]."""

@@ -308,4 +308,71 @@ int rspr_read_layer(const char* path, uint64_t* dims, double* w_cols, double* a_
   })
 }
 
+// -- model-level callers (model.cpp:89-269, search.cpp:36-105) --------------
+// init_model + write_model (model.cpp:89-113, 767-792): a reference ToyModel
+// in an RSPW file.
+int rspr_model_write(size_t num_layers, size_t embed, size_t hidden, size_t heads, size_t vocab, uint64_t seed,
+                     size_t max_seq, const char* path) {
+  GUARD({
+    ModelConfig cfg;
+    cfg.num_layers = num_layers;
+    cfg.embed_dim = embed;
+    cfg.hidden_dim = hidden;
+    cfg.num_heads = heads;
+    cfg.vocab_size = vocab;
+    cfg.seed = seed;
+    cfg.max_seq = max_seq;
+    write_model(init_model(cfg), path);
+  })
+}
+
+namespace {
+// A DecomposedModel from layer handles (rspr_layer_create), global linear order.
+DecomposedModel gather_model(const void* const* layers, size_t count) {
+  DecomposedModel dm;
+  for (size_t i = 0; i < count; ++i) dm.layers.push_back(*static_cast<const DecomposedLayer*>(layers[i]));
+  return dm;
+}
+}  // namespace
+
+// read_model + model_forward (model.cpp:159-242): logits T x vocab;
+// layers == NULL: the dense model.
+int rspr_model_logits(const char* path, const int* tokens, size_t T, const void* const* layers, size_t nlayers,
+                      size_t decode_start, double* logits) {
+  GUARD({
+    const ToyModel m = read_model(path);
+    DecomposedModel dm;
+    if (layers) dm = gather_model(layers, nlayers);
+    const Matrix out = model_forward(m, std::span<const int>(tokens, T), layers ? &dm : nullptr, decode_start);
+    std::memcpy(logits, out.data(), out.size() * sizeof(double));
+  })
+}
+
+// read_model + perplexity (model.cpp:244-269).
+int rspr_model_perplexity(const char* path, const int* tokens, size_t T, size_t split_point,
+                          const void* const* layers, size_t nlayers, double* out) {
+  GUARD({
+    const ToyModel m = read_model(path);
+    DecomposedModel dm;
+    if (layers) dm = gather_model(layers, nlayers);
+    *out = perplexity(m, std::span<const int>(tokens, T), split_point, layers ? &dm : nullptr);
+  })
+}
+
+// RecipeEvaluator(model, calibration, seq_len).loss(Recipe{rho, budget}) and
+// dense_loss() (search.cpp:36-105): the reference's own pipeline (Jacobi
+// SVD, scores, decompose_with_svd, perplexity).
+int rspr_recipe_loss(const char* path, const int* calib, size_t ncalib, size_t seq_len, const double* rho,
+                     const double* budget, size_t nlin, double* loss, double* dense_loss) {
+  GUARD({
+    const ToyModel m = read_model(path);
+    const RecipeEvaluator ev(m, std::span<const int>(calib, ncalib), seq_len);
+    Recipe rc;
+    rc.rho.assign(rho, rho + nlin);
+    rc.budget.assign(budget, budget + nlin);
+    *loss = ev.loss(rc);
+    if (dense_loss) *dense_loss = ev.dense_loss();
+  })
+}
+
 }  // extern "C"

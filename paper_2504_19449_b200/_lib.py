@@ -25,7 +25,7 @@ EXPORTS = [
     "rsp_top_k_by_magnitude", "rsp_threshold_sparsify", "rsp_stack_create", "rsp_stack_create_ex",
     "rsp_stack_launch", "rsp_stack_destroy", "rsp_device_sm_count", "rsp_debug_forward_trace",
     "rsp_debug_stack_trace", "rsp_debug_batch_trace", "rsp_debug_set_batch_trace", "rsp_stack_io_spans",
-    "rsp_stack_launch_host", "rsp_rspl_read", "rsp_linear_load_rspl", "rsp_linear_save_rspl", "rsp_linear_components",
+    "rsp_stack_launch_host", "rsp_stack_create_ops", "rsp_rspl_read", "rsp_linear_load_rspl", "rsp_linear_save_rspl", "rsp_linear_components",
     "rsp_aggregate_scores", "rsp_select_components", "rsp_split_factors", "rsp_linear_set_components",
 ]
 
@@ -43,6 +43,7 @@ class LinearDesc(ct.Structure):
 
 RSP_FLAG_DETERMINISTIC = 1
 RSP_FLAG_BATCH_TCGEN05 = 2
+RSP_XOP_NONE, RSP_XOP_SILU_GATE = 0, 1
 RSP_PATH_PERSISTENT, RSP_PATH_BATCH_MMA, RSP_PATH_BATCH_TCGEN05, RSP_PATH_DETERMINISTIC = 1, 2, 4, 8
 
 
@@ -133,6 +134,9 @@ def lib() -> ct.CDLL:
                                         ct.POINTER(vp), ct.c_int, ct.POINTER(vp)]),
         "rsp_stack_create_ex": (ct.c_int, [ct.POINTER(vp), u32, ct.POINTER(vp), ct.c_int,
                                            ct.POINTER(vp), ct.c_int, ct.POINTER(ct.c_uint8), ct.POINTER(vp)]),
+        "rsp_stack_create_ops": (ct.c_int, [ct.POINTER(vp), u32, ct.POINTER(vp), ct.c_int,
+                                            ct.POINTER(vp), ct.c_int, ct.POINTER(ct.c_uint8), ct.POINTER(ct.c_uint8),
+                                            ct.POINTER(vp)]),
         "rsp_stack_launch": (ct.c_int, [vp, vp]),
         "rsp_stack_destroy": (None, [vp]),
         "rsp_device_sm_count": (ct.c_int, [ct.c_int]),

@@ -979,8 +979,19 @@ rsp_status rsp_linear_export(const rsp_linear* h, int which, double* out) {
 rsp_status rsp_stack_create_ex(const rsp_linear* const* layers, uint32_t count, const void* const* x_devs,
                                rsp_dtype xdt, float* const* y_devs, int dense, const uint8_t* wait_prev,
                                rsp_stack** out) {
+  return rsp_stack_create_ops(layers, count, x_devs, xdt, y_devs, dense, wait_prev, nullptr, out);
+}
+
+rsp_status rsp_stack_create_ops(const rsp_linear* const* layers, uint32_t count, const void* const* x_devs,
+                                rsp_dtype xdt, float* const* y_devs, int dense, const uint8_t* wait_prev,
+                                const uint8_t* x_ops, rsp_stack** out) {
   if (!layers || !x_devs || !y_devs || !out || count == 0) return fail(RSP_E_USAGE, "bad stack arguments");
   if (rsp_status st = check_x_dtype(xdt)) return st;
+  for (uint32_t i = 0; x_ops && i < count; ++i) {
+    if (x_ops[i] > RSP_XOP_SILU_GATE) return fail(RSP_E_USAGE, "x_ops[%u] = %u is not an RSP_XOP_*", i, x_ops[i]);
+    if (x_ops[i] == RSP_XOP_SILU_GATE && xdt != RSP_F32)
+      return fail(RSP_E_USAGE, "RSP_XOP_SILU_GATE needs fp32 activations (the gated input is formed in fp32)");
+  }
   *out = nullptr;
   const rsp_linear* h0 = layers[0];
   const int dev = h0->device;
@@ -1030,8 +1041,9 @@ rsp_status rsp_stack_create_ex(const rsp_linear* const* layers, uint32_t count, 
       budget = std::min(budget, sms - cta0 - static_cast<int>(g1 - 1 - i));  // leave >= 1 CTA per later member
       if (rsp_status st = make_plan(*layers[i], dpx, &plans[i], std::max(1, budget))) return st;
       const bool wp = i > 0 && (i == g0);
+      const int xop = (x_ops && x_ops[i] == RSP_XOP_SILU_GATE) ? rsp::kLinSiluGate : 0;
       descs[i] = lin_desc(layers[i], x_devs[i], y_devs[i], dense != 0, static_cast<int>(i),
-                          wp ? rsp::kLinWaitPrev : 0, &plans[i], cta0);
+                          (wp ? rsp::kLinWaitPrev : 0) | xop, &plans[i], cta0);
       if (wp) {
         descs[i].dep0 = static_cast<int>(pg0);
         descs[i].ndep = static_cast<int>(pg1 - pg0);
@@ -1067,7 +1079,7 @@ rsp_status rsp_stack_create_ex(const rsp_linear* const* layers, uint32_t count, 
     for (uint32_t i = 0; i < count; ++i) {
       const uintptr_t xa = reinterpret_cast<uintptr_t>(x_devs[i]), ya = reinterpret_cast<uintptr_t>(y_devs[i]);
       xl = std::min(xl, xa);
-      xh = std::max(xh, xa + xe * layers[i]->m_in);
+      xh = std::max(xh, xa + xe * layers[i]->m_in * ((x_ops && x_ops[i] == RSP_XOP_SILU_GATE) ? 2 : 1));
       yl = std::min(yl, ya);
       yh = std::max(yh, ya + sizeof(float) * layers[i]->m);
     }

@@ -17,6 +17,8 @@ constexpr int kPlanBytes = 96;        // one (linear, CTA) entry of a stack's pl
 // Flags of one linear in a stack launch.
 constexpr int kLinWaitPrev = 1;  // its x depends on the previous group's y: wait for that group's CTAs first
 constexpr int kLinDense = 2;     // all n channels through W, no selection, no low-rank term
+constexpr int kLinSiluGate = 4;  // fp32 x holds [a (n) | g (n)]: the input is a * silu(g) (gated MLP), formed
+                                 // in the x load (model.cpp:122-126: hidden = up * silu(gate))
 
 // One linear of a stack launch (descriptors live in device memory; a
 // single-linear forward passes its descriptor inline).

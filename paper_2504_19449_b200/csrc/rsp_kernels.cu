@@ -267,6 +267,23 @@ __device__ __forceinline__ unsigned* slot_of(const StackParams& P, int slot) {
   return P.slots + static_cast<size_t>(slot) * kSlotWords;
 }
 
+// Gated-MLP input formed in the x load (fp32): x_j = a_j * silu(g_j) with
+// [a | g] the two fp32 vectors at x (up's and gate's outputs of the same
+// stack: model.cpp:122-126).  silu(g) = g / (1 + expf(-g)), IEEE division --
+// bit-identical to torch's a * (g / (1 + exp(-g))) in fp32 on the device.
+__device__ __forceinline__ void sel_load_silu_gate(const void* __restrict__ x, int n, SelArea s, bool hist) {
+  const float* a = static_cast<const float*>(x);
+  const float* g = a + n;
+  for (int j = threadIdx.x; j < n; j += kThreads) {
+    const float gj = __ldcg(g + j);
+    const float v = __ldcg(a + j) * (gj / (1.0f + expf(-gj)));
+    const uint32_t bits = __float_as_uint(v);
+    sts(s.xs + 4u * static_cast<uint32_t>(j), bits);
+    if (hist) hist_add(s, bits);
+  }
+  __syncthreads();
+}
+
 // Per-(linear, CTA) constants of run_linear.  Each integer division is a
 // ~20-instruction dependent chain; a linear needs ~20 of them, which cost
 // ~0.5 us at the head of every linear when computed there.  Thread 0
@@ -400,7 +417,7 @@ __device__ __forceinline__ void prep_linear(const StackParams& P, const LinDesc&
   if (tid == 32 && (reinterpret_cast<uintptr_t>(d.x) & 15u) == 0) {
     // x (contiguous) towards L2 before its producer is done (harmless: L2 is the
     // coherence point its reductions land in); measured -0.7% (2270 -> 2255 us)
-    const uint32_t xb = static_cast<uint32_t>(d.n) * (XBF ? 2u : 4u);
+    const uint32_t xb = static_cast<uint32_t>(d.n) * (XBF ? 2u : 4u) * ((d.flags & kLinSiluGate) ? 2u : 1u);
     prefetch_l2_bulk(d.x, (xb + 15u) & ~15u);
   }
   const bool det = P.deterministic != 0;
@@ -478,7 +495,8 @@ __device__ __forceinline__ void run_linear(const StackParams& P, const LinDesc& 
     RSP_TRACE(2);
     if (!dense) cut = sel_cut16(d.n, d.k, S);
   } else {
-    sel_load<false>(d.x, d.n, S, !dense);
+    if (d.flags & kLinSiluGate) sel_load_silu_gate(d.x, d.n, S, !dense);
+    else sel_load<false>(d.x, d.n, S, !dense);
     RSP_TRACE(2);
     if (!dense) cut = sel_cut<false>(d.n, d.k, S);
   }

