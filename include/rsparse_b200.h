@@ -264,6 +264,28 @@ rsp_status rsp_stack_create_ex(const rsp_linear* const* layers, uint32_t count,
 rsp_status rsp_stack_create_ops(const rsp_linear* const* layers, uint32_t count,
                                 const void* const* x_devs, rsp_dtype x_dtype, float* const* y_devs,
                                 int dense, const uint8_t* wait_prev, const uint8_t* x_ops, rsp_stack** out);
+/* The general form.  npeer > 1 (row-sharded ranks): the
+ * output rows of linear i are written by the kernel to npeer destinations
+ * y_peers[i * npeer + p] -- each rank's copy of the FULL y of that linear,
+ * offset to this shard's first row -- so the all-gather of y is done by the
+ * stores of the producing CTAs themselves instead of a collective after the
+ * launch (with several GPUs the destinations are peer-mapped memory over
+ * NVLink; on one GPU, several ranks' shards run as one launch over all
+ * ranks' buffers).  y_devs is still required (the spans of
+ * rsp_stack_launch_host). */
+typedef struct rsp_stack_spec {
+  const rsp_linear* const* layers;
+  uint32_t count;
+  const void* const* x_devs;
+  rsp_dtype x_dtype;
+  float* const* y_devs;
+  int dense;
+  const uint8_t* wait_prev;  /* may be NULL: every linear waits for its predecessor */
+  const uint8_t* x_ops;      /* may be NULL: RSP_XOP_NONE */
+  uint32_t npeer;            /* 0 or 1: y_devs only; 2..8: y_peers */
+  float* const* y_peers;     /* count x npeer destinations (npeer > 1) */
+} rsp_stack_spec;
+rsp_status rsp_stack_create_spec(const rsp_stack_spec* spec, rsp_stack** out);
 rsp_status rsp_stack_launch(rsp_stack* s, void* stream);
 /* The end-to-end stack path with host buffers: x_host (x_bytes) is copied to
  * the span of device memory covering all the stack's inputs (the x_devs given

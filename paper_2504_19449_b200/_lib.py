@@ -25,7 +25,7 @@ EXPORTS = [
     "rsp_top_k_by_magnitude", "rsp_threshold_sparsify", "rsp_stack_create", "rsp_stack_create_ex",
     "rsp_stack_launch", "rsp_stack_destroy", "rsp_device_sm_count", "rsp_debug_forward_trace",
     "rsp_debug_stack_trace", "rsp_debug_batch_trace", "rsp_debug_set_batch_trace", "rsp_stack_io_spans",
-    "rsp_stack_launch_host", "rsp_stack_create_ops", "rsp_rspl_read", "rsp_linear_load_rspl", "rsp_linear_save_rspl", "rsp_linear_components",
+    "rsp_stack_launch_host", "rsp_stack_create_ops", "rsp_stack_create_spec", "rsp_rspl_read", "rsp_linear_load_rspl", "rsp_linear_save_rspl", "rsp_linear_components",
     "rsp_aggregate_scores", "rsp_select_components", "rsp_split_factors", "rsp_linear_set_components",
 ]
 
@@ -62,6 +62,15 @@ class IoReport(ct.Structure):
         ("dense_bytes", ct.c_uint64), ("touched_bytes", ct.c_uint64),
         ("relative_cost", ct.c_double), ("kernel_weight_bytes", ct.c_uint64),
         ("kernel_total_bytes", ct.c_uint64), ("dense_weight_bytes", ct.c_uint64),
+    ]
+
+
+class StackSpec(ct.Structure):
+    _fields_ = [
+        ("layers", ct.POINTER(ct.c_void_p)), ("count", ct.c_uint32), ("x_devs", ct.POINTER(ct.c_void_p)),
+        ("x_dtype", ct.c_int), ("y_devs", ct.POINTER(ct.c_void_p)), ("dense", ct.c_int),
+        ("wait_prev", ct.POINTER(ct.c_uint8)), ("x_ops", ct.POINTER(ct.c_uint8)), ("npeer", ct.c_uint32),
+        ("y_peers", ct.POINTER(ct.c_void_p)),
     ]
 
 
@@ -137,6 +146,7 @@ def lib() -> ct.CDLL:
         "rsp_stack_create_ops": (ct.c_int, [ct.POINTER(vp), u32, ct.POINTER(vp), ct.c_int,
                                             ct.POINTER(vp), ct.c_int, ct.POINTER(ct.c_uint8), ct.POINTER(ct.c_uint8),
                                             ct.POINTER(vp)]),
+        "rsp_stack_create_spec": (ct.c_int, [ct.POINTER(StackSpec), ct.POINTER(vp)]),
         "rsp_stack_launch": (ct.c_int, [vp, vp]),
         "rsp_stack_destroy": (None, [vp]),
         "rsp_device_sm_count": (ct.c_int, [ct.c_int]),

@@ -137,6 +137,7 @@ struct rsp_stack {
   cudaGraphExec_t exec = nullptr;
   void* ws = nullptr;
   LinDesc* descs = nullptr;  // device array
+  float** ypeer = nullptr;   // device [count][kMaxPeers] y destinations (npeer > 1)
   rsp::LinCtl* ctl = nullptr;  // device control table
   void* plans = nullptr;     // device plan table [count][grid]
   StackParams params = {};   // the captured launch (re-launched by the debug trace)
@@ -985,6 +986,35 @@ rsp_status rsp_stack_create_ex(const rsp_linear* const* layers, uint32_t count, 
 rsp_status rsp_stack_create_ops(const rsp_linear* const* layers, uint32_t count, const void* const* x_devs,
                                 rsp_dtype xdt, float* const* y_devs, int dense, const uint8_t* wait_prev,
                                 const uint8_t* x_ops, rsp_stack** out) {
+  rsp_stack_spec sp = {};
+  sp.layers = layers;
+  sp.count = count;
+  sp.x_devs = x_devs;
+  sp.x_dtype = xdt;
+  sp.y_devs = y_devs;
+  sp.dense = dense;
+  sp.wait_prev = wait_prev;
+  sp.x_ops = x_ops;
+  sp.npeer = 1;
+  return rsp_stack_create_spec(&sp, out);
+}
+
+rsp_status rsp_stack_create_spec(const rsp_stack_spec* spec, rsp_stack** out) {
+  if (!spec || !out) return fail(RSP_E_USAGE, "bad stack arguments");
+  const rsp_linear* const* layers = spec->layers;
+  const uint32_t count = spec->count;
+  const void* const* x_devs = spec->x_devs;
+  const rsp_dtype xdt = spec->x_dtype;
+  float* const* y_devs = spec->y_devs;
+  const int dense = spec->dense;
+  const uint8_t* wait_prev = spec->wait_prev;
+  const uint8_t* x_ops = spec->x_ops;
+  const uint32_t npeer = spec->npeer ? spec->npeer : 1;
+  if (npeer > static_cast<uint32_t>(rsp::kMaxPeers))
+    return fail(RSP_E_USAGE, "npeer %u exceeds %d y destinations", npeer, rsp::kMaxPeers);
+  if (npeer > 1 && !spec->y_peers) return fail(RSP_E_USAGE, "npeer > 1 needs y_peers");
+  for (uint32_t i = 0; npeer > 1 && i < count * npeer; ++i)
+    if (!spec->y_peers[i]) return fail(RSP_E_USAGE, "null y_peers[%u]", i);
   if (!layers || !x_devs || !y_devs || !out || count == 0) return fail(RSP_E_USAGE, "bad stack arguments");
   if (rsp_status st = check_x_dtype(xdt)) return st;
   for (uint32_t i = 0; x_ops && i < count; ++i) {
@@ -1100,6 +1130,13 @@ rsp_status rsp_stack_create_ops(const rsp_linear* const* layers, uint32_t count,
   for (uint32_t i = 0; i < count; ++i)
     ctl[i] = rsp::LinCtl{descs[i].flags, descs[i].dep0, descs[i].ndep, descs[i].cta0, descs[i].grid, descs[i].slot,
                          descs[gstart[i]].slot, 0};
+  if (e == cudaSuccess && npeer > 1) {
+    std::vector<float*> tab(static_cast<size_t>(count) * rsp::kMaxPeers, nullptr);
+    for (uint32_t i = 0; i < count; ++i)
+      for (uint32_t p = 0; p < npeer; ++p) tab[static_cast<size_t>(i) * rsp::kMaxPeers + p] = spec->y_peers[i * npeer + p];
+    e = cudaMalloc(&s->ypeer, sizeof(float*) * tab.size());
+    if (e == cudaSuccess) e = cudaMemcpy(s->ypeer, tab.data(), sizeof(float*) * tab.size(), cudaMemcpyHostToDevice);
+  }
   if (e == cudaSuccess) e = cudaMalloc(&s->ctl, sizeof(rsp::LinCtl) * count);
   if (e == cudaSuccess) e = cudaMemcpy(s->ctl, ctl.data(), sizeof(rsp::LinCtl) * count, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
@@ -1122,6 +1159,8 @@ rsp_status rsp_stack_create_ops(const rsp_linear* const* layers, uint32_t count,
     p.nb_pad = nb_pad;
     p.deterministic = det ? 1 : 0;
     p.zero = 0u;
+    p.ypeer = s->ypeer;
+    p.npeer = static_cast<int>(npeer);
     p.plans = s->plans;
     p.ctl = s->ctl;
     bind_workspace(&p, s->ws, wl);
@@ -1200,6 +1239,7 @@ void rsp_stack_destroy(rsp_stack* s) {
   cudaFree(s->descs);
   cudaFree(s->plans);
   cudaFree(s->ctl);
+  cudaFree(s->ypeer);
   delete s;
 }
 

@@ -13,6 +13,7 @@ constexpr unsigned kSlotWords = 32;  // per-linear barrier slot: [0] y arrivals,
 constexpr unsigned kMaxTickets = kSlotWords - 2;
 constexpr unsigned kWsHdrBytes = 256;  // [0] launch epoch, [1] CTAs done in this launch
 constexpr int kPlanBytes = 96;        // one (linear, CTA) entry of a stack's plan table
+constexpr int kMaxPeers = 8;          // y destinations per linear (row-sharded ranks)
 
 // Flags of one linear in a stack launch.
 constexpr int kLinWaitPrev = 1;  // its x depends on the previous group's y: wait for that group's CTAs first
@@ -59,6 +60,8 @@ struct StackParams {
   int deterministic;               // 1: fixed-order combines (bit-reproducible y); linears serialised
   int pdl;                         // 1: launched with programmatic dependent launch
   unsigned zero;                   // always 0: a value the compiler cannot fold (load batching in stream_list)
+  float* const* ypeer;             // npeer > 1: [count][kMaxPeers] destinations of each linear's y rows
+  int npeer;                       // destinations per y (1: the descriptor's y only)
   long long* trace;                // debug: [grid][16] phase timestamps of the last linear (null in production)
   const void* plans;               // [count][grid] per-CTA plans (plan_kernel), or null: computed in the kernel
   const LinCtl* ctl;               // [count] control table, or null (single linear: built from `one`)

@@ -422,9 +422,18 @@ __device__ __forceinline__ void prep_linear(const StackParams& P, const LinDesc&
   }
   const bool det = P.deterministic != 0;
   const int KS = d.k_splits;
+  const int np = P.npeer > 1 ? P.npeer : 1;
+  if (np > 1 && tid < np) {
+    // this linear's y destinations (the row-sharded ranks' copies of y) -> shared memory
+    const uint64_t yp = reinterpret_cast<uint64_t>(P.ypeer[static_cast<size_t>(d.slot) * kMaxPeers + tid]);
+    sts2(C.S.misc + 4u * (M_PEER + 2 * tid), static_cast<uint32_t>(yp), static_cast<uint32_t>(yp >> 32));
+  }
   if (KS > 1 && !det) {
     const int y0 = part(d.m, b, NB), y1 = part(d.m, b + 1, NB);
-    for (int i = y0 + tid; i < y1; i += kThreads) d.y[i] = 0.f;
+    for (int p = 0; p < np; ++p) {
+      float* yd = np > 1 ? P.ypeer[static_cast<size_t>(d.slot) * kMaxPeers + p] : d.y;
+      for (int i = y0 + tid; i < y1; i += kThreads) yd[i] = 0.f;
+    }
   }
   {
     // The next launch's t buffer of this slot is zeroed by EVERY launch that
@@ -682,7 +691,17 @@ __device__ __forceinline__ void run_linear(const StackParams& P, const LinDesc& 
   const int NG = G2;
   __syncthreads();
   const int tcw = tw * VE;  // floats in this tile (multiple of 4)
-  const bool y16 = (reinterpret_cast<uintptr_t>(d.y) & 15u) == 0;
+  // y destinations: the descriptor's y, or (row-sharded stacks) every rank's
+  // copy of the full y at this shard's rows -- the all-gather done by the
+  // stores themselves
+  const int np = P.npeer > 1 ? P.npeer : 1;
+  auto ydst = [&](int p) -> float* {
+    if (np == 1) return d.y;
+    const uint2 u = lds2(S.misc + 4u * (M_PEER + 2 * p));
+    return reinterpret_cast<float*>(static_cast<uint64_t>(u.x) | (static_cast<uint64_t>(u.y) << 32));
+  };
+  bool y16 = true;
+  for (int p = 0; p < np; ++p) y16 = y16 && (reinterpret_cast<uintptr_t>(ydst(p)) & 15u) == 0;
   for (int q = tid; q < tcw / 4; q += kThreads) {
     float s4[4] = {0.f, 0.f, 0.f, 0.f};
     for (int g = 0; g < NG; ++g) {
@@ -698,13 +717,19 @@ __device__ __forceinline__ void run_linear(const StackParams& P, const LinDesc& 
       *reinterpret_cast<float4*>(P.y_part + static_cast<size_t>(ks) * d.m_pad + col) =
           make_float4(s4[0], s4[1], s4[2], s4[3]);
     } else if (KS > 1) {
-      if (y16 && col + 3 < d.m) {
-        red_add_v4(d.y + col, s4[0], s4[1], s4[2], s4[3]);
-      } else {
-        for (int e = 0; e < 4 && col + e < d.m; ++e) red_add_f32(d.y + col + e, s4[e]);
+      for (int p = 0; p < np; ++p) {
+        float* yd = ydst(p);
+        if (y16 && col + 3 < d.m) {
+          red_add_v4(yd + col, s4[0], s4[1], s4[2], s4[3]);
+        } else {
+          for (int e = 0; e < 4 && col + e < d.m; ++e) red_add_f32(yd + col + e, s4[e]);
+        }
       }
     } else {
-      for (int e = 0; e < 4 && col + e < d.m; ++e) d.y[col + e] = s4[e];
+      for (int p = 0; p < np; ++p) {
+        float* yd = ydst(p);
+        for (int e = 0; e < 4 && col + e < d.m; ++e) yd[col + e] = s4[e];
+      }
     }
   }
   if (KS > 1 && det) {
@@ -721,7 +746,7 @@ __device__ __forceinline__ void run_linear(const StackParams& P, const LinDesc& 
         float sum = 0.f;
 #pragma unroll 4
         for (int kk = 0; kk < KS; ++kk) sum += __ldcg(P.y_part + static_cast<size_t>(kk) * d.m_pad + col);
-        d.y[col] = sum;
+        for (int p = 0; p < np; ++p) ydst(p)[col] = sum;
       }
       if (tid == 0) st_relaxed_gpu(ticket, 0u);
     }

@@ -42,7 +42,7 @@ namespace rsp {
 constexpr int kBins = 4096;   // level-1 histogram: key bits 30..19 (exponent + 4 mantissa bits)
 constexpr int kH16Words = 16384;  // 32768 bf16 keys x 16-bit counters (n <= 65535)
 constexpr int kCandWords = 2048;  // gathered boundary-bin members (more: refine over all of x)
-constexpr int kMiscWords = 208;
+constexpr int kMiscWords = 224;
 
 // misc[] word slots
 enum : int {
@@ -59,6 +59,7 @@ enum : int {
   M_PLAN1 = 128,  // [128, 152): plan slot 1
   M_DESC0 = 160,  // [160, 184): staged linear descriptor, slot 0
   M_DESC1 = 184,  // [184, 208): slot 1
+  M_PEER = 208,   // [208, 224): the stack kernel's y destinations of the current linear (8 pointers)
 };
 
 struct Cut {

@@ -428,7 +428,11 @@ class Stack:
     and overlap with it."""
 
     def __init__(self, layers: List[DecomposedLayer], xs, ys, dense: bool = False,
-                 wait_prev: Optional[Sequence[bool]] = None, silu_gate: Optional[Sequence[bool]] = None):
+                 wait_prev: Optional[Sequence[bool]] = None, silu_gate: Optional[Sequence[bool]] = None,
+                 y_peers: Optional[Sequence[Sequence]] = None):
+        """y_peers[i] (optional): the destinations of linear i's output rows --
+        every rank's copy of the full y at this shard's first row (tensors or
+        device pointers); the kernel writes all of them (rsp_stack_create_spec)."""
         self.layers = layers
         self.xs, self.ys = xs, ys
         n = len(layers)
@@ -448,8 +452,23 @@ class Stack:
             ops = (ct.c_uint8 * n)(*[L.RSP_XOP_SILU_GATE if g else L.RSP_XOP_NONE for g in silu_gate])
         h = ct.c_void_p()
         torch.cuda.synchronize()
-        check(L.lib().rsp_stack_create_ops(hp, n, xp, _x_dtype(xs[0]), yp, 1 if dense else 0, wp, ops, ct.byref(h)),
-              "rsp_stack_create_ops")
+        if y_peers is None:
+            check(L.lib().rsp_stack_create_ops(hp, n, xp, _x_dtype(xs[0]), yp, 1 if dense else 0, wp, ops,
+                                               ct.byref(h)), "rsp_stack_create_ops")
+        else:
+            npeer = len(y_peers[0])
+            if len(y_peers) != n or any(len(p) != npeer for p in y_peers):
+                raise L.UsageError(L.RSP_E_USAGE, "y_peers needs the same number of destinations for every linear")
+            ptrs = [(t.data_ptr() if hasattr(t, "data_ptr") else int(t)) for pl in y_peers for t in pl]
+            self._peers = y_peers
+            sp = L.StackSpec()
+            sp.layers, sp.count, sp.x_devs, sp.x_dtype, sp.y_devs = hp, n, xp, _x_dtype(xs[0]), yp
+            sp.dense = 1 if dense else 0
+            sp.wait_prev = ct.cast(wp, ct.POINTER(ct.c_uint8)) if wp is not None else None
+            sp.x_ops = ct.cast(ops, ct.POINTER(ct.c_uint8)) if ops is not None else None
+            sp.npeer = npeer
+            sp.y_peers = (ct.c_void_p * len(ptrs))(*ptrs)
+            check(L.lib().rsp_stack_create_spec(ct.byref(sp), ct.byref(h)), "rsp_stack_create_spec")
         self._h = h
 
     def launch(self, stream=None) -> None:
