@@ -284,6 +284,9 @@ typedef struct rsp_stack_spec {
   const uint8_t* x_ops;      /* may be NULL: RSP_XOP_NONE */
   uint32_t npeer;            /* 0 or 1: y_devs only; 2..8: y_peers */
   float* const* y_peers;     /* count x npeer destinations (npeer > 1) */
+  uint32_t max_ctas;         /* 0: one CTA per SM; else at most this many CTAs (one per SM), so
+                                that independent stacks -- e.g. the B tokens of a small batch,
+                                SPEC.md:331 -- run concurrently on disjoint SMs */
 } rsp_stack_spec;
 rsp_status rsp_stack_create_spec(const rsp_stack_spec* spec, rsp_stack** out);
 rsp_status rsp_stack_launch(rsp_stack* s, void* stream);

@@ -70,7 +70,7 @@ class StackSpec(ct.Structure):
         ("layers", ct.POINTER(ct.c_void_p)), ("count", ct.c_uint32), ("x_devs", ct.POINTER(ct.c_void_p)),
         ("x_dtype", ct.c_int), ("y_devs", ct.POINTER(ct.c_void_p)), ("dense", ct.c_int),
         ("wait_prev", ct.POINTER(ct.c_uint8)), ("x_ops", ct.POINTER(ct.c_uint8)), ("npeer", ct.c_uint32),
-        ("y_peers", ct.POINTER(ct.c_void_p)),
+        ("y_peers", ct.POINTER(ct.c_void_p)), ("max_ctas", ct.c_uint32),
     ]
 
 

@@ -1064,7 +1064,10 @@ rsp_status rsp_stack_create_spec(const rsp_stack_spec* spec, rsp_stack** out) {
       tot += bytes[i - g0];
     }
     int cta0 = 0;
-    const int sms = std::max(1, dpx.sms);
+    // CTA budget of the whole launch: the device's SMs, or fewer (spec.max_ctas)
+    // so that several stacks -- e.g. the tokens of a small batch -- run side
+    // by side on disjoint SMs
+    const int sms = std::max(1, spec->max_ctas ? std::min(dpx.sms, static_cast<int>(spec->max_ctas)) : dpx.sms);
     for (uint32_t i = g0; i < g1; ++i) {
       int budget = g1 - g0 == 1 ? sms
                                 : std::max(1, static_cast<int>(std::floor(sms * bytes[i - g0] / std::max(tot, 1.0))));

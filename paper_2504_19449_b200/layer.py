@@ -429,7 +429,7 @@ class Stack:
 
     def __init__(self, layers: List[DecomposedLayer], xs, ys, dense: bool = False,
                  wait_prev: Optional[Sequence[bool]] = None, silu_gate: Optional[Sequence[bool]] = None,
-                 y_peers: Optional[Sequence[Sequence]] = None):
+                 y_peers: Optional[Sequence[Sequence]] = None, max_ctas: int = 0):
         """y_peers[i] (optional): the destinations of linear i's output rows --
         every rank's copy of the full y at this shard's first row (tensors or
         device pointers); the kernel writes all of them (rsp_stack_create_spec)."""
@@ -452,27 +452,31 @@ class Stack:
             ops = (ct.c_uint8 * n)(*[L.RSP_XOP_SILU_GATE if g else L.RSP_XOP_NONE for g in silu_gate])
         h = ct.c_void_p()
         torch.cuda.synchronize()
-        if y_peers is None:
+        if y_peers is None and not max_ctas:
             check(L.lib().rsp_stack_create_ops(hp, n, xp, _x_dtype(xs[0]), yp, 1 if dense else 0, wp, ops,
                                                ct.byref(h)), "rsp_stack_create_ops")
         else:
-            npeer = len(y_peers[0])
-            if len(y_peers) != n or any(len(p) != npeer for p in y_peers):
+            npeer = len(y_peers[0]) if y_peers is not None else 1
+            if y_peers is not None and (len(y_peers) != n or any(len(p) != npeer for p in y_peers)):
                 raise L.UsageError(L.RSP_E_USAGE, "y_peers needs the same number of destinations for every linear")
-            ptrs = [(t.data_ptr() if hasattr(t, "data_ptr") else int(t)) for pl in y_peers for t in pl]
+            ptrs = [(t.data_ptr() if hasattr(t, "data_ptr") else int(t)) for pl in (y_peers or []) for t in pl]
             self._peers = y_peers
             sp = L.StackSpec()
+            sp.max_ctas = int(max_ctas)
             sp.layers, sp.count, sp.x_devs, sp.x_dtype, sp.y_devs = hp, n, xp, _x_dtype(xs[0]), yp
             sp.dense = 1 if dense else 0
             sp.wait_prev = ct.cast(wp, ct.POINTER(ct.c_uint8)) if wp is not None else None
             sp.x_ops = ct.cast(ops, ct.POINTER(ct.c_uint8)) if ops is not None else None
             sp.npeer = npeer
-            sp.y_peers = (ct.c_void_p * len(ptrs))(*ptrs)
+            sp.y_peers = (ct.c_void_p * len(ptrs))(*ptrs) if ptrs else None
             check(L.lib().rsp_stack_create_spec(ct.byref(sp), ct.byref(h)), "rsp_stack_create_spec")
         self._h = h
 
     def launch(self, stream=None) -> None:
         check(L.lib().rsp_stack_launch(self._h, _stream_ptr(stream)), "rsp_stack_launch")
+
+    def info(self):
+        return {"handle": self._h.value}
 
     def io_spans(self):
         """(x_bytes, y_bytes): the device spans covering all inputs / outputs."""
@@ -499,3 +503,59 @@ class Stack:
             self.close()
         except Exception:
             pass
+
+
+class TokenParallelStack:
+    """A decode stack over a small batch of B tokens as B independent
+    persistent stack launches on disjoint SM partitions (max_ctas = SMs / B),
+    forked onto B streams and joined -- captured into one CUDA graph.  The
+    reference semantics of a batch (B independent forward
+    calls) taken literally: each token keeps its own selection; the
+    per-dependency-step fixed costs of the B tokens overlap instead of adding
+    up.  xs[i] / ys[i] are (B, m_in) / (B, m_out) per linear."""
+
+    def __init__(self, layers: List[DecomposedLayer], xs, ys, wait_prev: Optional[Sequence[bool]] = None,
+                 stream=None):
+        self.B = int(xs[0].shape[0])
+        dev = xs[0].device
+        sms = int(L.lib().rsp_device_sm_count(dev.index or 0))
+        self.stacks = [Stack(layers, [x[b] for x in xs], [y[b] for y in ys], wait_prev=wait_prev,
+                             max_ctas=max(1, sms // self.B)) for b in range(self.B)]
+        self.stream = stream or torch.cuda.current_stream(dev)
+        self.side = [torch.cuda.Stream(device=dev) for _ in range(self.B)]
+        self.graph = None
+        with torch.cuda.stream(self.stream):
+            self._run()
+            torch.cuda.synchronize()
+            try:  # graph launches inside a capture (else: eager fork/join per step)
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=self.stream):
+                    self._run()
+                self.graph = g
+            except RuntimeError:
+                torch.cuda.synchronize()
+
+    def _run(self):
+        fork = torch.cuda.Event()
+        fork.record(self.stream)
+        joins = []
+        for st, sd in zip(self.stacks, self.side):
+            sd.wait_event(fork)
+            st.launch(sd)
+            ev = torch.cuda.Event()
+            ev.record(sd)
+            joins.append(ev)
+        for ev in joins:
+            self.stream.wait_event(ev)
+
+    def launch(self, stream=None) -> None:
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            with torch.cuda.stream(self.stream):
+                self._run()
+
+    def close(self) -> None:
+        for st in self.stacks:
+            st.close()
+

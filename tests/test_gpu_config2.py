@@ -190,3 +190,32 @@ def test_stack_launch_host_matches_device_launch(cuda):
         import ctypes as ct
         from paper_2504_19449_b200 import _lib as L
         L.check(L.lib().rsp_stack_launch_host(st._h, x_host.data_ptr(), 2, y_host.data_ptr(), 4, None))
+
+
+def test_token_parallel_stack_matches_per_token(cuda):
+    """TokenParallelStack: B tokens as B persistent stacks on disjoint SM
+    partitions (rsp_stack_spec.max_ctas) -- each token's outputs equal its
+    own batch-1 forward."""
+    rng = np.random.default_rng(12)
+    shapes = [("layers.0.q_proj", 1024, 512, 0.3, 48), ("layers.0.k_proj", 512, 512, 0.25, 32),
+              ("layers.0.o_proj", 512, 512, 0.2, 40), ("layers.0.down_proj", 512, 1024, 0.35, 64)]
+    gid, wait = wl.input_groups(shapes)
+    layers = [rsp.DecomposedLayer(torch.randn(m, n, device=cuda) * 0.05, torch.randn(m, r, device=cuda) * 0.1,
+                                  torch.randn(r, n, device=cuda) * 0.1, rsp.SparsityPlan(s, r))
+              for (_, m, n, s, r) in shapes]
+    for B in (2, 3):
+        X = {}
+        for i, (name, m, n, s, r) in enumerate(shapes):
+            if gid[i] not in X:
+                X[gid[i]] = torch.from_numpy(np.stack([wl.heavy_tailed_x(n, rng) for _ in range(B)])).to(cuda).to(
+                    torch.bfloat16)
+        xs = [X[gid[i]] for i in range(len(shapes))]
+        ys = [torch.zeros((B, l.m_out), device=cuda) for l in layers]
+        tp = rsp.TokenParallelStack(layers, xs, ys, wait_prev=wait)
+        for _ in range(2):
+            tp.launch()
+        torch.cuda.synchronize()
+        for l, x, y in zip(layers, xs, ys):
+            for b in range(B):
+                assert maxrel(y[b].cpu().numpy(), l.forward(x[b]).cpu().numpy()) <= 1e-6
+        tp.close()

@@ -91,6 +91,15 @@ def main():
                 ms = time_graph(lambda: st.launch(stream), a.steps, a.warmup, stream)
                 res["stack_us_per_token"] = ms * 1e3
                 st.close()
+            if 1 < B <= 4:
+                # B independent per-token persistent stacks on disjoint SM partitions
+                tp = rsp.TokenParallelStack(layers, [xs[gid[i]] for i in range(len(layers))], ys, wait_prev=wait,
+                                            stream=stream)
+                ms = time_graph(lambda: tp.launch(stream), a.steps, a.warmup, stream)
+                res["token_parallel_us_per_token"] = ms * 1e3 / B
+                res["token_parallel_graph"] = tp.graph is not None
+                tp.close()
+
             def step():
                 for i, l in enumerate(layers):
                     l.forward(xs[gid[i]] if B > 1 else xs[gid[i]][0], out=ys[i] if B > 1 else ys[i][0],
@@ -116,7 +125,8 @@ def main():
             ms = time_graph(lambda: g2.replay(), a.steps, a.warmup, stream)
             res["dense_cublas_us_per_token"] = ms * 1e3 / B
             del g2
-        best = min(v for k, v in res.items() if k in ("stack_us_per_token", "per_linear_us_per_token"))
+        best = min(v for k, v in res.items()
+                   if k in ("stack_us_per_token", "per_linear_us_per_token", "token_parallel_us_per_token"))
         res["speedup_vs_dense_cublas"] = res["dense_cublas_us_per_token"] / best
         print(json.dumps(res), flush=True)
         del ys, xs
