@@ -39,12 +39,35 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
 
 #include "rsp_device.cuh"
 #include "rsp_internal.h"
 #include "rsp_select.cuh"
 
 namespace rsp {
+
+// Debug build (tools/gpu_debugchecks.sh: -DRSP_DEBUG_CHECKS=1): device-side
+// bounds checks on the shared-memory carve-up, the plan and the workspace
+// indices; a violated check traps (the sanitizers are not available on the
+// GPU pool).  Compiled out of the product build.
+#ifndef RSP_DEBUG_CHECKS
+#define RSP_DEBUG_CHECKS 0
+#endif
+#if RSP_DEBUG_CHECKS
+#define RSP_CHECK(cond)                                                                    \
+  do {                                                                                     \
+    if (!(cond)) {                                                                         \
+      printf("RSP_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__, \
+             static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x));                 \
+      __trap();                                                                            \
+    }                                                                                      \
+  } while (0)
+#else
+#define RSP_CHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
 
 constexpr int kU = 16;              // rows in flight per warp
 constexpr int kUA = 8;              // A_r^T rows per warp loaded ahead of the barrier wait
@@ -530,6 +553,12 @@ __device__ __forceinline__ void run_linear(const StackParams& P, const LinDesc& 
   }
   RSP_TRACE(4);
   if (trace && tid == 0) trace[15] = nW | (static_cast<long long>(nU) << 32);  // debug: this CTA's row counts
+  // list capacities, the plan's tile and A rows, the t buffer, the A-copy area
+  RSP_CHECK(nW >= 0 && nW <= P.cap_w && nU >= 0 && nU <= P.cap_u && na >= 0 && na <= P.cap_a);
+  RSP_CHECK(v0 >= 0 && tw >= 0 && v0 + tw <= d.m_pad * ES / 16 && alo + na <= d.r);
+  RSP_CHECK(uc0 >= 0 && uc0 <= uc1 && uc1 <= d.n && cp.wc0 >= 0 && cp.wc1 <= d.n);
+  RSP_CHECK(d.r_pad <= static_cast<int>(kTAccCap) && d.n <= P.n_max);
+  RSP_CHECK(na_s <= na && na_s * tw * 16 <= C.acap);
   const bool acp = (cp.flags & kPlanACp) != 0;
   // A_r^T tile rows [0, na_s) -> the histogram area (row-major, tw units per
   // row), issued by each warp inside its W stream (side job)
