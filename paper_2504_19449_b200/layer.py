@@ -523,17 +523,14 @@ class TokenParallelStack:
                              max_ctas=max(1, sms // self.B)) for b in range(self.B)]
         self.stream = stream or torch.cuda.current_stream(dev)
         self.side = [torch.cuda.Stream(device=dev) for _ in range(self.B)]
+        # each stack is already one CUDA graph; the fork/join around them is
+        # B+1 event records per step (a torch capture of graph launches is not
+        # supported by this runtime, and a failed capture leaves torch's CUDA
+        # RNG state unusable)
         self.graph = None
         with torch.cuda.stream(self.stream):
             self._run()
             torch.cuda.synchronize()
-            try:  # graph launches inside a capture (else: eager fork/join per step)
-                g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g, stream=self.stream):
-                    self._run()
-                self.graph = g
-            except RuntimeError:
-                torch.cuda.synchronize()
 
     def _run(self):
         fork = torch.cuda.Event()
