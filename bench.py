@@ -257,8 +257,11 @@ def cpu_reference_leg(plans, threads, seconds=None, warmup=1, passes=None, layer
     for (name, m, n) in REF_SHAPES:
         g = REF_GROUP[name]
         if g not in xs:
-            x = (rng.standard_normal(n) / (1 + np.exp(-rng.standard_normal(n)))) if name == "down_proj" else \
-                rng.laplace(size=n) * rng.lognormal(size=n)
+            if name == "down_proj":  # SiLU(g) * u, g, u ~ N(0, 1) (model.cpp:122-126)
+                g, u = rng.standard_normal(n), rng.standard_normal(n)
+                x = g / (1 + np.exp(-g)) * u
+            else:  # heavy-tailed (Laplace x LogNormal)
+                x = rng.laplace(size=n) * rng.lognormal(size=n)
             xs[g] = np.ascontiguousarray(x, dtype=np.float64)
     # decoder layers stay resident across passes when host memory allows
     # (~2 GB of fp64 per layer); otherwise each layer is rebuilt per pass
