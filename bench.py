@@ -258,8 +258,8 @@ def cpu_reference_leg(plans, threads, seconds=None, warmup=1, passes=None, layer
         g = REF_GROUP[name]
         if g not in xs:
             if name == "down_proj":  # SiLU(g) * u, g, u ~ N(0, 1) (model.cpp:122-126)
-                g, u = rng.standard_normal(n), rng.standard_normal(n)
-                x = g / (1 + np.exp(-g)) * u
+                gz, uz = rng.standard_normal(n), rng.standard_normal(n)
+                x = gz / (1 + np.exp(-gz)) * uz
             else:  # heavy-tailed (Laplace x LogNormal)
                 x = rng.laplace(size=n) * rng.lognormal(size=n)
             xs[g] = np.ascontiguousarray(x, dtype=np.float64)
