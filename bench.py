@@ -152,14 +152,24 @@ def build_stack(rsp, wl, plans, rank, world, dev, torch, deterministic=False):
     return layers, xs_host, gid, wait
 
 
-def kernel_bytes(layers):
+def algorithmic_bytes(layers):
     """Algorithmic bytes per step (SURVEY §8(d) model, this rank's shards):
-    elem*(k*m + (n-k)*r + r*m) + x + y, summed over the stack."""
+    elem*(k*m + (n-k)*r + r*m) + x + y with padded widths, summed over the
+    stack -- the S^c rows of b_r only, whatever the kernel actually reads."""
     tot = 0
     for l in layers:
-        rep = l.io_cost()
-        tot += rep.kernel_total_bytes
+        info = l.info
+        m, n, k, r = info["m_pad"], info["m_in"], info["k"], info["rank"]
+        rp = info["r_pad"]
+        lr = r > 0 and k < n
+        tot += 2 * (k * m + ((n - k) * rp + r * m if lr else 0)) + 4 * n + 4 * (info["row_end"] - info["row_begin"])
     return tot
+
+
+def kernel_bytes(layers):
+    """Bytes the kernels read per step (rsp_linear_io_cost: the residual form
+    of bf16 layers reads every row of b_r^T, n r instead of (n - k) r)."""
+    return sum(l.io_cost().kernel_total_bytes for l in layers)
 
 
 def time_graph(torch, launch, steps, warmup, stream, barrier=None):
@@ -420,7 +430,8 @@ def run_ours(args):
         ms_step = float(t.item())
     us_token = ms_step * 1e3
 
-    bytes_step = kernel_bytes(layers)  # this rank's algorithmic bytes
+    bytes_step = algorithmic_bytes(layers)  # this rank's algorithmic bytes (SURVEY model)
+    kbytes_step = kernel_bytes(layers)
     hbm_peak, peak_kind = measured_peaks()
     achieved = bytes_step / (ms_step * 1e-3) / 1e9
 
@@ -472,6 +483,7 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": None if sharded else load_traffic(),
                      "peak_kind": peak_kind, "algorithmic_bytes_per_step": bytes_step,
+                     "kernel_bytes_per_step": kbytes_step,
                      "kernel": ("stack_kernel<bf16,bf16> (1 launch per input group, + NCCL all-gather of y)" if sharded
                                 else "stack_kernel<bf16,bf16> (1 persistent launch/step, 224 linears)")},
         "e2e": {"value": e2e_ms * 1e3, "unit": "us/token", "h2d_bytes_per_step": h2d,

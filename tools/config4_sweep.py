@@ -70,7 +70,11 @@ def main():
             ys = [torch.empty(l.m_out, device=dev) for l in layers]
             st = rsp.Stack(layers, [xs[gid[i]] for i in range(len(layers))], ys, wait_prev=wait)
             ms = timed(lambda: st.launch(), a.steps, a.warmup)
-            alg = sum(l.io_cost().kernel_total_bytes for l in layers)
+            import importlib.util as _iu
+            _spec = _iu.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+            _bm = _iu.module_from_spec(_spec)
+            _spec.loader.exec_module(_bm)
+            alg = _bm.algorithmic_bytes(layers)  # SURVEY 8(d) model (S^c rows of b_r)
             ref = sum(l.io_cost().touched_bytes for l in layers)
             dense = sum(2 * m * n for (_, m, n, _, _) in plans)
             res = {"config": "config4", "sparsity": sp, "rank": rank, "layers": a.layers, "us_per_token": ms * 1e3,

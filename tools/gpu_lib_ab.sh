@@ -2,7 +2,7 @@
 # A/B of the default build against librsparse_b200_base.so (the previous kernel, built with
 # RSP_NVCC_EXTRA), after the default build's parity tests; then a phase trace of the default build.
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_config2.py tests/test_gpu_parity.py tests/test_gpu_exchange.py tests/test_model.py -m gpu -x -q -k "stack or config2 or exchange or forward or model or mlp" -p no:cacheprovider > gpurun_out/ab_pytest.txt 2>&1
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/ab_pytest.txt 2>&1
 tail -2 gpurun_out/ab_pytest.txt
 for rep in 1 2; do
   for v in new base; do
