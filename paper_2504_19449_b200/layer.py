@@ -556,3 +556,60 @@ class TokenParallelStack:
         for st in self.stacks:
             st.close()
 
+
+
+class BatchedStack:
+    """A decode stack over a batch of B tokens (xs[i]: (B, m_in), ys[i]:
+    (B, m_out)) with the executor chosen by B (profiles/r02_config3_*):
+
+    * B == 1: the persistent stack kernel (:class:`Stack`);
+    * 2 <= B <= TOKEN_PARALLEL_MAX: B concurrent per-token stacks on disjoint
+      SM partitions (:class:`TokenParallelStack`);
+    * larger B: the union-of-masks pass per linear (rsp_linear_forward with
+      batch = B: each W row of the tokens' union read once), captured into one
+      CUDA graph.
+
+    Every token keeps its own selection (the reference's batch semantics,
+    SPEC.md:325, 331)."""
+
+    TOKEN_PARALLEL_MAX = 5  # measured crossover: B = 5 1.33 vs 1.39 ms, B = 6 1.25 vs 1.17 (token-parallel vs union)
+
+    def __init__(self, layers: List[DecomposedLayer], xs, ys, wait_prev: Optional[Sequence[bool]] = None,
+                 stream=None):
+        self.B = int(xs[0].shape[0])
+        self.stream = stream or torch.cuda.current_stream(xs[0].device)
+        self.graph = None
+        if self.B == 1:
+            self.mode = "persistent"
+            self.impl = Stack(layers, [x[0] for x in xs], [y[0] for y in ys], wait_prev=wait_prev)
+        elif self.B <= self.TOKEN_PARALLEL_MAX:
+            self.mode = "token_parallel"
+            self.impl = TokenParallelStack(layers, xs, ys, wait_prev=wait_prev, stream=self.stream)
+        else:
+            self.mode = "union_per_linear"
+            self.impl = None
+            self.layers, self.xs, self.ys = layers, xs, ys
+            self.ws = [l.workspace() for l in layers]
+            with torch.cuda.stream(self.stream):
+                self._run()
+                torch.cuda.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=self.stream):
+                    self._run()
+                self.graph = g
+
+    def _run(self):
+        for l, x, y, ws in zip(self.layers, self.xs, self.ys, self.ws):
+            l.forward(x, out=y, workspace=ws, stream=self.stream)
+
+    def launch(self, stream=None) -> None:
+        if self.graph is not None:
+            self.graph.replay()
+        elif self.mode == "persistent":
+            self.impl.launch(stream or self.stream)
+        else:
+            self.impl.launch()
+
+    def close(self) -> None:
+        if self.impl is not None:
+            self.impl.close()

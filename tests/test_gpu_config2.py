@@ -219,3 +219,32 @@ def test_token_parallel_stack_matches_per_token(cuda):
             for b in range(B):
                 assert maxrel(y[b].cpu().numpy(), l.forward(x[b]).cpu().numpy()) <= 1e-6
         tp.close()
+
+
+@pytest.mark.parametrize("B", [1, 3, 6])
+def test_batched_stack_modes_match_per_token(cuda, B):
+    """BatchedStack: persistent (B = 1), token-parallel (B <= 4), union
+    launches per linear (larger B) -- every token equals its own forward."""
+    rng = np.random.default_rng(20 + B)
+    shapes = [("layers.0.q_proj", 1024, 512, 0.3, 48), ("layers.0.k_proj", 512, 512, 0.25, 32),
+              ("layers.0.o_proj", 512, 512, 0.2, 40)]
+    gid, wait = wl.input_groups(shapes)
+    layers = [rsp.DecomposedLayer(torch.randn(m, n, device=cuda) * 0.05, torch.randn(m, r, device=cuda) * 0.1,
+                                  torch.randn(r, n, device=cuda) * 0.1, rsp.SparsityPlan(s, r))
+              for (_, m, n, s, r) in shapes]
+    X = {}
+    for i, (name, m, n, s, r) in enumerate(shapes):
+        if gid[i] not in X:
+            X[gid[i]] = torch.from_numpy(np.stack([wl.heavy_tailed_x(n, rng) for _ in range(B)])).to(cuda).to(
+                torch.bfloat16)
+    xs = [X[gid[i]] for i in range(len(shapes))]
+    ys = [torch.zeros((B, l.m_out), device=cuda) for l in layers]
+    bs = rsp.BatchedStack(layers, xs, ys, wait_prev=wait)
+    assert bs.mode == ("persistent" if B == 1 else "token_parallel" if B <= 5 else "union_per_linear")
+    for _ in range(2):
+        bs.launch()
+    torch.cuda.synchronize()
+    for l, x, y in zip(layers, xs, ys):
+        for b in range(B):
+            assert maxrel(y[b].cpu().numpy(), l.forward(x[b]).cpu().numpy()) <= 1e-4
+    bs.close()

@@ -91,7 +91,7 @@ def main():
                 ms = time_graph(lambda: st.launch(stream), a.steps, a.warmup, stream)
                 res["stack_us_per_token"] = ms * 1e3
                 st.close()
-            if 1 < B <= 4:
+            if 1 < B <= 8:
                 # B independent per-token persistent stacks on disjoint SM partitions
                 tp = rsp.TokenParallelStack(layers, [xs[gid[i]] for i in range(len(layers))], ys, wait_prev=wait,
                                             stream=stream)
