@@ -479,6 +479,8 @@ def run_ours(args):
                    "combine": "deterministic (fixed-order partials)" if args.deterministic else "float reductions at L2",
                    "sharded_graph": (getattr(st, "graph", None) is not None) if sharded else None,
                    "l2": "no flush: 16 GB resident operands >> 126 MB L2",
+                   "activations": "pre-filled synthetic x per input group; stack dependencies (wait_prev) keep "
+                                  "the decoder-layer order but y is not fed forward (model.DecodeBlock does that)",
                    "step_ms_p10_p50_p90": [float(np.percentile(per, q)) for q in (10, 50, 90)]},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": None if sharded else load_traffic(),

@@ -866,7 +866,10 @@ cudaError_t launch_batch(const BatchParams& p, bool x_bf16, cudaStream_t stream)
   const size_t smem = batch_smem_bytes(p);
   cudaError_t e = cudaFuncSetAttribute(batch_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
-  if (e != cudaSuccess) return e;
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    return e;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p.grid);
   cfg.blockDim = dim3(kThreads);

@@ -973,6 +973,7 @@ cudaError_t stack_set_smem(size_t smem) {
   RSP_SET(float, true)
   RSP_SET(float, false)
 #undef RSP_SET
+  if (e != cudaSuccess) (void)cudaGetLastError();  // do not leave the failure pending for a later launch
   return e;
 }
 
