@@ -132,7 +132,12 @@ rsp_status rsp_shard_rows(uint32_t m_out, uint32_t shard_rank, uint32_t shard_co
 /* -- operator -------------------------------------------------------------- */
 /* Replaces building a rsparse::DecomposedLayer (decompose_with_svd,
  * layer.cpp:35-68, with the factors precomputed on the host).  Uploads W in
- * input-channel-major layout Wt[m_in][m_pad], A_r^T[r][m_pad], B_r^T[m_in][r_pad]. */
+ * input-channel-major layout Wt[m_in][m_pad], A_r^T[r][m_pad], B_r^T[m_in][r_pad].
+ * Limits of this implementation (RSP_E_UNSUPPORTED, the reference has none):
+ * m_in <= 32768 (selection keeps x on chip); one B_r^T row <= 4 KB, i.e.
+ * rank <= 2048 with bf16 weights and <= 1024 with fp32 weights (stage-1 t
+ * lives in shared memory).  Above rank m*n/(m+n) the factors outweigh W, so
+ * the limit only excludes plans slower than the dense GEMV. */
 rsp_status rsp_linear_create(const rsp_linear_desc* desc, rsp_linear** out);
 void rsp_linear_destroy(rsp_linear* h);
 rsp_status rsp_linear_info_get(const rsp_linear* h, rsp_linear_info* out);

@@ -590,21 +590,25 @@ class BatchedStack:
             self.impl = None
             self.layers, self.xs, self.ys = layers, xs, ys
             self.ws = [l.workspace() for l in layers]
-            with torch.cuda.stream(self.stream):
-                self._run()
-                torch.cuda.synchronize()
-                g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g, stream=self.stream):
-                    self._run()
-                self.graph = g
+            # captured on a private stream (a capture cannot run on the
+            # legacy default stream), replayed on self.stream
+            cap = torch.cuda.Stream(device=xs[0].device)
+            cap.wait_stream(self.stream)
+            self._run(cap)
+            cap.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=cap):
+                self._run(cap)
+            self.graph = g
 
-    def _run(self):
+    def _run(self, stream):
         for l, x, y, ws in zip(self.layers, self.xs, self.ys, self.ws):
-            l.forward(x, out=y, workspace=ws, stream=self.stream)
+            l.forward(x, out=y, workspace=ws, stream=stream)
 
     def launch(self, stream=None) -> None:
         if self.graph is not None:
-            self.graph.replay()
+            with torch.cuda.stream(stream or self.stream):
+                self.graph.replay()
         elif self.mode == "persistent":
             self.impl.launch(stream or self.stream)
         else:

@@ -1,0 +1,112 @@
+"""Seeded random sweeps of the sm_100a path against the oracle.
+
+The fixed-shape parity tests (test_gpu_parity.py, test_gpu_config2.py) pin
+the reference's configurations; these sweeps draw shapes, ranks, keep
+fractions, dtypes and activation distributions at random so that the
+planner's partitions (k-splits, CTA groups, the C1 stage-1 warp maps, the
+list capacities) are hit in combinations no hand-written case names.  Every
+case is checked the same way as the parity suite: the selected set
+bit-exact and y within TOL_EXACT_INPUTS of the oracle run on the values the
+device holds (rsparse::forward, layer.cpp:95-123).
+"""
+import numpy as np
+import pytest
+import torch
+
+import paper_2504_19449_b200 as rsp
+from paper_2504_19449_b200 import workloads as wl
+from paper_2504_19449_b200._lib import RSP_E_UNSUPPORTED
+
+from test_gpu_parity import TOL_EXACT_INPUTS, maxrel, oracle_on_device_values
+
+pytestmark = pytest.mark.gpu
+
+
+def random_x(rng, n):
+    """One of several activation distributions, ties and zeros included."""
+    kind = rng.integers(0, 5)
+    if kind == 0:
+        x = wl.heavy_tailed_x(n, rng, outliers=min(8, n))
+    elif kind == 1:
+        x = rng.standard_normal(n)
+    elif kind == 2:  # coarse levels: many exact ties in |x|, resolved by lower index
+        x = np.round(rng.standard_normal(n) * 2.0) / 2.0
+    elif kind == 3:  # mostly zeros
+        x = rng.standard_normal(n) * (rng.random(n) < 0.2)
+    else:
+        x = wl.silu_gate_x(n, rng)
+    return np.asarray(x, np.float32)
+
+
+def random_linear(rng, cuda, wdt, m=None, n=None, det=None):
+    m = int(m or rng.integers(1, 9000))
+    n = int(n or rng.integers(1, 9000))
+    # B_r^T rows of at most 4 KB (rsp_linear_create's documented limit)
+    r_max = 2048 if wdt == "bf16" else 1024
+    r = int(min(m, n, r_max, rng.choice([0, 1, 7, 64, 255, 256, 513, 1024, 1025, 1100, 2048])))
+    s = float(rng.choice([0.0, 1.0, rng.random(), rng.random(), rng.random()]))
+    w = torch.randn(m, n, device=cuda) * 0.02
+    a = torch.randn(m, r, device=cuda) * 0.1
+    b = torch.randn(r, n, device=cuda) * 0.1
+    if det is None:
+        det = bool(rng.random() < 0.2)
+    return rsp.DecomposedLayer(w, a, b, rsp.SparsityPlan(s, r), weight_dtype=wdt, deterministic=det)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_forward_random_configs(coracle, cuda, seed):
+    rng = np.random.default_rng(1000 + seed)
+    for _ in range(8):
+        wdt = str(rng.choice(["f32", "bf16"]))
+        xdt = str(rng.choice(["f32", "bf16"]))
+        layer = random_linear(rng, cuda, wdt)
+        xt = torch.from_numpy(random_x(rng, layer.m_in)).to(cuda)
+        xt = xt.to(torch.bfloat16) if xdt == "bf16" else xt
+        y = layer.forward(xt).cpu().numpy()
+        yo, kept, _ = oracle_on_device_values(coracle, layer, xt)
+        tag = (layer.m_out, layer.m_in, layer.plan.rank, layer.plan.keep_fraction, wdt, xdt)
+        assert np.array_equal(layer.selected(xt), kept), tag
+        assert maxrel(y, yo) <= TOL_EXACT_INPUTS, (tag, maxrel(y, yo))
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_stack_random_configs(coracle, cuda, seed):
+    """A random persistent stack: random shapes, ranks and keep fractions,
+    random sharing of inputs (wait_prev False) and dependencies."""
+    rng = np.random.default_rng(2000 + seed)
+    wdt, xdt = [("bf16", "bf16"), ("f32", "f32"), ("bf16", "f32"), ("f32", "bf16")][seed]
+    count = int(rng.integers(5, 13))
+    det = seed == 3  # a stack runs in one combine mode (rsp_stack_create rejects a mix)
+    layers, xs, wait = [], [], []
+    for i in range(count):
+        share = i > 0 and rng.random() < 0.35
+        n = layers[-1].m_in if share else None
+        layers.append(random_linear(rng, cuda, wdt, n=n, det=det))
+        if share:
+            xs.append(xs[-1])
+        else:
+            xt = torch.from_numpy(random_x(rng, layers[-1].m_in)).to(cuda)
+            xs.append(xt.to(torch.bfloat16) if xdt == "bf16" else xt)
+        wait.append(not share)
+    ys = [torch.full((l.m_out,), float("nan"), device=cuda) for l in layers]
+    st = rsp.Stack(layers, xs, ys, wait_prev=wait)
+    for _ in range(2):
+        st.launch()
+    torch.cuda.synchronize()
+    for i, (l, x, y) in enumerate(zip(layers, xs, ys)):
+        yo, _, _ = oracle_on_device_values(coracle, l, x)
+        got = y.cpu().numpy()
+        assert np.isfinite(got).all(), i
+        assert maxrel(got, yo) <= TOL_EXACT_INPUTS, (i, l.m_out, l.m_in, l.plan.rank, maxrel(got, yo))
+
+
+def test_rank_limit_is_unsupported_not_wrong(cuda):
+    """Ranks whose B_r^T row exceeds 4 KB are refused at create time with
+    RSP_E_UNSUPPORTED (documented in rsp_linear_create), never run."""
+    m, n = 2100, 2100
+    for wdt, r in (("f32", 1025), ("bf16", 2049)):
+        w = torch.randn(m, n, device=cuda)
+        with pytest.raises(rsp.RspError) as e:
+            rsp.DecomposedLayer(w, torch.randn(m, r, device=cuda), torch.randn(r, n, device=cuda),
+                                rsp.SparsityPlan(0.5, r), weight_dtype=wdt)
+        assert e.value.status == RSP_E_UNSUPPORTED
