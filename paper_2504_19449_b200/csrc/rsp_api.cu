@@ -1045,9 +1045,23 @@ rsp_status rsp_stack_create_spec(const rsp_stack_spec* spec, rsp_stack** out) {
   std::vector<LaunchPlan> plans(count);
   std::vector<uint32_t> gstart(count);  // first linear of each linear's group
   uint32_t pg0 = 0, pg1 = 0;  // the previous group
+  // CTA budget of the whole launch: the device's SMs, or fewer (spec.max_ctas)
+  // so that several stacks -- e.g. the tokens of a small batch -- run side
+  // by side on disjoint SMs
+  const int sms = std::max(1, spec->max_ctas ? std::min(dpx.sms, static_cast<int>(spec->max_ctas)) : dpx.sms);
+  // fewest CTAs a linear's column tiling accepts (tiles of <= 8 warp columns)
+  auto min_ctas = [](const rsp_linear* h) {
+    const int wcols = (static_cast<int>(h->m_pad * h->es / 16) + 31) / 32;
+    return std::max(1, (wcols + 7) / 8);
+  };
   for (uint32_t g0 = 0; g0 < count;) {
     uint32_t g1 = g0 + 1;
-    while (g1 < count && !det && wait_prev && !wait_prev[g1]) ++g1;
+    // a group whose members cannot all get their minimum partition at once
+    // is split; the later part then waits for the earlier (stricter order,
+    // same results)
+    int need = min_ctas(layers[g0]);
+    while (g1 < count && !det && wait_prev && !wait_prev[g1] && need + min_ctas(layers[g1]) <= sms)
+      need += min_ctas(layers[g1++]);
     for (uint32_t i = g0; i < g1; ++i) gstart[i] = g0;
     double tot = 0.0;
     std::vector<double> bytes(g1 - g0);
@@ -1064,14 +1078,13 @@ rsp_status rsp_stack_create_spec(const rsp_stack_spec* spec, rsp_stack** out) {
       tot += bytes[i - g0];
     }
     int cta0 = 0;
-    // CTA budget of the whole launch: the device's SMs, or fewer (spec.max_ctas)
-    // so that several stacks -- e.g. the tokens of a small batch -- run side
-    // by side on disjoint SMs
-    const int sms = std::max(1, spec->max_ctas ? std::min(dpx.sms, static_cast<int>(spec->max_ctas)) : dpx.sms);
     for (uint32_t i = g0; i < g1; ++i) {
       int budget = g1 - g0 == 1 ? sms
-                                : std::max(1, static_cast<int>(std::floor(sms * bytes[i - g0] / std::max(tot, 1.0))));
-      budget = std::min(budget, sms - cta0 - static_cast<int>(g1 - 1 - i));  // leave >= 1 CTA per later member
+                                : std::max(min_ctas(layers[i]),
+                                           static_cast<int>(std::floor(sms * bytes[i - g0] / std::max(tot, 1.0))));
+      int later = 0;  // leave every later member its minimum partition
+      for (uint32_t j = i + 1; j < g1; ++j) later += min_ctas(layers[j]);
+      budget = std::min(budget, sms - cta0 - later);
       if (rsp_status st = make_plan(*layers[i], dpx, &plans[i], std::max(1, budget))) return st;
       const bool wp = i > 0 && (i == g0);
       const int xop = (x_ops && x_ops[i] == RSP_XOP_SILU_GATE) ? rsp::kLinSiluGate : 0;

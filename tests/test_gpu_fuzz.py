@@ -110,3 +110,25 @@ def test_rank_limit_is_unsupported_not_wrong(cuda):
             rsp.DecomposedLayer(w, torch.randn(m, r, device=cuda), torch.randn(r, n, device=cuda),
                                 rsp.SparsityPlan(0.5, r), weight_dtype=wdt)
         assert e.value.status == RSP_E_UNSUPPORTED
+
+
+@pytest.mark.parametrize("max_ctas", [0, 8])
+def test_stack_group_minimum_partitions(coracle, cuda, max_ctas):
+    """Input-sharing group members whose byte share is tiny (s = 0, r = 0
+    moves no weight bytes) still get the CTAs their column tiling needs; a
+    group whose minimums exceed the launch budget (max_ctas = 8 against
+    3 x 4 CTAs) is split and run in order."""
+    rng = np.random.default_rng(77)
+    n = 3000
+    shapes = [(4096, 0.4, 256), (4096, 0.0, 0), (3813, 0.7, 100)]
+    layers = [rsp.DecomposedLayer(torch.randn(m, n, device=cuda) * 0.02, torch.randn(m, r, device=cuda) * 0.1,
+                                  torch.randn(r, n, device=cuda) * 0.1, rsp.SparsityPlan(s, r), weight_dtype="f32")
+              for (m, s, r) in shapes]
+    x = torch.from_numpy(wl.heavy_tailed_x(n, rng)).to(cuda)
+    ys = [torch.full((l.m_out,), float("nan"), device=cuda) for l in layers]
+    st = rsp.Stack(layers, [x] * 3, ys, wait_prev=[True, False, False], max_ctas=max_ctas)
+    st.launch()
+    torch.cuda.synchronize()
+    for l, y in zip(layers, ys):
+        yo, _, _ = oracle_on_device_values(coracle, l, x)
+        assert maxrel(y.cpu().numpy(), yo) <= TOL_EXACT_INPUTS
