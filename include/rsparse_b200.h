@@ -19,7 +19,10 @@
  * DecomposedLayer, layer.hpp:38-48).  rsp_linear_forward is re-entrant
  * across streams when each concurrent call passes its own workspace
  * (SPEC.md:331 allows concurrent forward calls).  rsp_linear_forward_host
- * uses per-handle staging buffers and is NOT re-entrant on one handle.
+ * may be called from several threads on one handle: its per-handle staging
+ * buffers are behind a mutex, so such calls run one after another.  A stack
+ * owns one workspace: launches of one rsp_stack must be ordered (one stream,
+ * or the caller's events); independent tokens use independent stacks.
  */
 #ifndef RSPARSE_B200_H_
 #define RSPARSE_B200_H_

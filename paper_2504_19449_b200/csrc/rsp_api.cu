@@ -128,6 +128,7 @@ struct rsp_linear {
   void* x_pin = nullptr;
   float* y_pin = nullptr;
   uint32_t host_batch = 0;
+  std::mutex host_mu;  // concurrent forward_host calls on one handle take turns on the staging
   std::vector<uint32_t> comps;  // DecomposedLayer::selected_components
 };
 
@@ -689,6 +690,7 @@ rsp_status rsp_linear_forward_host(rsp_linear* h, const void* x_host, rsp_dtype 
   if (rsp_status st = check_x_dtype(xdt)) return st;
   if (ydt != RSP_F32 && ydt != RSP_F64) return fail(RSP_E_USAGE, "y dtype must be F32 or F64");
   if (batch == 0) return RSP_OK;
+  std::lock_guard<std::mutex> lock(h->host_mu);
   DeviceGuard g(h->device);
   const size_t xs = static_cast<size_t>(h->m_in) * 4;  // room for fp32
   if (!h->stream) RSP_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));

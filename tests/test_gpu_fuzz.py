@@ -132,3 +132,36 @@ def test_stack_group_minimum_partitions(coracle, cuda, max_ctas):
     for l, y in zip(layers, ys):
         yo, _, _ = oracle_on_device_values(coracle, l, x)
         assert maxrel(y.cpu().numpy(), yo) <= TOL_EXACT_INPUTS
+
+
+def test_forward_host_concurrent_threads(coracle, cuda):
+    """forward is re-entrant in the reference; the host-buffer
+    entry point on ONE handle from several threads (ctypes drops the GIL)
+    must give every caller its own token's result."""
+    import threading
+    rng = np.random.default_rng(5)
+    m, n, r = 2048, 3072, 128
+    layer = rsp.DecomposedLayer(torch.randn(m, n, device=cuda) * 0.02, torch.randn(m, r, device=cuda) * 0.1,
+                                torch.randn(r, n, device=cuda) * 0.1, rsp.SparsityPlan(0.4, r),
+                                deterministic=True)  # bit-reproducible, so any mix-up shows
+    xs = [wl.heavy_tailed_x(n, rng) for _ in range(8)]
+    want = [layer.forward_host(x) for x in xs]
+    got = [None] * len(xs)
+
+    def work(t):
+        for _ in range(20):
+            i = (t * 3 + _) % len(xs)
+            y = layer.forward_host(xs[i])
+            if not np.array_equal(y, want[i]):
+                got[t] = i
+                return
+        got[t] = -1
+
+    threads = [threading.Thread(target=work, args=(t,)) for t in range(len(xs))]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert got == [-1] * len(xs)
+    yo, _, _ = oracle_on_device_values(coracle, layer, torch.from_numpy(xs[0]).to(cuda))
+    assert maxrel(want[0], yo) <= TOL_EXACT_INPUTS
