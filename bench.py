@@ -326,8 +326,10 @@ def cpu_reference_leg(plans, threads, seconds=None, warmup=1, passes=None, layer
         "kind": "reference" if use_ref else "port",
         "sample": (f"{'reference rsparse::forward (oracle/_ref, fp64, -O3)' if use_ref else 'C port (oracle)'}: "
                    f"one decode token through {n_layers} decoder layer(s) x 7 linears of the config-2 plans "
-                   f"per pass (no extrapolation), linears of one input group concurrent on up to "
-                   f"{min(threads, 3)} threads, groups sequential; median of {len(times)} passes; "
+                   f"per pass (no extrapolation), "
+                   + (f"linears of one input group concurrent on up to {min(threads, 3)} threads, groups sequential"
+                      if threads > 1 else "single-threaded, every linear in decode order")
+                   + f"; median of {len(times)} passes; "
                    f"host {hi.get('cpu_model', '?')}, nproc {hi.get('nproc')}"),
         "passes": len(times), "pass_times_s": times, "host": hi, "layers_timed": n_layers,
         "resident": resident,
@@ -500,9 +502,12 @@ def run_ours(args):
         out["speedup_vs_dense_cublas"] = out["dense_cublas_us_per_token"] / us_token
         out["speedup_vs_dense_inhouse"] = out["dense_inhouse_us_per_token"] / us_token
     if rank == 0 and world == 1 and not args.no_cpu and not args.profile:
-        cpu = cpu_reference_leg(plans, os.cpu_count() or 1, seconds=args.cpu_seconds, layers=args.cpu_layers)
+        # single-threaded, as the reference runs (no internal threading,
+        # layer.cpp:95-123); the --impl reference arm times the
+        # whole stack with its input groups on concurrent threads
+        cpu = cpu_reference_leg(plans, 1, seconds=args.cpu_seconds, layers=args.cpu_layers)
         # per-token time of the sampled layers, scaled to the stack (a
-        # reported baseline only; the reference arm times the whole stack)
+        # reported baseline only)
         scale = len(plans) / (7 * cpu["layers_timed"])
         out["cpu_baseline"] = {"value": cpu["value"] * scale, "unit": "us/token", "cores": cpu["cores"],
                                "kind": cpu["kind"],
