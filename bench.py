@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--check", action="store_true",
                     help="after the timed loop, check a sample of the stack outputs against the oracle")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "kernel"],
+                    help="row-sharded runs: y assembled by NCCL all-gathers after each group's launch, or by "
+                         "the kernel's own stores into every rank's y over peer memory (PeerStack)")
     ap.add_argument("--force-sharded", action="store_true",
                     help="use the row-sharded + all-gather path even on one rank (exercises it on 1 GPU)")
     return ap.parse_args()
@@ -405,6 +408,16 @@ def run_ours(args):
         # one persistent launch per token; q/k/v and gate/up overlap (shared input)
         st = rsp.Stack(layers, xs, ys, wait_prev=wait)
         launch = lambda: st.launch(stream)  # noqa: E731
+    elif args.exchange == "kernel":
+        # row-sharded linears in ONE persistent launch per rank and token; each
+        # CTA stores its rows into every rank's full y (CUDA IPC peer memory)
+        # and publishes them on every rank's exchange words -- no collective
+        from paper_2504_19449_b200.sharding import PeerStack, _CudaArray
+        st = PeerStack(layers, xs, wait_prev=wait, device=local)
+        launch = lambda: st.launch(stream)  # noqa: E731
+        y_dev = torch.as_tensor(_CudaArray(st.base, st.xoff // 4, "<f4"), device=dev)  # every full y
+        y_host = torch.empty_like(y_dev, device="cpu").pin_memory()
+        ys = [st.full_y(i) for i in range(len(layers))]
     else:
         # row-sharded linears, each followed by one in-place NCCL all-gather
         # of y (paper_2504_19449_b200/sharding.py), captured as one graph
@@ -477,7 +490,8 @@ def run_ours(args):
                                "50% model-level sparsity (rho~U(0.3,0.7), C=0.5), bf16 W/x, fp32 accum; "
                                "q/k/v and gate/up share one input (decoder-layer dataflow)",
                    "global_batch": 1, "layers": args.layers, "linears": len(layers),
-                   "parallelism": f"row-shard{world}" + ("+allgather" if sharded else ""),
+                   "parallelism": f"row-shard{world}" + (("+kernel-exchange" if args.exchange == "kernel"
+                                                             else "+allgather") if sharded else ""),
                    "combine": "deterministic (fixed-order partials)" if args.deterministic else "float reductions at L2",
                    "sharded_graph": (getattr(st, "graph", None) is not None) if sharded else None,
                    "l2": "no flush: 16 GB resident operands >> 126 MB L2",
@@ -488,13 +502,15 @@ def run_ours(args):
                      "frac": achieved / hbm_peak, "traffic": None if sharded else load_traffic(),
                      "peak_kind": peak_kind, "algorithmic_bytes_per_step": bytes_step,
                      "kernel_bytes_per_step": kbytes_step,
-                     "kernel": ("stack_kernel<bf16,bf16> (1 launch per input group, + NCCL all-gather of y)" if sharded
+                     "kernel": ("stack_kernel<bf16,bf16> (1 persistent launch/step, y stored into every rank)"
+                                if sharded and args.exchange == "kernel" else
+                                "stack_kernel<bf16,bf16> (1 launch per input group, + NCCL all-gather of y)" if sharded
                                 else "stack_kernel<bf16,bf16> (1 persistent launch/step, 224 linears)")},
         "e2e": {"value": e2e_ms * 1e3, "unit": "us/token", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
                 "path": "rsp_stack_launch_host (C ABI, pinned host buffers, synchronised per token)" if not sharded
                 else "torch pinned copies around the sharded graph"},
-        "gpu_launches": args.steps * (max(gid) + 1 if sharded else 1),
+        "gpu_launches": args.steps * (max(gid) + 1 if sharded and args.exchange == "nccl" else 1),
         "clocks": clocks.summary(),
     }
     out.update(extras)
@@ -537,7 +553,8 @@ def check_outputs(layers, xs, ys, plans, every=16):
         W, A, B = l.export()
         x = xs[i].float().cpu().numpy().astype(np.float64)
         yo, kept = C.forward(np.ascontiguousarray(W.T), A, B, plans[i][3], x, return_kept=True)
-        y = ys[i].cpu().numpy().astype(np.float64)
+        yi = ys[i][l.row_begin:l.row_end] if ys[i].numel() == l.m_out else ys[i]  # a rank's own rows
+        y = yi.cpu().numpy().astype(np.float64)
         e = float(np.max(np.abs(y - yo)) / max(np.max(np.abs(yo)), 1e-300))
         worst = max(worst, e)
         if e > 1e-5 or not np.array_equal(l.selected(xs[i]), kept):

@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define RSP_ABI_VERSION 2
+#define RSP_ABI_VERSION 3
 
 typedef enum rsp_status {
   RSP_OK = 0,
@@ -295,7 +295,26 @@ typedef struct rsp_stack_spec {
   uint32_t max_ctas;         /* 0: one CTA per SM; else at most this many CTAs (one per SM), so
                                 that independent stacks -- e.g. the B tokens of a small batch,
                                 SPEC.md:331 -- run concurrently on disjoint SMs */
+  /* Cross-process row sharding (one process per GPU, xrank >= 1 ranks): this
+   * rank's stack holds its row shards; y_peers (npeer == xrank) address every
+   * rank's y, mapped into this process (rsp_ipc_*), and the group completion
+   * counters live in every rank's exchange area: xctr[p] is rank p's area
+   * (rsp_stack_exchange_words(count) 64-bit words, zeroed once before the
+   * first launch, never reset), xctr[xself] this rank's own.  Every CTA
+   * publishes its rows to all ranks (fence.acq_rel.sys + one add per rank);
+   * a dependent group waits for all ranks' CTAs; a start fence per launch
+   * keeps a rank from zeroing rows a slower rank still reads.  All ranks must
+   * build the same stack (same shapes, even shards: equal per-linear grids,
+   * rsp_stack_grids) and launch it the same number of times.  Not with
+   * RSP_FLAG_DETERMINISTIC. */
+  uint32_t xrank;
+  uint32_t xself;
+  unsigned long long* const* xctr;
 } rsp_stack_spec;
+size_t rsp_stack_exchange_words(uint32_t count);
+/* Per-linear CTA counts of a stack (count entries): equal on every rank of
+ * a cross-process stack. */
+rsp_status rsp_stack_grids(const rsp_stack* s, uint32_t* grids, uint32_t count);
 rsp_status rsp_stack_create_spec(const rsp_stack_spec* spec, rsp_stack** out);
 rsp_status rsp_stack_launch(rsp_stack* s, void* stream);
 /* The end-to-end stack path with host buffers: x_host (x_bytes) is copied to
@@ -309,6 +328,19 @@ rsp_status rsp_stack_io_spans(const rsp_stack* s, size_t* x_bytes, size_t* y_byt
 rsp_status rsp_stack_launch_host(rsp_stack* s, const void* x_host, size_t x_bytes, void* y_host,
                                  size_t y_bytes, void* stream);
 void rsp_stack_destroy(rsp_stack* s);
+
+/* -- peer memory (cross-process exchange) ------------------------------------
+ * A device allocation shared between the processes of one node through CUDA
+ * IPC: rsp_ipc_alloc (zeroed), rsp_ipc_export its handle (RSP_IPC_HANDLE_BYTES
+ * opaque bytes, sent to the peers by the caller), rsp_ipc_open a peer's
+ * handle on this process's device (peer access over NVLink), rsp_ipc_close /
+ * rsp_ipc_free. */
+#define RSP_IPC_HANDLE_BYTES 64
+rsp_status rsp_ipc_alloc(int device, size_t bytes, void** dev_ptr);
+rsp_status rsp_ipc_free(void* dev_ptr);
+rsp_status rsp_ipc_export(const void* dev_ptr, void* handle_out);
+rsp_status rsp_ipc_open(int device, const void* handle, void** dev_ptr);
+rsp_status rsp_ipc_close(void* dev_ptr);
 
 /* -- diagnostics ---------------------------------------------------------------- */
 /* rsp_linear_forward (dense=0) or rsp_linear_dense_forward (dense=1) that also

@@ -27,7 +27,10 @@ EXPORTS = [
     "rsp_debug_stack_trace", "rsp_debug_batch_trace", "rsp_debug_set_batch_trace", "rsp_stack_io_spans",
     "rsp_stack_launch_host", "rsp_stack_create_ops", "rsp_stack_create_spec", "rsp_rspl_read", "rsp_linear_load_rspl", "rsp_linear_save_rspl", "rsp_linear_components",
     "rsp_aggregate_scores", "rsp_select_components", "rsp_split_factors", "rsp_linear_set_components",
+    "rsp_stack_exchange_words", "rsp_stack_grids", "rsp_ipc_alloc", "rsp_ipc_free", "rsp_ipc_export",
+    "rsp_ipc_open", "rsp_ipc_close",
 ]
+RSP_IPC_HANDLE_BYTES = 64
 
 
 class LinearDesc(ct.Structure):
@@ -71,6 +74,7 @@ class StackSpec(ct.Structure):
         ("x_dtype", ct.c_int), ("y_devs", ct.POINTER(ct.c_void_p)), ("dense", ct.c_int),
         ("wait_prev", ct.POINTER(ct.c_uint8)), ("x_ops", ct.POINTER(ct.c_uint8)), ("npeer", ct.c_uint32),
         ("y_peers", ct.POINTER(ct.c_void_p)), ("max_ctas", ct.c_uint32),
+        ("xrank", ct.c_uint32), ("xself", ct.c_uint32), ("xctr", ct.POINTER(ct.c_void_p)),
     ]
 
 
@@ -150,6 +154,13 @@ def lib() -> ct.CDLL:
         "rsp_stack_launch": (ct.c_int, [vp, vp]),
         "rsp_stack_destroy": (None, [vp]),
         "rsp_device_sm_count": (ct.c_int, [ct.c_int]),
+        "rsp_stack_exchange_words": (ct.c_size_t, [ct.c_uint32]),
+        "rsp_stack_grids": (ct.c_int, [vp, ct.POINTER(ct.c_uint32), ct.c_uint32]),
+        "rsp_ipc_alloc": (ct.c_int, [ct.c_int, ct.c_size_t, ct.POINTER(vp)]),
+        "rsp_ipc_free": (ct.c_int, [vp]),
+        "rsp_ipc_export": (ct.c_int, [vp, ct.c_char_p]),
+        "rsp_ipc_open": (ct.c_int, [ct.c_int, ct.c_char_p, ct.POINTER(vp)]),
+        "rsp_ipc_close": (ct.c_int, [vp]),
         "rsp_debug_forward_trace": (ct.c_int, [vp, vp, ct.c_int, vp, vp, ct.c_size_t, vp, ct.c_int, vp]),
         "rsp_debug_stack_trace": (ct.c_int, [vp, vp, ct.POINTER(u32), vp]),
         "rsp_debug_batch_trace": (ct.c_int, [vp, u32]),

@@ -139,6 +139,8 @@ struct rsp_stack {
   void* ws = nullptr;
   LinDesc* descs = nullptr;  // device array
   float** ypeer = nullptr;   // device [count][kMaxPeers] y destinations (npeer > 1)
+  unsigned long long** xctr = nullptr;  // device [xrank] every rank's exchange words (cross-process)
+  std::vector<uint32_t> grids;          // per-linear CTA counts
   rsp::LinCtl* ctl = nullptr;  // device control table
   void* plans = nullptr;     // device plan table [count][grid]
   StackParams params = {};   // the captured launch (re-launched by the debug trace)
@@ -1019,6 +1021,17 @@ rsp_status rsp_stack_create_spec(const rsp_stack_spec* spec, rsp_stack** out) {
     if (!spec->y_peers[i]) return fail(RSP_E_USAGE, "null y_peers[%u]", i);
   if (!layers || !x_devs || !y_devs || !out || count == 0) return fail(RSP_E_USAGE, "bad stack arguments");
   if (rsp_status st = check_x_dtype(xdt)) return st;
+  const uint32_t xrank = spec->xrank;
+  if (xrank > 0) {
+    if (xrank > static_cast<uint32_t>(rsp::kMaxPeers)) return fail(RSP_E_USAGE, "xrank %u exceeds %d", xrank, rsp::kMaxPeers);
+    if (npeer != xrank && !(xrank == 1 && npeer == 1))
+      return fail(RSP_E_USAGE, "xrank %u needs npeer == xrank y destinations (got %u)", xrank, npeer);
+    if (!spec->xctr || spec->xself >= xrank) return fail(RSP_E_USAGE, "xrank needs xctr[xrank] and xself < xrank");
+    for (uint32_t p = 0; p < xrank; ++p)
+      if (!spec->xctr[p]) return fail(RSP_E_USAGE, "null xctr[%u]", p);
+    if (layers[0] && layers[0]->deterministic)
+      return fail(RSP_E_UNSUPPORTED, "cross-process stacks do not support RSP_FLAG_DETERMINISTIC");
+  }
   for (uint32_t i = 0; x_ops && i < count; ++i) {
     if (x_ops[i] > RSP_XOP_SILU_GATE) return fail(RSP_E_USAGE, "x_ops[%u] = %u is not an RSP_XOP_*", i, x_ops[i]);
     if (x_ops[i] == RSP_XOP_SILU_GATE && xdt != RSP_F32)
@@ -1155,6 +1168,13 @@ rsp_status rsp_stack_create_spec(const rsp_stack_spec* spec, rsp_stack** out) {
     e = cudaMalloc(&s->ypeer, sizeof(float*) * tab.size());
     if (e == cudaSuccess) e = cudaMemcpy(s->ypeer, tab.data(), sizeof(float*) * tab.size(), cudaMemcpyHostToDevice);
   }
+  if (e == cudaSuccess && xrank > 0) {
+    e = cudaMalloc(&s->xctr, sizeof(unsigned long long*) * xrank);
+    if (e == cudaSuccess)
+      e = cudaMemcpy(s->xctr, spec->xctr, sizeof(unsigned long long*) * xrank, cudaMemcpyHostToDevice);
+  }
+  s->grids.resize(count);
+  for (uint32_t i = 0; i < count; ++i) s->grids[i] = static_cast<uint32_t>(descs[i].grid);
   if (e == cudaSuccess) e = cudaMalloc(&s->ctl, sizeof(rsp::LinCtl) * count);
   if (e == cudaSuccess) e = cudaMemcpy(s->ctl, ctl.data(), sizeof(rsp::LinCtl) * count, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
@@ -1179,6 +1199,10 @@ rsp_status rsp_stack_create_spec(const rsp_stack_spec* spec, rsp_stack** out) {
     p.zero = 0u;
     p.ypeer = s->ypeer;
     p.npeer = static_cast<int>(npeer);
+    p.xctr = s->xctr;
+    p.xlocal = xrank > 0 ? spec->xctr[spec->xself] : nullptr;
+    p.xrank = static_cast<int>(xrank);
+    p.xslots = static_cast<int>(count);  // arrival words [0, count) (group slots), then the start fence
     p.plans = s->plans;
     p.ctl = s->ctl;
     bind_workspace(&p, s->ws, wl);
@@ -1248,6 +1272,51 @@ rsp_status rsp_debug_stack_trace(rsp_stack* s, int64_t* trace_dev, uint32_t* gri
   return RSP_OK;
 }
 
+size_t rsp_stack_exchange_words(uint32_t count) { return static_cast<size_t>(count) + 1; }
+
+rsp_status rsp_stack_grids(const rsp_stack* s, uint32_t* grids, uint32_t count) {
+  if (!s || !grids || count != s->grids.size()) return fail(RSP_E_USAGE, "rsp_stack_grids: null or count mismatch");
+  std::copy(s->grids.begin(), s->grids.end(), grids);
+  return RSP_OK;
+}
+
+rsp_status rsp_ipc_alloc(int device, size_t bytes, void** dev_ptr) {
+  if (!dev_ptr || bytes == 0) return fail(RSP_E_USAGE, "rsp_ipc_alloc: null pointer or zero bytes");
+  DeviceGuard g(device);
+  RSP_CUDA(cudaMalloc(dev_ptr, bytes));  // its own allocation: an IPC handle maps exactly this block
+  RSP_CUDA(cudaMemset(*dev_ptr, 0, bytes));
+  return RSP_OK;
+}
+
+rsp_status rsp_ipc_free(void* dev_ptr) {
+  RSP_CUDA(cudaFree(dev_ptr));
+  return RSP_OK;
+}
+
+rsp_status rsp_ipc_export(const void* dev_ptr, void* handle_out) {
+  static_assert(sizeof(cudaIpcMemHandle_t) <= RSP_IPC_HANDLE_BYTES, "IPC handle size");
+  if (!dev_ptr || !handle_out) return fail(RSP_E_USAGE, "rsp_ipc_export: null pointer");
+  cudaIpcMemHandle_t h;
+  RSP_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
+  std::memset(handle_out, 0, RSP_IPC_HANDLE_BYTES);
+  std::memcpy(handle_out, &h, sizeof(h));
+  return RSP_OK;
+}
+
+rsp_status rsp_ipc_open(int device, const void* handle, void** dev_ptr) {
+  if (!handle || !dev_ptr) return fail(RSP_E_USAGE, "rsp_ipc_open: null pointer");
+  DeviceGuard g(device);
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  RSP_CUDA(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return RSP_OK;
+}
+
+rsp_status rsp_ipc_close(void* dev_ptr) {
+  RSP_CUDA(cudaIpcCloseMemHandle(dev_ptr));
+  return RSP_OK;
+}
+
 void rsp_stack_destroy(rsp_stack* s) {
   if (!s) return;
   DeviceGuard g(s->device);
@@ -1258,6 +1327,7 @@ void rsp_stack_destroy(rsp_stack* s) {
   cudaFree(s->plans);
   cudaFree(s->ctl);
   cudaFree(s->ypeer);
+  cudaFree(s->xctr);
   delete s;
 }
 

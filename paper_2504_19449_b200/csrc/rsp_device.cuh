@@ -422,4 +422,29 @@ __device__ __forceinline__ void spin_until_count(const unsigned* p, unsigned tar
   }
 }
 
+// ---------------------------------------------------------------------------
+// Cross-process exchange counters (row-sharded ranks on several GPUs): 64-bit
+// words in every rank's exchange area, mapped into the peers over NVLink.
+// They are cumulative (never reset: a late arrival from a slower rank can
+// not race a reset), so a wait compares against (launch epoch + 1) x the
+// arrivals of one launch.  Arrive = fence.acq_rel.sys, then relaxed sys-scope
+// adds on every rank's word (one fence for all peers); wait = sys-scope
+// acquire poll.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+__device__ __forceinline__ void red_relaxed_sys_add_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void spin_until_u64_sys(const unsigned long long* p, unsigned long long target) {
+  unsigned long long spins = 0;
+  while (ld_acquire_sys_u64(p) < target) {
+    if (++spins > (1ull << 26)) __trap();  // watchdog: a rank that never launched / arrived
+  }
+}
+
 }  // namespace rsp

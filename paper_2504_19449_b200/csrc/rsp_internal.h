@@ -62,6 +62,13 @@ struct StackParams {
   unsigned zero;                   // always 0: a value the compiler cannot fold (load batching in stream_list)
   float* const* ypeer;             // npeer > 1: [count][kMaxPeers] destinations of each linear's y rows
   int npeer;                       // destinations per y (1: the descriptor's y only)
+  // Cross-process row sharding (xrank > 0, one launch per rank and token):
+  // every rank's exchange words ([xslots] group arrivals + 1 start fence),
+  // this rank's own words, the rank count.  Arrivals go to every rank;
+  // dependency waits poll the local words (targets x xrank, cumulative).
+  unsigned long long* const* xctr;
+  unsigned long long* xlocal;
+  int xrank, xslots;
   long long* trace;                // debug: [grid][16] phase timestamps of the last linear (null in production)
   const void* plans;               // [count][grid] per-CTA plans (plan_kernel), or null: computed in the kernel
   const LinCtl* ctl;               // [count] control table, or null (single linear: built from `one`)

@@ -854,6 +854,18 @@ __global__ void __launch_bounds__(kThreads, 1) stack_kernel(const StackParams P)
   if (tid == 0) C.S.set_m(M_GEN, ld_relaxed_gpu(P.hdr));  // launch epoch (stable during the launch)
   __syncthreads();
   C.epoch = C.S.m(M_GEN);
+  const int xr = P.xrank;
+  if (xr > 0) {
+    // Start fence across ranks: no CTA writes into a peer's y (the first
+    // linear's prep zeroes rows there) before every rank has started this
+    // token, i.e. finished reading the previous token's y (stream order).
+    if (tid == 0) {
+      if (b == 0)
+        for (int p = 0; p < xr; ++p) red_relaxed_sys_add_u64(P.xctr[p] + P.xslots, 1ull);
+      spin_until_u64_sys(P.xlocal + P.xslots, (static_cast<unsigned long long>(C.epoch) + 1ull) * xr);
+    }
+    __syncthreads();
+  }
   if (m0 < P.count) prep_linear<WT, XBF>(P, dm, b, C, plan_slot(C.S, 0));
 
   int mc = 0;        // member linears run so far (shared slot parity)
@@ -879,7 +891,11 @@ __global__ void __launch_bounds__(kThreads, 1) stack_kernel(const StackParams P)
             if (ck.aslot != cj.aslot) break;
             target += static_cast<unsigned>(ck.grid);
           }
-          spin_until_count(slot_of(P, cj.aslot), target);
+          if (xr > 0)  // every rank's CTAs of these linears, cumulative over launches
+            spin_until_u64_sys(P.xlocal + cj.aslot,
+                               (static_cast<unsigned long long>(C.epoch) + 1ull) * target * static_cast<unsigned>(xr));
+          else
+            spin_until_count(slot_of(P, cj.aslot), target);
           j = j2;
         }
       }
@@ -903,7 +919,15 @@ __global__ void __launch_bounds__(kThreads, 1) stack_kernel(const StackParams P)
     run_linear<WT, XBF>(P, dm, C, tr, plan_slot(C.S, mc));
     cp_async_wait_all();  // this thread's staged copies have landed
     __syncthreads();      // this CTA's y contributions are issued; shared memory is free
-    if (tid == 0) red_release_add(slot_of(P, cl.aslot), 1u);
+    if (tid == 0) {
+      if (xr > 0) {
+        // this CTA's rows are in every rank's y: publish to all ranks
+        fence_acq_rel_sys();
+        for (int p = 0; p < xr; ++p) red_relaxed_sys_add_u64(P.xctr[p] + cl.aslot, 1ull);
+      } else {
+        red_release_add(slot_of(P, cl.aslot), 1u);
+      }
+    }
     ++mc;
     mnext = mn;
     if (mn < P.count) {

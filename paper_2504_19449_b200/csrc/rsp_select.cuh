@@ -128,6 +128,10 @@ __device__ __forceinline__ void sel_clear(SelArea s) {
 // x (global; bf16 or fp32, any alignment) -> s.xs, and (when `hist`) the
 // level-1 histogram (s.h1 zeroed and published).  All of a thread's 16-byte
 // loads of one round are issued before any is consumed.  Ends with __syncthreads.
+// x is read at L2 (ld.global.cg), not through the read-only non-coherent
+// path: inside a stack launch it may have been written by other CTAs (an
+// earlier linear's output, another rank's rows), ordered by the dependency
+// acquire.
 template <bool XBF>
 __device__ __forceinline__ void sel_load(const void* __restrict__ x, int n, SelArea s, bool hist) {
   constexpr int kPer = XBF ? 8 : 4;  // elements per 16 B
@@ -140,7 +144,7 @@ __device__ __forceinline__ void sel_load(const void* __restrict__ x, int n, SelA
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int i = base + q * kThreads + static_cast<int>(threadIdx.x);
-        u[q] = i < nv ? __ldg(xv + i) : make_uint4(0, 0, 0, 0);
+        u[q] = i < nv ? __ldcg(xv + i) : make_uint4(0, 0, 0, 0);
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -169,7 +173,7 @@ __device__ __forceinline__ void sel_load(const void* __restrict__ x, int n, SelA
         asm volatile("st.shared.u16 [%0], %1;" ::"r"(s.xs + 2u * j), "h"(raw) : "memory");
         bits = static_cast<uint32_t>(raw) << 16;
       } else {
-        bits = __ldg(static_cast<const uint32_t*>(x) + j);
+        bits = __ldcg(static_cast<const uint32_t*>(x) + j);
         sts(s.xs + 4u * j, bits);
       }
       if (hist) hist_add(s, bits);
@@ -517,7 +521,7 @@ __device__ __forceinline__ void sel_load16(const void* __restrict__ x, int n, Se
 #pragma unroll
       for (int q = 0; q < kB; ++q) {
         const int i = base + q * kThreads + static_cast<int>(threadIdx.x);
-        u[q] = i < nv ? __ldg(xv + i) : make_uint4(0, 0, 0, 0);
+        u[q] = i < nv ? __ldcg(xv + i) : make_uint4(0, 0, 0, 0);
       }
       // every histogram update waits on every load of the round (see stream_list)
       uint32_t dep = 0;

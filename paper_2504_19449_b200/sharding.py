@@ -220,3 +220,177 @@ class ShardedGroupStack:
     def close(self):
         for st, _, _ in self.groups:
             st.close()
+
+
+# ----------------------------------------------------------------------------
+# The exchange inside the kernel, across processes (rsp_stack_spec.xrank)
+# ----------------------------------------------------------------------------
+class IpcOps:
+    """The CUDA IPC calls the cross-process exchange needs (rsp_ipc_* in the
+    library).  Kept behind one object so that the host logic -- handle
+    exchange, address tables, plan agreement -- runs in CPU tests with a
+    stand-in (tests/test_sharding.py)."""
+
+    def alloc(self, device: int, nbytes: int) -> int:
+        from . import _lib as L
+        p = L.ct.c_void_p()
+        L.check(L.lib().rsp_ipc_alloc(device, nbytes, L.ct.byref(p)), "rsp_ipc_alloc")
+        return int(p.value)
+
+    def export(self, ptr: int) -> bytes:
+        from . import _lib as L
+        buf = L.ct.create_string_buffer(L.RSP_IPC_HANDLE_BYTES)
+        L.check(L.lib().rsp_ipc_export(L.ct.c_void_p(ptr), buf), "rsp_ipc_export")
+        return buf.raw
+
+    def open(self, device: int, handle: bytes) -> int:
+        from . import _lib as L
+        p = L.ct.c_void_p()
+        L.check(L.lib().rsp_ipc_open(device, handle, L.ct.byref(p)), "rsp_ipc_open")
+        return int(p.value)
+
+    def close(self, ptr: int) -> None:
+        from . import _lib as L
+        L.lib().rsp_ipc_close(L.ct.c_void_p(ptr))
+
+    def free(self, ptr: int) -> None:
+        from . import _lib as L
+        L.lib().rsp_ipc_free(L.ct.c_void_p(ptr))
+
+
+def _align(v: int, a: int = 256) -> int:
+    return (v + a - 1) // a * a
+
+
+def exchange_layout(m_outs: Sequence[int]) -> Tuple[List[int], int, int]:
+    """Byte layout of a rank's exchange area, the same on every rank: the
+    full fp32 y of every linear (16-B aligned), then the 64-bit exchange
+    words (rsp_stack_exchange_words: one arrival word per linear slot, then
+    the start fence).  Returns (y offsets, word offset, total bytes)."""
+    offs, cur = [], 0
+    for m in m_outs:
+        offs.append(cur)
+        cur = _align(cur + 4 * int(m), 16)
+    xoff = _align(cur)
+    return offs, xoff, _align(xoff + 8 * (len(m_outs) + 1))
+
+
+def exchange_tables(bases: Sequence[int], y_offs: Sequence[int], xoff: int,
+                    row_begins: Sequence[int]) -> Tuple[List[List[int]], List[int]]:
+    """Every linear's y destinations on all ranks (this shard's first row in
+    each rank's full y) and every rank's exchange words."""
+    y_peers = [[b + off + 4 * rb for b in bases] for off, rb in zip(y_offs, row_begins)]
+    return y_peers, [b + xoff for b in bases]
+
+
+def _all_gather_object(obj, group):
+    rank, world = _group_info(group)
+    if world == 1:
+        return [obj]
+    out = [None] * world
+    dist.all_gather_object(out, obj, group=group)
+    return out
+
+
+def plans_agree(grids: Sequence[int], group=None) -> None:
+    """The dependency targets of a cross-process stack count every rank's
+    CTAs as this rank's grid x world: all ranks must have planned the same
+    per-linear grids.  Raises on every rank otherwise."""
+    allg = _all_gather_object(list(grids), group)
+    if any(g != allg[0] for g in allg):
+        raise RuntimeError(f"PeerStack: the ranks planned different CTA grids (uneven shards?): {allg}")
+
+
+class _CudaArray:
+    """__cuda_array_interface__ over a raw device range (torch views of the area)."""
+
+    def __init__(self, ptr: int, n: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False), "version": 3}
+
+
+class PeerStack:
+    """One rank's part of a row-sharded stack with one process per GPU and
+    the all-gather of y done by the kernel itself (SURVEY 8(e) without a
+    collective after the launch): every shard CTA stores its output rows
+    into EVERY rank's full y -- peer memory mapped over NVLink through CUDA
+    IPC -- and publishes them on every rank's exchange words
+    (rsp_stack_spec.xrank).  A dependent group on any rank starts once all
+    ranks' CTAs of the previous group have published.
+
+    ``layers``: this rank's shards (shard_rank = rank, shard_count = world);
+    ``xs[i]``: a device tensor, or an int j = "the full output of linear j"
+    (its copy in this rank's exchange area, assembled by all ranks);
+    ``wait_prev`` as for :class:`layer.Stack`.  Every rank builds the same
+    stack; the plans are checked to agree.  ``ipc`` / ``create`` exist for the
+    CPU tests of the host logic."""
+
+    def __init__(self, layers: Sequence[DecomposedLayer], xs, wait_prev=None, group=None,
+                 device: int = 0, ipc: Optional[IpcOps] = None, create: bool = True):
+        from . import _lib as L
+        self.rank, self.world = _group_info(group)
+        self.group = group
+        self.layers = list(layers)
+        self.ipc = ipc or IpcOps()
+        m_full = [l.m_out for l in self.layers]
+        rows = [(l.row_begin, l.row_end) for l in self.layers]
+        for l, (rb, re) in zip(self.layers, rows):
+            if (rb, re) != shard_rows(l.m_out, self.rank, self.world):
+                raise ValueError("PeerStack: layers must be this rank's row shards")
+        self.y_offs, self.xoff, self.nbytes = exchange_layout(m_full)
+        self.base = self.ipc.alloc(device, self.nbytes)  # zeroed: y and the exchange words
+        handles = _all_gather_object(self.ipc.export(self.base), group)
+        self.bases = [self.base if p == self.rank else self.ipc.open(device, handles[p])
+                      for p in range(self.world)]
+        self.y_peers, self.xctr = exchange_tables(self.bases, self.y_offs, self.xoff, [r[0] for r in rows])
+        self.y_devs = [self.base + off + 4 * rb for off, (rb, _) in zip(self.y_offs, rows)]
+        self.x_devs = [self.base + self.y_offs[x] if isinstance(x, int) else x.data_ptr() for x in xs]
+        self._h = None
+        if not create:
+            return
+        self._keep = xs
+        n = len(self.layers)
+        sp = L.StackSpec()
+        hp = (L.ct.c_void_p * n)(*[l.handle.value for l in self.layers])
+        xp = (L.ct.c_void_p * n)(*self.x_devs)
+        yp = (L.ct.c_void_p * n)(*self.y_devs)
+        xdt = next((x for x in xs if not isinstance(x, int)), None)
+        sp.layers, sp.count, sp.x_devs, sp.y_devs = hp, n, xp, yp
+        sp.x_dtype = L.RSP_BF16 if (xdt is not None and xdt.dtype == torch.bfloat16) else L.RSP_F32
+        wp = None
+        if wait_prev is not None:
+            wp = (L.ct.c_uint8 * n)(*[1 if w else 0 for w in wait_prev])
+            sp.wait_prev = L.ct.cast(wp, L.ct.POINTER(L.ct.c_uint8))
+        sp.npeer = self.world
+        flat = [p for pl in self.y_peers for p in pl]
+        sp.y_peers = (L.ct.c_void_p * len(flat))(*flat)
+        sp.xrank, sp.xself = self.world, self.rank
+        sp.xctr = (L.ct.c_void_p * self.world)(*self.xctr)
+        h = L.ct.c_void_p()
+        torch.cuda.synchronize(device)
+        L.check(L.lib().rsp_stack_create_spec(L.ct.byref(sp), L.ct.byref(h)), "rsp_stack_create_spec")
+        self._h = h
+        grids = (L.ct.c_uint32 * n)()
+        L.check(L.lib().rsp_stack_grids(h, grids, n), "rsp_stack_grids")
+        plans_agree(list(grids), group)
+
+    def full_y(self, i: int):
+        """Linear i's full output in this rank's exchange area (fp32 view)."""
+        return torch.as_tensor(_CudaArray(self.base + self.y_offs[i], self.layers[i].m_out, "<f4"),
+                               device=f"cuda:{torch.cuda.current_device()}")
+
+    def launch(self, stream=None) -> None:
+        from . import _lib as L
+        from .layer import _stream_ptr
+        L.check(L.lib().rsp_stack_launch(self._h, _stream_ptr(stream)), "rsp_stack_launch")
+
+    def close(self) -> None:
+        from . import _lib as L
+        if self._h:
+            L.lib().rsp_stack_destroy(self._h)
+            self._h = None
+        for p, b in enumerate(getattr(self, "bases", [])):
+            if p != self.rank:
+                self.ipc.close(b)
+        if getattr(self, "base", None):
+            self.ipc.free(self.base)
+            self.base = None

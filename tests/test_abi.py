@@ -33,7 +33,7 @@ def test_library_exports_every_declared_symbol():
     out = subprocess.run(["nm", "-D", "--defined-only", L.LIB], capture_output=True, text=True).stdout
     exported = set(re.findall(r"\bT (rsp_\w+)", out))
     assert set(declared_functions()) <= exported
-    assert L.lib().rsp_abi_version() == 2
+    assert L.lib().rsp_abi_version() == 3
 
 
 def test_library_is_sm100a():

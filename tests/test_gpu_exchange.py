@@ -57,3 +57,58 @@ def test_ranks_in_one_launch_exchange_y_in_kernel(cuda, ranks):
         assert maxrel(Y["o"][p].cpu().numpy(), full["o"].forward(Y["q"][p]).cpu().numpy()) <= 1e-6
     for p in range(1, ranks):  # every rank holds the same assembled outputs (up to float-atomic order)
         assert maxrel(Y["q"][p].cpu().numpy(), Y["q"][0].cpu().numpy()) <= 1e-6
+
+
+def test_peer_stack_one_rank_counts_and_outputs(cuda):
+    """The cross-process path (rsp_stack_spec.xrank) at world size 1 -- the
+    only size one GPU can run without ranks whose kernels wait on each other:
+    the per-launch start fence, the sys-scope arrivals on the exchange words
+    and the cumulative (never reset) dependency targets over many launches.
+    o reads q's full output from the exchange area (in-launch dataflow)."""
+    from paper_2504_19449_b200.sharding import PeerStack, _CudaArray
+    rng = np.random.default_rng(11)
+    specs = [(1536, 512, 0.3, 48), (512, 512, 0.25, 32), (512, 1536, 0.2, 64)]
+    layers = [rsp.DecomposedLayer(torch.randn(m, n, device=cuda) * 0.05, torch.randn(m, r, device=cuda) * 0.1,
+                                  torch.randn(r, n, device=cuda) * 0.1, rsp.SparsityPlan(s, r), weight_dtype="bf16")
+              for (m, n, s, r) in specs]
+    x = torch.from_numpy(wl.heavy_tailed_x(512, rng)).to(cuda)
+    ps = PeerStack(layers, [x, x, 0], wait_prev=[True, False, True])
+    launches = 25
+    for _ in range(launches):
+        ps.launch()
+    torch.cuda.synchronize()
+    q, k, o = (ps.full_y(i).clone() for i in range(3))
+    assert maxrel(q.cpu().numpy(), layers[0].forward(x).cpu().numpy()) <= 1e-6
+    assert maxrel(k.cpu().numpy(), layers[1].forward(x).cpu().numpy()) <= 1e-6
+    assert maxrel(o.cpu().numpy(), layers[2].forward(q).cpu().numpy()) <= 1e-6
+    grids = (rsp._lib.ct.c_uint32 * 3)()
+    rsp._lib.check(rsp.lib().rsp_stack_grids(ps._h, grids, 3))
+    words = torch.as_tensor(_CudaArray(ps.base + ps.xoff, 4, "<u8"), device=cuda).cpu().tolist()
+    # group {q, k} arrives on q's slot, o on its own; k's word is unused; then the start fence
+    assert words == [launches * (grids[0] + grids[1]), 0, launches * grids[2], launches], (words, list(grids))
+    ps.close()
+
+
+def test_peer_stack_spec_errors(cuda):
+    from paper_2504_19449_b200 import _lib as L
+    l = rsp.DecomposedLayer(torch.randn(256, 256, device=cuda), torch.randn(256, 8, device=cuda),
+                            torch.randn(8, 256, device=cuda), rsp.SparsityPlan(0.5, 8))
+    x = torch.randn(256, device=cuda)
+    y = torch.empty(256, device=cuda)
+    ctr = torch.zeros(4, dtype=torch.int64, device=cuda)
+    sp = L.StackSpec()
+    sp.layers = (L.ct.c_void_p * 1)(l.handle.value)
+    sp.count, sp.x_dtype = 1, L.RSP_F32
+    sp.x_devs = (L.ct.c_void_p * 1)(x.data_ptr())
+    sp.y_devs = (L.ct.c_void_p * 1)(y.data_ptr())
+    sp.xrank, sp.xself, sp.npeer = 2, 0, 1  # two ranks but one y destination
+    sp.xctr = (L.ct.c_void_p * 2)(ctr.data_ptr(), ctr.data_ptr())
+    h = L.ct.c_void_p()
+    assert L.lib().rsp_stack_create_spec(L.ct.byref(sp), L.ct.byref(h)) == L.RSP_E_USAGE
+    sp.xrank, sp.xself = 1, 1  # xself out of range
+    assert L.lib().rsp_stack_create_spec(L.ct.byref(sp), L.ct.byref(h)) == L.RSP_E_USAGE
+    d = rsp.DecomposedLayer(torch.randn(256, 256, device=cuda), torch.randn(256, 8, device=cuda),
+                            torch.randn(8, 256, device=cuda), rsp.SparsityPlan(0.5, 8), deterministic=True)
+    sp.layers = (L.ct.c_void_p * 1)(d.handle.value)
+    sp.xself = 0
+    assert L.lib().rsp_stack_create_spec(L.ct.byref(sp), L.ct.byref(h)) == L.RSP_E_UNSUPPORTED
