@@ -436,6 +436,8 @@ class Stack:
         self.layers = layers
         self.xs, self.ys = xs, ys
         n = len(layers)
+        if len({x.dtype for x in xs}) != 1:  # the ABI takes one activation dtype per stack
+            raise L.UsageError(L.RSP_E_USAGE, "stack inputs must share one dtype")
         hp = (ct.c_void_p * n)(*[l.handle.value for l in layers])
         xp = (ct.c_void_p * n)(*[x.data_ptr() for x in xs])
         yp = (ct.c_void_p * n)(*[y.data_ptr() for y in ys])

@@ -353,9 +353,13 @@ class PeerStack:
         hp = (L.ct.c_void_p * n)(*[l.handle.value for l in self.layers])
         xp = (L.ct.c_void_p * n)(*self.x_devs)
         yp = (L.ct.c_void_p * n)(*self.y_devs)
-        xdt = next((x for x in xs if not isinstance(x, int)), None)
+        dts = {x.dtype for x in xs if not isinstance(x, int)} | ({torch.float32} if any(
+            isinstance(x, int) for x in xs) else set())
+        if len(dts) != 1 or not dts <= {torch.float32, torch.bfloat16}:
+            # one activation dtype per stack; the exchange area holds fp32 outputs
+            raise ValueError(f"PeerStack: all inputs must share one dtype (fp32 or bf16), got {dts}")
         sp.layers, sp.count, sp.x_devs, sp.y_devs = hp, n, xp, yp
-        sp.x_dtype = L.RSP_BF16 if (xdt is not None and xdt.dtype == torch.bfloat16) else L.RSP_F32
+        sp.x_dtype = L.RSP_BF16 if dts == {torch.bfloat16} else L.RSP_F32
         wp = None
         if wait_prev is not None:
             wp = (L.ct.c_uint8 * n)(*[1 if w else 0 for w in wait_prev])
