@@ -51,7 +51,8 @@ def parse():
     ap.add_argument("--cpu-layers", type=int, default=4,
                     help="decoder layers in the cpu_baseline sample of the GPU arm (one token through them)")
     ap.add_argument("--ref-layers", type=int, default=None,
-                    help="--impl reference: decoder layers per pass (default: all --layers)")
+                    help="--impl reference: decoder layers per pass, scaled to --layers (default: all of them, "
+                         "or a bounded sample when --steps would take more than ~4 minutes)")
     ap.add_argument("--deterministic", action="store_true",
                     help="fixed-order (bit-reproducible) combines instead of float reductions at L2")
     ap.add_argument("--check", action="store_true",
@@ -339,6 +340,10 @@ def cpu_reference_leg(plans, threads, seconds=None, warmup=1, passes=None, layer
     }
 
 
+REF_S_PER_LAYER = 0.06  # measured: ~1.8 s per 32-layer token on the GPU box's host (profiles/r02b_bench_reference.json)
+REF_BUDGET_S = 240.0
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -348,9 +353,16 @@ def run_reference(args):
     plans = ref_config2_plans(R, n_layers=args.layers)
     threads = os.cpu_count() or 1
     t_run = time.perf_counter()
-    res = cpu_reference_leg(plans, threads, warmup=min(args.warmup, 1), passes=args.steps,
-                            layers=args.ref_layers)
-    same = args.ref_layers is None or args.ref_layers == args.layers
+    ref_layers = args.ref_layers
+    if ref_layers is None and args.steps * REF_S_PER_LAYER * args.layers > REF_BUDGET_S:
+        # keep the run within a few minutes: each step a bounded sample (the
+        # first decoder layers of the stack), scaled to the whole stack below
+        ref_layers = max(1, int(REF_BUDGET_S / (args.steps * REF_S_PER_LAYER)))
+    res = cpu_reference_leg(plans, threads, warmup=min(args.warmup, 1), passes=args.steps, layers=ref_layers)
+    scale = args.layers / ref_layers if ref_layers else 1.0
+    if scale != 1.0:
+        res["value"] *= scale
+        res["sample"] += f"; x{scale:g} from {ref_layers} to {args.layers} layers (bounded sample for --steps {args.steps})"
     line = {
         "metric": METRIC, "impl": "reference", "value": res["value"], "unit": "us/token",
         "n_gpus": world, "steps": args.steps, "warmup": min(args.warmup, 1),
@@ -358,8 +370,8 @@ def run_reference(args):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "config2: 32-layer Llama-2-7B-shaped R-Sparse linear stack, batch 1, "
                                "50% model-level sparsity (rho~U(0.3,0.7), C=0.5)",
-                   "global_batch": 1, "layers": args.layers if same else args.ref_layers,
-                   "linears": 7 * (args.layers if same else args.ref_layers)},
+                   "global_batch": 1, "layers": args.layers, "linears": 7 * args.layers,
+                   "layers_timed_per_step": ref_layers or args.layers},
         "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": res["value"], "unit": "us/token", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "host": res["host"], "timed_seconds": sum(res["pass_times_s"]),

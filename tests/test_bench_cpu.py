@@ -44,3 +44,7 @@ def test_reference_arm_does_not_load_the_product(reforacle):
     assert line["impl"] == "reference" and line["cpu_baseline"]["kind"] == "reference"
     assert line["timed_seconds"] <= line["wall_seconds"]
     assert np.isfinite(line["value"]) and line["value"] > 0
+    # a bounded sample (1 of 32 layers per step) is scaled to the whole stack and says so
+    assert line["config"]["layers"] == 32 and line["config"]["layers_timed_per_step"] == 1
+    assert "x32 from 1 to 32 layers" in line["cpu_baseline"]["sample"]
+    assert line["value"] == line["cpu_baseline"]["value"] == line["e2e"]["value"]
