@@ -330,7 +330,7 @@ def cpu_reference_leg(plans, threads, seconds=None, warmup=1, passes=None, layer
         "kind": "reference" if use_ref else "port",
         "sample": (f"{'reference rsparse::forward (oracle/_ref, fp64, -O3)' if use_ref else 'C port (oracle)'}: "
                    f"one decode token through {n_layers} decoder layer(s) x 7 linears of the config-2 plans "
-                   f"per pass (no extrapolation), "
+                   f"per pass, "
                    + (f"linears of one input group concurrent on up to {min(threads, 3)} threads, groups sequential"
                       if threads > 1 else "single-threaded, every linear in decode order")
                    + f"; median of {len(times)} passes; "
