@@ -378,7 +378,8 @@ class PeerStack:
         plans_agree(list(grids), group)
 
     def full_y(self, i: int):
-        """Linear i's full output in this rank's exchange area (fp32 view)."""
+        """Linear i's full output in this rank's exchange area (fp32 view;
+        valid until :meth:`close`, which frees the area)."""
         return torch.as_tensor(_CudaArray(self.base + self.y_offs[i], self.layers[i].m_out, "<f4"),
                                device=f"cuda:{torch.cuda.current_device()}")
 
@@ -395,6 +396,13 @@ class PeerStack:
         for p, b in enumerate(getattr(self, "bases", [])):
             if p != self.rank:
                 self.ipc.close(b)
+        self.bases = []
         if getattr(self, "base", None):
             self.ipc.free(self.base)
             self.base = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
