@@ -32,7 +32,7 @@ import numpy as np
 import torch
 
 from . import _lib as L
-from .layer import DecomposedLayer, Recipe, SparsityPlan, Stack
+from .layer import DecomposedLayer, Recipe, Stack
 
 KRMS_EPS = 1e-6  # model.cpp:66
 SLOTS = ("q", "k", "v", "o", "up", "gate", "down")  # LinearSlot order (model.hpp:30)

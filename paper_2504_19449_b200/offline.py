@@ -21,7 +21,7 @@ from __future__ import annotations
 
 import ctypes as ct
 from dataclasses import dataclass
-from typing import List, Optional, Sequence
+from typing import List, Sequence
 
 import torch
 

@@ -187,7 +187,6 @@ def test_stack_launch_host_matches_device_launch(cuda):
     assert torch.allclose(y_host, want, rtol=1e-6, atol=1e-6)
     with pytest.raises(rsp.UsageError):
         rsp.lib()  # noqa: B018 (keep the library loaded)
-        import ctypes as ct
         from paper_2504_19449_b200 import _lib as L
         L.check(L.lib().rsp_stack_launch_host(st._h, x_host.data_ptr(), 2, y_host.data_ptr(), 4, None))
 

@@ -1,5 +1,4 @@
 """CPU checks of the BASELINE config generators (no GPU)."""
-import numpy as np
 
 from paper_2504_19449_b200 import workloads as wl
 

@@ -1,7 +1,6 @@
 """Phase timeline of one batched forward (rsp_debug_set_batch_trace): medians and
 maxima over the CTAs of the per-phase clock64 stamps, in us at --mhz."""
 import argparse
-import ctypes as ct
 import os
 import sys
 

@@ -4,7 +4,6 @@ Prints, per shape, the median / max over CTAs of each phase stamp in µs
 since CTA start, and the spread of CTA start times.
 """
 import argparse
-import ctypes as ct
 import os
 import sys
 
