@@ -1,7 +1,9 @@
 """A small config-2-like stack (one decoder layer at reduced width, grouped
 q/k/v and gate/up, bf16) plus single and batched forwards, launched a few
-times: the workload for compute-sanitizer memcheck / racecheck / synccheck
-(tools/gpu_sanitize.sh).  Exits non-zero on a parity failure."""
+times: a workload for compute-sanitizer memcheck / racecheck / synccheck
+where the sanitizer is allowed (it is closed on this project's GPU pool, where
+the bounds-checked build, tools/gpu_debugchecks.sh, runs instead).  Exits
+non-zero on a parity failure."""
 import os
 import sys
 
