@@ -300,9 +300,10 @@ typedef struct rsp_stack_spec {
    * rank's y, mapped into this process (rsp_ipc_*), and the group completion
    * counters live in every rank's exchange area: xctr[p] is rank p's area
    * (rsp_stack_exchange_words(count) 64-bit words, zeroed once before the
-   * first launch, never reset), xctr[xself] this rank's own.  Every CTA
-   * publishes its rows to all ranks (fence.acq_rel.sys + one add per rank);
-   * a dependent group waits for all ranks' CTAs; a start fence per launch
+   * first launch, never reset), xctr[xself] this rank's own.  The CTA that
+   * completes a group on its rank publishes the group to all ranks
+   * (fence.acq_rel.sys + one add per rank); a dependent group waits for
+   * every rank's publication; a start fence per launch
    * keeps a rank from zeroing rows a slower rank still reads.  All ranks must
    * build the same stack (same shapes, even shards: equal per-linear grids,
    * rsp_stack_grids) and launch it the same number of times.  Not with

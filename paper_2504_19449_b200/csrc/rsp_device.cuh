@@ -427,9 +427,9 @@ __device__ __forceinline__ void spin_until_count(const unsigned* p, unsigned tar
 // words in every rank's exchange area, mapped into the peers over NVLink.
 // They are cumulative (never reset: a late arrival from a slower rank can
 // not race a reset), so a wait compares against (launch epoch + 1) x the
-// arrivals of one launch.  Arrive = fence.acq_rel.sys, then relaxed sys-scope
-// adds on every rank's word (one fence for all peers); wait = sys-scope
-// acquire poll.
+// arrivals of one launch.  Publish = fence.acq_rel.sys, then relaxed
+// sys-scope adds on every rank's word (one fence for all peers); wait =
+// sys-scope acquire poll.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 __device__ __forceinline__ void red_relaxed_sys_add_u64(unsigned long long* p, unsigned long long v) {
