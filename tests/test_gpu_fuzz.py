@@ -165,3 +165,28 @@ def test_forward_host_concurrent_threads(coracle, cuda):
     assert got == [-1] * len(xs)
     yo, _, _ = oracle_on_device_values(coracle, layer, torch.from_numpy(xs[0]).to(cuda))
     assert maxrel(want[0], yo) <= TOL_EXACT_INPUTS
+
+
+@pytest.mark.parametrize("xdt", ["f32", "bf16"])
+def test_misaligned_inputs_and_outputs(coracle, cuda, xdt):
+    """x and y that are not 16-byte aligned (views one element into a buffer)
+    take the scalar load / store paths of the selector and the combine."""
+    rng = np.random.default_rng(31)
+    m, n, r = 1000, 2056, 96
+    layers = [rsp.DecomposedLayer(torch.randn(m, n, device=cuda) * 0.02, torch.randn(m, r, device=cuda) * 0.1,
+                                  torch.randn(r, n, device=cuda) * 0.1, rsp.SparsityPlan(s, r)) for s in (0.3, 0.6)]
+    buf = torch.from_numpy(random_x(rng, n + 1)).to(cuda)
+    buf = buf.to(torch.bfloat16) if xdt == "bf16" else buf
+    x = buf[1:]  # 2 or 4 bytes past a 16-byte boundary
+    ybuf = torch.full((2 * m + 2,), float("nan"), device=cuda)
+    ys = [ybuf[1:1 + m], ybuf[1 + m:1 + 2 * m]]
+    for l in layers:
+        yo, kept, _ = oracle_on_device_values(coracle, l, x)
+        assert np.array_equal(l.selected(x), kept)
+        assert maxrel(l.forward(x).cpu().numpy(), yo) <= TOL_EXACT_INPUTS
+    st = rsp.Stack(layers, [x, x], ys, wait_prev=[True, False])
+    st.launch()
+    torch.cuda.synchronize()
+    for l, y in zip(layers, ys):
+        yo, _, _ = oracle_on_device_values(coracle, l, x)
+        assert maxrel(y.cpu().numpy(), yo) <= TOL_EXACT_INPUTS
