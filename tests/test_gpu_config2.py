@@ -247,3 +247,37 @@ def test_batched_stack_modes_match_per_token(cuda, B):
         for b in range(B):
             assert maxrel(y[b].cpu().numpy(), l.forward(x[b]).cpu().numpy()) <= 1e-4
     bs.close()
+
+
+@pytest.mark.parametrize("sparsity,rank", [(0.5, 256), (0.7, 512), (0.3, 64)])
+def test_config4_layer_stack_every_output_vs_oracle(coracle, cuda, sparsity, rank):
+    """Config 4 (Llama-3-8B: GQA k/v 1024 x 4096, gate/up 14336 x 4096, down
+    4096 x 14336) through the stack with the bench's grouping, at three
+    points of the sparsity x rank sweep -- (0.7, 512) with the k/v ranks
+    clamped (s = 0) -- and 16 outlier channels per input; every output and
+    selection against the oracle."""
+    plans, clamped = wl.config4_plans(sparsity, rank, n_layers=1)
+    if (sparsity, rank) == (0.7, 512):
+        assert {c[0] for c in clamped} == {"k_proj", "v_proj"}
+    gid, wait = wl.input_groups(plans)
+    rng = np.random.default_rng(int(100 * sparsity) + rank)
+    layers, xs, xg = [], [], {}
+    for i, (name, m, n, s, r) in enumerate(plans):
+        w = torch.randn(m, n, device=cuda) * 0.02
+        a = torch.randn(m, r, device=cuda) * 0.05
+        b = torch.randn(r, n, device=cuda) * 0.05
+        layers.append(rsp.DecomposedLayer(w, a, b, rsp.SparsityPlan(s, r), weight_dtype="bf16"))
+        if gid[i] not in xg:
+            x = wl.silu_gate_x(n, rng) if name.endswith("down_proj") else wl.heavy_tailed_x(n, rng, outliers=16)
+            xg[gid[i]] = torch.from_numpy(x).to(cuda).to(torch.bfloat16)
+        xs.append(xg[gid[i]])
+    ys = [torch.full((l.m_out,), float("nan"), device=cuda) for l in layers]
+    st = rsp.Stack(layers, xs, ys, wait_prev=wait)
+    for _ in range(2):
+        st.launch()
+    torch.cuda.synchronize()
+    for (name, m, n, s, r), layer, x, y in zip(plans, layers, xs, ys):
+        W, A, B = layer.export()
+        yo, kept = coracle.forward(np.ascontiguousarray(W.T), A, B, s, as_seen(x), return_kept=True)
+        assert np.array_equal(layer.selected(x), kept), name
+        assert maxrel(y.cpu().numpy(), yo) <= TOL_EXACT_INPUTS, (name, maxrel(y.cpu().numpy(), yo))
