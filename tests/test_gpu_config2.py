@@ -281,3 +281,35 @@ def test_config4_layer_stack_every_output_vs_oracle(coracle, cuda, sparsity, ran
         yo, kept = coracle.forward(np.ascontiguousarray(W.T), A, B, s, as_seen(x), return_kept=True)
         assert np.array_equal(layer.selected(x), kept), name
         assert maxrel(y.cpu().numpy(), yo) <= TOL_EXACT_INPUTS, (name, maxrel(y.cpu().numpy(), yo))
+
+
+@pytest.mark.parametrize("B", [2, 6])
+def test_config2_batched_stack_every_token_vs_oracle(coracle, cuda, B):
+    """Config 3 at config-2 scale: one config-2 decoder layer (r > 1024
+    included) through BatchedStack -- B = 2 as concurrent per-token stacks,
+    B = 6 as union-of-masks passes -- each token against its own reference
+    forward (B independent forwards)."""
+    plans, built = _config2_layers((13,), cuda)
+    gid, wait = wl.input_groups(plans)
+    rng = np.random.default_rng(40 + B)
+    layers, X = [], {}
+    for i, (name, m, n, s, r, w, a, b) in enumerate(built):
+        layers.append(rsp.DecomposedLayer(w, a, b, rsp.SparsityPlan(s, r), weight_dtype="bf16"))
+        if gid[i] not in X:
+            gen = wl.silu_gate_x if name.endswith("down_proj") else wl.heavy_tailed_x
+            X[gid[i]] = torch.from_numpy(np.stack([gen(n, rng) for _ in range(B)])).to(cuda).to(torch.bfloat16)
+    xs = [X[gid[i]] for i in range(len(layers))]
+    ys = [torch.full((B, l.m_out), float("nan"), device=cuda) for l in layers]
+    bs = rsp.BatchedStack(layers, xs, ys, wait_prev=wait)
+    assert bs.mode == ("token_parallel" if B == 2 else "union_per_linear")
+    bs.launch()
+    torch.cuda.synchronize()
+    tol = TOL_EXACT_INPUTS if B == 2 else 1e-4  # union path: t split into bf16 hi + lo (~2^-16)
+    for (name, m, n, s, r, *_), layer, x, y in zip(built, layers, xs, ys):
+        W, A, Bm = layer.export()
+        Wt = np.ascontiguousarray(W.T)
+        for t in range(B):
+            yo, kept = coracle.forward(Wt, A, Bm, s, as_seen(x[t]), return_kept=True)
+            assert np.array_equal(layer.selected(x[t]), kept), (name, t)
+            assert maxrel(y[t].cpu().numpy(), yo) <= tol, (name, t, maxrel(y[t].cpu().numpy(), yo))
+    bs.close()
