@@ -137,7 +137,9 @@ rsp_status rsp_shard_rows(uint32_t m_out, uint32_t shard_rank, uint32_t shard_co
  * layer.cpp:35-68, with the factors precomputed on the host).  Uploads W in
  * input-channel-major layout Wt[m_in][m_pad], A_r^T[r][m_pad], B_r^T[m_in][r_pad].
  * Limits of this implementation (RSP_E_UNSUPPORTED, the reference has none):
- * m_in <= 32768 (selection keeps x on chip); one B_r^T row <= 4 KB, i.e.
+ * m_in <= 32768 (selection keeps x on chip; above ~28000 channels only with
+ * bf16 activations -- fp32 x then returns RSP_E_UNSUPPORTED at forward);
+ * one B_r^T row <= 4 KB, i.e.
  * rank <= 2048 with bf16 weights and <= 1024 with fp32 weights (stage-1 t
  * lives in shared memory).  Above rank m*n/(m+n) the factors outweigh W, so
  * the limit only excludes plans slower than the dense GEMV. */

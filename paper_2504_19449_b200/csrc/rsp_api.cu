@@ -102,6 +102,7 @@ struct LaunchPlan {
   int nb_pad = 4;
   size_t smem = 0;
   size_t ws_bytes = 0;  // single-linear workspace
+  bool bf16_x_only = false;  // m_in too wide for fp32 activations on chip
 };
 
 }  // namespace
@@ -205,8 +206,13 @@ rsp_status make_plan(const rsp_linear& L, const DevProps& dp, LaunchPlan* out, i
   p.cap_u = static_cast<int>((n + p.grid - 1) / p.grid) + 1;  // stage-1 channel range of one CTA
   p.cap_a = static_cast<int>((L.rank + ks - 1) / ks) + 1;     // A_r^T rows of one CTA
   p.smem = rsp::stack_smem_bytes(static_cast<int>(n), false, p.cap_w, p.cap_u, p.cap_a);  // fp32 x: the larger
-  if (p.smem > static_cast<size_t>(dp.smem_optin))
-    return fail(RSP_E_UNSUPPORTED, "fused kernel needs %zu B shared memory (> %d)", p.smem, dp.smem_optin);
+  if (p.smem > static_cast<size_t>(dp.smem_optin)) {
+    // wide inputs: x kept on chip as bf16 only (fp32 activations refused at forward)
+    p.smem = rsp::stack_smem_bytes(static_cast<int>(n), true, p.cap_w, p.cap_u, p.cap_a);
+    p.bf16_x_only = true;
+    if (p.smem > static_cast<size_t>(dp.smem_optin))
+      return fail(RSP_E_UNSUPPORTED, "fused kernel needs %zu B shared memory (> %d)", p.smem, dp.smem_optin);
+  }
   p.ws_bytes = WsLayout::make(1, p.nb_pad, static_cast<int>(L.r_pad), ks, static_cast<int>(L.m_pad)).bytes;
   *out = p;
   return RSP_OK;
@@ -324,6 +330,9 @@ rsp_status launch_forward(const rsp_linear* h, const void* x, rsp_dtype xdt, flo
   if (!ws || ws_bytes < h->plan.ws_bytes)
     return fail(RSP_E_USAGE, "workspace of %zu bytes is smaller than the %zu required", ws_bytes,
                 h->plan.ws_bytes);
+  if (xdt != RSP_BF16 && h->plan.bf16_x_only)
+    return fail(RSP_E_UNSUPPORTED, "m_in %u: fp32 activations do not fit in shared memory; pass bf16 activations",
+                h->m_in);
   StackParams p = {};
   p.descs = nullptr;
   p.one = lin_desc(h, x, y, dense, 0, 0);

@@ -190,3 +190,24 @@ def test_misaligned_inputs_and_outputs(coracle, cuda, xdt):
     for l, y in zip(layers, ys):
         yo, _, _ = oracle_on_device_values(coracle, l, x)
         assert maxrel(y.cpu().numpy(), yo) <= TOL_EXACT_INPUTS
+
+
+def test_widest_inputs(coracle, cuda):
+    """m_in up to 32768: with bf16 activations x stays on chip as bf16;
+    fp32 activations that no longer fit are refused (RSP_E_UNSUPPORTED),
+    not computed wrongly.  28000 channels still take fp32."""
+    rng = np.random.default_rng(3)
+    for n, f32_ok in ((28000, True), (32768, False)):
+        m, r = 256, 64
+        l = rsp.DecomposedLayer(torch.randn(m, n, device=cuda) * 0.02, torch.randn(m, r, device=cuda) * 0.1,
+                                torch.randn(r, n, device=cuda) * 0.1, rsp.SparsityPlan(0.3, r))
+        x32 = torch.from_numpy(random_x(rng, n)).to(cuda)
+        for x in (x32.to(torch.bfloat16), x32):
+            if x.dtype == torch.float32 and not f32_ok:
+                with pytest.raises(rsp.RspError) as e:
+                    l.forward(x)
+                assert e.value.status == RSP_E_UNSUPPORTED
+                continue
+            yo, kept, _ = oracle_on_device_values(coracle, l, x)
+            assert np.array_equal(l.selected(x), kept), (n, x.dtype)
+            assert maxrel(l.forward(x).cpu().numpy(), yo) <= TOL_EXACT_INPUTS, (n, x.dtype)
