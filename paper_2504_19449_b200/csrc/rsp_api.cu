@@ -1167,7 +1167,7 @@ rsp_status rsp_stack_create_spec(const rsp_stack_spec* spec, rsp_stack** out) {
   // Completion arrivals go to one counter per group (the slot of its first
   // linear): a dependent group polls one counter, not one per linear (each
   // poll is an L2 round trip).
-  // (pad1 = the arrivals its group's counter collects per launch: the CTA
+  // (garr = the arrivals its group's counter collects per launch: the CTA
   // that completes it publishes the group to the other ranks)
   std::vector<int> garr(count, 0);
   for (uint32_t i = 0; i < count; ++i) garr[gstart[i]] += descs[i].grid;

@@ -42,7 +42,7 @@ struct LinDesc {
 struct LinCtl {
   int flags, dep0, ndep, cta0, grid, slot;
   int aslot;  // slot whose word 0 counts this linear's completed CTAs (shared by its group)
-  int pad1;
+  int garr;   // arrivals that complete the group's counter in one launch (sum of its grids)
 };
 
 // Parameters of one launch of the stack kernel (rsp_kernels.cu).

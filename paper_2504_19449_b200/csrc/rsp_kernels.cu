@@ -925,7 +925,7 @@ __global__ void __launch_bounds__(kThreads, 1) stack_kernel(const StackParams P)
         // group to all ranks: one system-scope fence per group and rank
         // (measured: a fence in every CTA costs 3.6% more per token).
         const unsigned old = atom_add_acq_rel_gpu(slot_of(P, cl.aslot), 1u);
-        if (old + 1u == static_cast<unsigned>(cl.pad1)) {
+        if (old + 1u == static_cast<unsigned>(cl.garr)) {
           fence_acq_rel_sys();
           for (int p = 0; p < xr; ++p) red_relaxed_sys_add_u64(P.xctr[p] + cl.aslot, 1ull);
         }
