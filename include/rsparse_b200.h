@@ -320,6 +320,11 @@ size_t rsp_stack_exchange_words(uint32_t count);
 rsp_status rsp_stack_grids(const rsp_stack* s, uint32_t* grids, uint32_t count);
 rsp_status rsp_stack_create_spec(const rsp_stack_spec* spec, rsp_stack** out);
 rsp_status rsp_stack_launch(rsp_stack* s, void* stream);
+/* The same launch as a plain kernel launch instead of the stack's own CUDA
+ * graph: for callers that capture a larger graph around it (a graph launch
+ * inside a stream capture is not capturable everywhere), e.g. the stack
+ * launches and NCCL all-gathers of a row-sharded step. */
+rsp_status rsp_stack_launch_direct(rsp_stack* s, void* stream);
 /* The end-to-end stack path with host buffers: x_host (x_bytes) is copied to
  * the span of device memory covering all the stack's inputs (the x_devs given
  * at creation must lie in one contiguous allocation; x_bytes must equal that

@@ -28,7 +28,7 @@ EXPORTS = [
     "rsp_stack_launch_host", "rsp_stack_create_ops", "rsp_stack_create_spec", "rsp_rspl_read", "rsp_linear_load_rspl", "rsp_linear_save_rspl", "rsp_linear_components",
     "rsp_aggregate_scores", "rsp_select_components", "rsp_split_factors", "rsp_linear_set_components",
     "rsp_stack_exchange_words", "rsp_stack_grids", "rsp_ipc_alloc", "rsp_ipc_free", "rsp_ipc_export",
-    "rsp_ipc_open", "rsp_ipc_close",
+    "rsp_ipc_open", "rsp_ipc_close", "rsp_stack_launch_direct",
 ]
 RSP_IPC_HANDLE_BYTES = 64
 
@@ -156,6 +156,7 @@ def lib() -> ct.CDLL:
         "rsp_device_sm_count": (ct.c_int, [ct.c_int]),
         "rsp_stack_exchange_words": (ct.c_size_t, [ct.c_uint32]),
         "rsp_stack_grids": (ct.c_int, [vp, ct.POINTER(ct.c_uint32), ct.c_uint32]),
+        "rsp_stack_launch_direct": (ct.c_int, [vp, vp]),
         "rsp_ipc_alloc": (ct.c_int, [ct.c_int, ct.c_size_t, ct.POINTER(vp)]),
         "rsp_ipc_free": (ct.c_int, [vp]),
         "rsp_ipc_export": (ct.c_int, [vp, ct.c_char_p]),

@@ -147,6 +147,7 @@ struct rsp_stack {
   StackParams params = {};   // the captured launch (re-launched by the debug trace)
   int es = 2, grid = 1;
   bool x_bf16 = false;
+  bool pdl = true;
   size_t smem = 0;
   // contiguous device spans covering every x / y of the stack (host-buffer path)
   uint8_t* x_lo = nullptr;
@@ -1225,6 +1226,7 @@ rsp_status rsp_stack_create_spec(const rsp_stack_spec* spec, rsp_stack** out) {
     s->grid = grid;
     s->x_bf16 = xdt == RSP_BF16;
     s->smem = smem;
+    s->pdl = h0->pdl;
     const cudaError_t el = rsp::launch_stack(p, h0->es, xdt == RSP_BF16, grid, smem, cs, h0->pdl);
     cudaGraph_t graph = nullptr;
     const cudaError_t ec = cudaStreamEndCapture(cs, &graph);
@@ -1250,6 +1252,15 @@ rsp_status rsp_stack_launch(rsp_stack* s, void* stream) {
   if (!s) return fail(RSP_E_USAGE, "null stack");
   DeviceGuard g(s->device);
   RSP_CUDA(cudaGraphLaunch(s->exec, static_cast<cudaStream_t>(stream)));
+  return RSP_OK;
+}
+
+rsp_status rsp_stack_launch_direct(rsp_stack* s, void* stream) {
+  if (!s) return fail(RSP_E_USAGE, "null stack");
+  DeviceGuard g(s->device);
+  cudaError_t e = rsp::launch_stack(s->params, s->es, s->x_bf16, s->grid, s->smem, static_cast<cudaStream_t>(stream),
+                                    s->pdl);
+  if (e != cudaSuccess) return fail(RSP_E_CUDA, "stack launch: %s", cudaGetErrorString(e));
   return RSP_OK;
 }
 

@@ -474,8 +474,13 @@ class Stack:
             check(L.lib().rsp_stack_create_spec(ct.byref(sp), ct.byref(h)), "rsp_stack_create_spec")
         self._h = h
 
-    def launch(self, stream=None) -> None:
-        check(L.lib().rsp_stack_launch(self._h, _stream_ptr(stream)), "rsp_stack_launch")
+    def launch(self, stream=None, direct: bool = False) -> None:
+        """One token through the stack.  ``direct``: a plain kernel launch
+        instead of the stack's CUDA graph (capturable into a caller's graph)."""
+        if direct:
+            check(L.lib().rsp_stack_launch_direct(self._h, _stream_ptr(stream)), "rsp_stack_launch_direct")
+        else:
+            check(L.lib().rsp_stack_launch(self._h, _stream_ptr(stream)), "rsp_stack_launch")
 
     def info(self):
         return {"handle": self._h.value}

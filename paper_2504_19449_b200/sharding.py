@@ -168,8 +168,8 @@ class ShardedGroupStack:
     group (q/k/v, o, gate/up, down) instead of one launch per linear: each
     group's shards run side by side (layer.Stack), then one in-place NCCL
     all-gather per linear assembles the full y on every rank.  All of it is
-    captured into one CUDA graph when the runtime allows a graph launch
-    inside a capture, else replayed eagerly.  Needs even shards (every
+    captured into one CUDA graph (the stack kernels as plain launches,
+    rsp_stack_launch_direct), else replayed eagerly.  Needs even shards (every
     BASELINE shape at N <= 8); `ys[i]` are the full-length outputs."""
 
     def __init__(self, layers: Sequence[DecomposedLayer], xs, ys, gid: Sequence[int], stream=None, group=None,
@@ -205,7 +205,7 @@ class ShardedGroupStack:
 
     def _run(self):
         for st, idx, locs in self.groups:
-            st.launch(self.stream)
+            st.launch(self.stream, direct=True)  # capturable into the step's graph with the all-gathers
             if self.world > 1 or self.force:
                 for i, loc in zip(idx, locs):
                     dist.all_gather_into_tensor(self.ys[i], loc, group=self.group)
