@@ -530,34 +530,34 @@ class TokenParallelStack:
                              max_ctas=max(1, sms // self.B)) for b in range(self.B)]
         self.stream = stream or torch.cuda.current_stream(dev)
         self.side = [torch.cuda.Stream(device=dev) for _ in range(self.B)]
-        # each stack is already one CUDA graph; the fork/join around them is
-        # B+1 event records per step (a torch capture of graph launches is not
-        # supported by this runtime, and a failed capture leaves torch's CUDA
-        # RNG state unusable)
-        self.graph = None
+        # fork / B plain stack launches (rsp_stack_launch_direct) / join,
+        # captured once into one CUDA graph on a private stream
         with torch.cuda.stream(self.stream):
-            self._run()
+            self._run(self.stream)
             torch.cuda.synchronize()
+        cap = torch.cuda.Stream(device=dev)
+        cap.wait_stream(self.stream)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=cap):
+            self._run(cap)
+        self.graph = g
 
-    def _run(self):
+    def _run(self, root):
         fork = torch.cuda.Event()
-        fork.record(self.stream)
+        fork.record(root)
         joins = []
         for st, sd in zip(self.stacks, self.side):
             sd.wait_event(fork)
-            st.launch(sd)
+            st.launch(sd, direct=True)
             ev = torch.cuda.Event()
             ev.record(sd)
             joins.append(ev)
         for ev in joins:
-            self.stream.wait_event(ev)
+            root.wait_event(ev)
 
     def launch(self, stream=None) -> None:
-        if self.graph is not None:
+        with torch.cuda.stream(stream or self.stream):
             self.graph.replay()
-        else:
-            with torch.cuda.stream(self.stream):
-                self._run()
 
     def close(self) -> None:
         for st in self.stacks:
